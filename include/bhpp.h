@@ -1,0 +1,150 @@
+/*
+ * bhpp.h -- C ABI of the B200-native BHPP engine (libbhpp.so).
+ *
+ * The reference (`bipush`, pure Python + numpy/scipy) has no native boundary:
+ * its hot path is the Python API below, and its inner loops run in scipy's
+ * csr_matvec.  This ABI is what that Python API binds (ctypes, see
+ * paper_2312_06724_b200/_capi.py and INTEGRATION.md).  Plain pointers and
+ * sizes only; no torch types.  All functions are thread-safe (a graph handle
+ * serialises its own engine use with an internal mutex).
+ *
+ *   reference interface (file:line under pkg/src/bipush)    -> entry point
+ *   BipartiteGraph CSR core + u_step/v_step (bigraph.py:53-188) -> bh_graph_create
+ *   bhpp_query + topk (bhpp_query.py:160-218), batched          -> bh_query_batch
+ *   ss_push / selective_push / pi_push (push_engine.py:120-258) -> bh_push_run
+ *   power_iteration (push_engine.py:101-117), estimate_lambda   -> bh_power_iteration
+ *   topk (bhpp_query.py:206-218) on an arbitrary score vector   -> bh_topk
+ *
+ * Status codes: 0 ok; BH_EINVAL -> ValueError; BH_EUNFLUSHED -> ValueError
+ * ("unflushed ledger", push_engine.py:214-217); BH_ECUDA -> RuntimeError;
+ * BH_ENOMEM -> MemoryError.  bh_last_error() returns the calling thread's
+ * last message.
+ */
+#ifndef BHPP_H
+#define BHPP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BH_OK 0
+#define BH_EINVAL 1
+#define BH_EUNFLUSHED 2
+#define BH_ECUDA 3
+#define BH_ENOMEM 4
+
+#define BH_DTYPE_F64 0 /* fp64 storage, fp64 arithmetic                       */
+#define BH_DTYPE_F32 1 /* fp32 storage, fp64 row accumulation and control     */
+
+#define BH_JOB_BHPP 0      /* ss_push -> pi_push -> power iteration -> combine */
+#define BH_JOB_SS_PUSH 1   /* backward with budget switch (push_engine.py:145) */
+#define BH_JOB_SELECTIVE 2 /* backward without budget (push_engine.py:120)     */
+#define BH_JOB_PI_PUSH 3   /* forward from a flushed ledger (push_engine.py:194) */
+#define BH_JOB_POWER 4     /* truncated power series (push_engine.py:101)      */
+
+#define BH_TERM_THRESHOLD 0 /* "threshold-met" */
+#define BH_TERM_BUDGET 1    /* "budget-switch" */
+#define BH_TERM_DRAINED 2   /* "mass-drained"  */
+
+#define BH_PHASE_SELECTIVE 0  /* round_hook phase "selective"          */
+#define BH_PHASE_SEQUENTIAL 1 /* round_hook phase "sequential"         */
+#define BH_PHASE_FORWARD 2    /* round_hook phase "forward-selective"  */
+
+typedef struct bh_graph bh_graph;
+
+/* Per-query phase trace: the integer counters of bhpp_query.py:198-201 plus
+ * the exact-tie bookkeeping of the PI-Push budget test. */
+typedef struct bh_trace {
+    int64_t sel_b;       /* backward selective_rounds                     */
+    int64_t seq_b;       /* backward sequential_rounds                    */
+    int64_t n_p_b;       /* backward n_p (after SS-Push)                  */
+    int64_t sel_f;       /* forward selective_rounds                      */
+    int64_t pi_iters;    /* forward power_iterations                      */
+    int64_t n_p_f;       /* forward n_p (cumulative)                      */
+    double gamma;        /* forward gamma (frozen weighted mass at entry) */
+    int32_t term_b;      /* BH_TERM_*                                     */
+    int32_t term_f;      /* BH_TERM_*                                     */
+    int32_t tie_checks;  /* budget checks taken with A == U every round   */
+    int32_t tie_broke;   /* 1 if the forward phase ended at such a check  */
+    int32_t source;      /* U index of the query                          */
+    int32_t status;      /* 0 ok                                          */
+} bh_trace;
+
+typedef struct bh_query_params {
+    double alpha;          /* restart probability, (0, 1)                       */
+    double lam;            /* IndexMeta.lam                                      */
+    double eps_b;          /* backward share of epsilon                          */
+    double eps_f;          /* forward share of epsilon                           */
+    int32_t k;             /* top-k per query (0 = no top-k)                     */
+    int32_t exclude_query; /* drop the source from its own top-k                 */
+    int32_t want_scores;   /* also write the full score vector per query         */
+    int32_t slots;         /* query-block width B (0 = automatic)                */
+    int32_t on_device;     /* 1: all pointer arguments are device pointers       */
+    int32_t reserved;
+} bh_query_params;
+
+typedef struct bh_graph_info {
+    int64_t n_u, n_v, n_e;
+    int32_t dtype, device;
+    int64_t device_bytes;   /* graph store footprint                         */
+    int32_t units_u, units_v, split_rows_u, split_rows_v;
+    int32_t chunk_edges, reserved;
+} bh_graph_info;
+
+/* Called after every push round of slot 0 in bh_push_run (the reference's
+ * round_hook, push_engine.py:133,166,182,232).  Arrays are host copies valid
+ * only during the call; residue_v is always zero at a round boundary. */
+typedef void (*bh_round_hook)(void *user, int32_t phase, int64_t rounds, const double *residue_u,
+                              const double *estimate, int64_t n_p);
+
+/* ---- graph store (K-G) ---------------------------------------------------- */
+int bh_graph_create(int64_t n_u, int64_t n_v, int64_t n_e, const int64_t *u_indptr,
+                    const int32_t *u_indices, const double *u_weights, const int64_t *v_indptr,
+                    const int32_t *v_indices, const double *v_weights, const double *ws_u,
+                    const double *ws_v, int32_t device, int32_t dtype, bh_graph **out);
+void bh_graph_destroy(bh_graph *g);
+int bh_graph_get_info(const bh_graph *g, bh_graph_info *out);
+
+/* ---- batched SS-BI-PUSH query (bhpp_query + topk for many sources) -------- */
+/* sources[n_q] int32; tie_skip[n_q] nullable (continue through this many exact
+ * PI-Push budget ties before breaking; default 0 = exact-arithmetic outcome).
+ * Outputs (nullable unless noted): topk_idx/topk_score [n_q*k] (-1 / 0 padded),
+ * trace [n_q] (required), scores [n_q*n_u] (want_scores).  `stream` is a
+ * cudaStream_t (NULL = the engine's own stream).  With on_device == 0 the
+ * pointers are host memory and the copies happen inside the call. */
+int bh_query_batch(bh_graph *g, const bh_query_params *p, const int32_t *sources, int64_t n_q,
+                   const int32_t *tie_skip, int32_t *topk_idx, double *topk_score, bh_trace *trace,
+                   double *scores, void *stream);
+
+/* ---- single-query ledger kernels (ss_push / selective_push / pi_push / bhpp) */
+/* job: BH_JOB_*.  residue_u / estimate [n_u] and n_p are in/out host ledger
+ * arrays (read for BH_JOB_PI_PUSH, written by every job).  scores [n_u] gets
+ * the forward scores (PI_PUSH) or the BHPP vector (BHPP).  hook nullable. */
+int bh_push_run(bh_graph *g, int32_t job, int32_t source, double alpha, double lam, double eps_b,
+                double eps_f, int32_t tie_skip, double *residue_u, double *estimate, int64_t *n_p,
+                double *scores, bh_trace *trace, bh_round_hook hook, void *user);
+
+/* ---- power iteration (push_engine.py:101-117) over n_vec start vectors ---- */
+/* start, out: [n_vec * n_u] row-major host arrays; out = alpha * acc_t. */
+int bh_power_iteration(bh_graph *g, const double *start, int64_t n_vec, double alpha, int32_t t,
+                       double *out);
+
+/* ---- top-k of an arbitrary score vector (bhpp_query.py:206-218) ---------- */
+/* (score desc, index asc); exclude < 0 keeps every index.  Returns count via
+ * *out_count.  Host pointers. */
+int bh_topk(const double *scores, int64_t n, int64_t k, int64_t exclude, int64_t *out_idx,
+            double *out_score, int64_t *out_count);
+
+/* ---- misc ----------------------------------------------------------------- */
+const char *bh_last_error(void);
+int bh_version(void);
+/* Number of CUDA kernels this library launched in this process (for the
+ * bench's gpu_launches claim). */
+int64_t bh_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BHPP_H */

@@ -1,0 +1,205 @@
+"""ctypes binding of libbhpp.so (include/bhpp.h).
+
+This is the only way the package reaches the device.  There is no CPU
+fallback: if the library is missing or no CUDA device is usable, every compute
+call raises.  The library is built in-tree by ``python -m
+paper_2312_06724_b200.build`` (also ``__graft_entry__.build()``).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+import weakref
+from pathlib import Path
+
+import numpy as np
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libbhpp.so"
+
+BH_OK, BH_EINVAL, BH_EUNFLUSHED, BH_ECUDA, BH_ENOMEM = 0, 1, 2, 3, 4
+DTYPES = {"fp64": 0, "f64": 0, "float64": 0, "fp32": 1, "f32": 1, "float32": 1}
+JOB_BHPP, JOB_SS_PUSH, JOB_SELECTIVE, JOB_PI_PUSH, JOB_POWER = 0, 1, 2, 3, 4
+TERMINATIONS = ("threshold-met", "budget-switch", "mass-drained")
+PHASES = ("selective", "sequential", "forward-selective")
+
+EXPORTS = (
+    "bh_graph_create", "bh_graph_destroy", "bh_graph_get_info", "bh_query_batch", "bh_push_run",
+    "bh_power_iteration", "bh_topk", "bh_last_error", "bh_version", "bh_kernel_launches",
+)
+
+
+class Trace(C.Structure):
+    _fields_ = [
+        ("sel_b", C.c_int64), ("seq_b", C.c_int64), ("n_p_b", C.c_int64),
+        ("sel_f", C.c_int64), ("pi_iters", C.c_int64), ("n_p_f", C.c_int64),
+        ("gamma", C.c_double),
+        ("term_b", C.c_int32), ("term_f", C.c_int32),
+        ("tie_checks", C.c_int32), ("tie_broke", C.c_int32),
+        ("source", C.c_int32), ("status", C.c_int32),
+    ]
+
+
+TRACE_DTYPE = np.dtype([
+    ("sel_b", "<i8"), ("seq_b", "<i8"), ("n_p_b", "<i8"), ("sel_f", "<i8"), ("pi_iters", "<i8"),
+    ("n_p_f", "<i8"), ("gamma", "<f8"), ("term_b", "<i4"), ("term_f", "<i4"), ("tie_checks", "<i4"),
+    ("tie_broke", "<i4"), ("source", "<i4"), ("status", "<i4"),
+])
+assert TRACE_DTYPE.itemsize == C.sizeof(Trace)
+
+
+class QueryParams(C.Structure):
+    _fields_ = [
+        ("alpha", C.c_double), ("lam", C.c_double), ("eps_b", C.c_double), ("eps_f", C.c_double),
+        ("k", C.c_int32), ("exclude_query", C.c_int32), ("want_scores", C.c_int32),
+        ("slots", C.c_int32), ("on_device", C.c_int32), ("reserved", C.c_int32),
+    ]
+
+
+class GraphInfo(C.Structure):
+    _fields_ = [
+        ("n_u", C.c_int64), ("n_v", C.c_int64), ("n_e", C.c_int64),
+        ("dtype", C.c_int32), ("device", C.c_int32), ("device_bytes", C.c_int64),
+        ("units_u", C.c_int32), ("units_v", C.c_int32), ("split_rows_u", C.c_int32),
+        ("split_rows_v", C.c_int32), ("chunk_edges", C.c_int32), ("reserved", C.c_int32),
+    ]
+
+
+HOOK = C.CFUNCTYPE(None, C.c_void_p, C.c_int32, C.c_int64, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                   C.c_int64)
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    """Load libbhpp.so; raise loudly when it is absent (no CPU fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            raise RuntimeError(
+                f"CUDA extension {LIB_PATH} is not built; run `python -m paper_2312_06724_b200.build` "
+                "(there is no CPU fallback)")
+        L = C.CDLL(str(LIB_PATH))
+        P = C.c_void_p
+        L.bh_graph_create.restype = C.c_int
+        L.bh_graph_create.argtypes = [C.c_int64] * 3 + [P] * 8 + [C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]
+        L.bh_graph_destroy.restype = None
+        L.bh_graph_destroy.argtypes = [P]
+        L.bh_graph_get_info.restype = C.c_int
+        L.bh_graph_get_info.argtypes = [P, C.POINTER(GraphInfo)]
+        L.bh_query_batch.restype = C.c_int
+        L.bh_query_batch.argtypes = [P, C.POINTER(QueryParams), P, C.c_int64, P, P, P, P, P, P]
+        L.bh_push_run.restype = C.c_int
+        L.bh_push_run.argtypes = [P, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_double, C.c_double,
+                                  C.c_int32, P, P, P, P, P, HOOK, P]
+        L.bh_power_iteration.restype = C.c_int
+        L.bh_power_iteration.argtypes = [P, P, C.c_int64, C.c_double, C.c_int32, P]
+        L.bh_topk.restype = C.c_int
+        L.bh_topk.argtypes = [P, C.c_int64, C.c_int64, C.c_int64, P, P, P]
+        L.bh_last_error.restype = C.c_char_p
+        L.bh_last_error.argtypes = []
+        L.bh_version.restype = C.c_int
+        L.bh_kernel_launches.restype = C.c_int64
+        _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc == BH_OK:
+        return
+    msg = (lib().bh_last_error() or b"").decode("utf-8", "replace")
+    if rc in (BH_EINVAL, BH_EUNFLUSHED):
+        raise ValueError(msg)
+    if rc == BH_ENOMEM:
+        raise MemoryError(msg)
+    raise RuntimeError(f"bhpp CUDA engine error: {msg}")
+
+
+def ptr(a):
+    return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+def kernel_launches() -> int:
+    return int(lib().bh_kernel_launches())
+
+
+class DeviceGraph:
+    """Owning handle of a device graph store (bh_graph)."""
+
+    def __init__(self, g, dtype: str = "fp64", device: int = 0):
+        self.dtype = dtype
+        self.device = int(device)
+        self.n_u, self.n_v, self.n_e = int(g.u_count), int(g.v_count), int(g.edge_count)
+        arrs = [
+            np.ascontiguousarray(g.u_indptr, dtype=np.int64),
+            np.ascontiguousarray(g.u_indices, dtype=np.int32),
+            np.ascontiguousarray(g.u_weights, dtype=np.float64),
+            np.ascontiguousarray(g.v_indptr, dtype=np.int64),
+            np.ascontiguousarray(g.v_indices, dtype=np.int32),
+            np.ascontiguousarray(g.v_weights, dtype=np.float64),
+            np.ascontiguousarray(g.ws_u, dtype=np.float64),
+            np.ascontiguousarray(g.ws_v, dtype=np.float64),
+        ]
+        h = C.c_void_p()
+        check(lib().bh_graph_create(self.n_u, self.n_v, self.n_e, *[ptr(a) for a in arrs], self.device,
+                                    DTYPES[dtype], C.byref(h)))
+        self.h = h
+        self._fin = weakref.finalize(self, lib().bh_graph_destroy, h)
+
+    def info(self) -> dict:
+        gi = GraphInfo()
+        check(lib().bh_graph_get_info(self.h, C.byref(gi)))
+        return {f: getattr(gi, f) for f, _ in GraphInfo._fields_}
+
+    def close(self):
+        self._fin()
+
+
+_graph_cache: dict = {}
+_graph_lock = threading.Lock()
+
+
+def device_graph(g, dtype: str = "fp64", device: int = 0) -> DeviceGraph:
+    """The device store for graph object ``g`` (either package's BipartiteGraph),
+    built once per (graph, dtype, device) and freed with the graph."""
+    if dtype not in DTYPES:
+        raise ValueError(f"dtype must be one of {sorted(set(DTYPES))}")
+    key = (id(g), DTYPES[dtype], int(device))
+    with _graph_lock:
+        ent = _graph_cache.get(key)
+        if ent is not None and ent[0]() is g:
+            return ent[1]
+        dg = DeviceGraph(g, dtype, device)
+        try:
+            ref = weakref.ref(g, lambda _r, k=key: _graph_cache.pop(k, None))
+        except TypeError:  # not weak-referenceable: cache for the process lifetime
+            ref = (lambda obj=g: obj)
+        _graph_cache[key] = (ref, dg)
+        return dg
+
+
+def trace_dicts(tr) -> tuple[dict, dict, dict]:
+    """(backward, forward, engine-extra) dicts in the reference's key layout
+    (push_engine.py:185-191,251-258; bhpp_query.py:198-201)."""
+    back = {
+        "selective_rounds": int(tr["sel_b"]),
+        "sequential_rounds": int(tr["seq_b"]),
+        "power_iterations": 0,
+        "n_p": int(tr["n_p_b"]),
+        "terminated_by": TERMINATIONS[int(tr["term_b"])],
+    }
+    fwd = {
+        "selective_rounds": int(tr["sel_f"]),
+        "sequential_rounds": 0,
+        "power_iterations": int(tr["pi_iters"]),
+        "n_p": int(tr["n_p_f"]),
+        "gamma": float(tr["gamma"]),
+        "terminated_by": TERMINATIONS[int(tr["term_f"])],
+    }
+    extra = {"tie_checks": int(tr["tie_checks"]), "tie_broke": int(tr["tie_broke"])}
+    return back, fwd, extra

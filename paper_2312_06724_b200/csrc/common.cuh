@@ -1,0 +1,154 @@
+// common.cuh -- shared types of the BHPP engine (device graph store, slots, args).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/bhpp.h"
+
+namespace bh {
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct InvalidArg : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define BH_CUDA(call)                                                                      \
+    do {                                                                                   \
+        cudaError_t _e = (call);                                                           \
+        if (_e != cudaSuccess)                                                             \
+            throw ::bh::CudaError(std::string(#call) + ": " + cudaGetErrorString(_e) +     \
+                                  " (" __FILE__ ":" + std::to_string(__LINE__) + ")");     \
+    } while (0)
+
+void count_launch(int n = 1);
+
+// ---------------------------------------------------------------------------
+// Work schedule of one pull side (rows = this side's nodes).  A unit is either
+// up to 32 whole rows holding <= chunk edges, or one piece (<= chunk edges) of
+// a row longer than `chunk`; pieces write fp64 partial sums to scratch and a
+// finisher warp adds them in piece order, so every row sum is deterministic.
+struct Unit {
+    int32_t row0;   // first row
+    int32_t nrows;  // rows in this unit (1 for a piece)
+    int64_t e0;     // first edge
+    int64_t e1;     // one past the last edge
+    int32_t piece;  // global piece index, -1 for whole rows
+    int32_t pad;
+};
+
+struct SplitRow {
+    int32_t row;
+    int32_t first_piece;
+    int32_t n_pieces;
+    int32_t pad;
+};
+
+struct Side {
+    int64_t n_rows = 0;
+    int64_t *indptr = nullptr;   // [n_rows + 1]
+    int32_t *indices = nullptr;  // [E] column (other side) index
+    void *vals = nullptr;        // [E] T, w / ws(row)
+    int32_t *deg = nullptr;      // [n_rows]
+    Unit *units = nullptr;
+    SplitRow *splits = nullptr;
+    int32_t n_units = 0, n_splits = 0, n_pieces = 0;
+};
+
+}  // namespace bh
+
+struct bh_graph {
+    int device = 0;
+    int dtype = BH_DTYPE_F64;
+    int64_t n_u = 0, n_v = 0, n_e = 0;
+    int32_t chunk = 128;
+    bh::Side U;  // rows u: cols v, vals w/ws(u)   (u_step, bigraph.py:148-155)
+    bh::Side V;  // rows v: cols u, vals w/ws(v)   (v_step, bigraph.py:157-164)
+    double *ws_u = nullptr;
+    double *inv_ws_u = nullptr;
+    int64_t device_bytes = 0;
+    std::mutex mu;
+    void *engines = nullptr;  // engine cache (engine.cu)
+};
+
+namespace bh {
+
+// ---------------------------------------------------------------------------
+// Per-slot round op: what K1 (prep), K2 (V pull) and K3 (U pull) do for this
+// slot in the coming round.
+enum Op : int32_t {
+    OP_IDLE = 0,
+    OP_BSEL_INIT = 1,  // ledger := e_src, then a selective round at eps_b
+    OP_BSEL = 2,       // selective round at eps_b           (push_engine.py:165)
+    OP_SEQ = 3,        // sequential round, threshold 0      (push_engine.py:181)
+    OP_FENTRY = 4,     // gamma at entry + forward round     (push_engine.py:222,231)
+    OP_FSEL = 5,       // forward round at theta_i           (push_engine.py:231)
+    OP_PIENTRY = 6,    // y0 := residue * ysc, first power iteration
+    OP_PIENTRY0 = 7,   // y0 only (t == 0)
+    OP_PI = 8,         // power iteration
+};
+
+enum Phase : int32_t { PH_IDLE = 0, PH_BSEL, PH_SEQ, PH_FWD, PH_PI, PH_DONE };
+
+// Slot state owned by the control kernel (K4).
+struct Slot {
+    int32_t op;        // op of the next round
+    int32_t job;       // BH_JOB_*
+    int32_t qidx;      // query index in the batch, -1 if idle
+    int32_t src;       // source / target U index
+    int32_t phase;     // Phase
+    int32_t term_b, term_f;
+    int32_t all_full;  // every forward round so far pushed all of U
+    int32_t tie_checks, tie_skip, tie_broke;
+    int32_t pi_t, pi_done;
+    int32_t last_phase;   // BH_PHASE_* of the last executed push round (-1 none)
+    int32_t budget;       // SS-Push budget enabled
+    int32_t push_seq;     // incremented after every push round (round_hook trigger)
+    int64_t n_p, n_p_entry, n_p_b;
+    int64_t sel_b, seq_b, sel_f;
+    int64_t last_rounds;  // counter reported to round_hook
+    double gamma;
+    double ws_q, inv_ws_q;  // ws(source), 1 / ws(source)
+    double ysc;             // y0 = residue * ysc in power iteration
+    double theta_c;         // eps_f / lam
+    double eps_b, eps_f;
+};
+
+// Finished-query record written by K4 for the finalize kernels.
+struct Finish {
+    int32_t qidx, src, job, has_pi;
+    double inv_ws_q;
+    bh_trace trace;
+};
+
+// Deterministic per-round reductions: one row per producing block.
+struct Partials {
+    int64_t *cnt;    // [rows][B] |A| (K1)
+    int64_t *np_u;   // [rows][B] sum deg(A) (K1)
+    double *gamma;   // [rows][B] sum w_ratio * r (K1, FENTRY)
+    int64_t *np_v;   // [rows][B] sum deg over r_v > 0 (K2)
+    int32_t *any;    // [rows][B] any(r > threshold) (K3)
+    double *sum;     // [rows][B] sum r (K3, backward)
+    double *wsum;    // [rows][B] sum w_ratio * r (K3, forward)
+    int rows_k1, rows_k2, rows_k3;  // valid rows (set by host per launch geometry)
+};
+
+struct Control {
+    int32_t active;    // slots still busy or queries left
+    int32_t next_q;    // next query index to start
+    int32_t n_q;       // queries in this batch
+    int32_t n_fin;     // slots finishing this round
+    int32_t fin_slots[256];
+};
+
+constexpr int MAX_B = 128;
+
+}  // namespace bh

@@ -1,0 +1,259 @@
+// control.cuh -- K4: per-query state machine, one thread per slot.
+//
+// Mirrors the loop bodies of ss_push (push_engine.py:164-184), selective_push
+// (131-142) and pi_push (230-250) plus required_iterations (85-98), evaluated
+// on device in fp64 after every round so no host round trip is needed.  Also
+// refills finished slots from the query queue in slot order (deterministic).
+#pragma once
+
+#include "kernels.cuh"
+
+namespace bh {
+
+struct ControlArgs {
+    Slot *slots;
+    Finish *fin;
+    Control *ctl;
+    Partials part;
+    const int32_t *sources;   // [n_q]
+    const int32_t *tie_skip;  // [n_q] or null
+    const double *ws_u;
+    int64_t n_u;
+    double alpha, lam, eps_b, eps_f;
+    double budget_scale;  // 2 |E|
+    double log_decay;     // log(1 / (1 - alpha))
+    int32_t job;
+    int32_t power_t;      // BH_JOB_POWER depth
+    int64_t init_np;      // BH_JOB_PI_PUSH seed ledger n_p
+    int32_t first;        // 1: no round ran yet, only assign queries
+    int32_t B;
+};
+
+__device__ __forceinline__ int32_t required_iterations_dev(double alpha, double eps_f, double mass) {
+    if (mass <= 0) return 0;
+    double x = ceil(log(mass / eps_f) / log(1.0 / (1.0 - alpha))) - 1.0;
+    return x > 0 ? (int32_t)x : 0;
+}
+
+__device__ void slot_start(Slot &sl, const ControlArgs &a, int32_t q) {
+    sl = Slot{};
+    sl.qidx = q;
+    sl.job = a.job;
+    sl.src = a.sources[q];
+    sl.tie_skip = a.tie_skip ? a.tie_skip[q] : 0;
+    sl.ws_q = a.ws_u[sl.src];
+    sl.inv_ws_q = 1.0 / sl.ws_q;
+    sl.eps_b = a.eps_b;
+    sl.eps_f = a.eps_f;
+    sl.theta_c = a.eps_f / a.lam;
+    sl.ysc = sl.inv_ws_q;
+    sl.last_phase = -1;
+    sl.budget = a.job != BH_JOB_SELECTIVE;
+    switch (a.job) {
+        case BH_JOB_PI_PUSH:
+            sl.n_p = a.init_np;
+            sl.n_p_entry = a.init_np;
+            sl.all_full = 1;
+            sl.phase = PH_FWD;
+            sl.op = OP_FENTRY;
+            break;
+        case BH_JOB_POWER:
+            sl.phase = PH_PI;
+            sl.pi_t = a.power_t;
+            sl.ysc = 1.0;
+            sl.op = a.power_t > 0 ? OP_PIENTRY : OP_PIENTRY0;
+            break;
+        default:
+            sl.phase = PH_BSEL;
+            sl.op = OP_BSEL_INIT;
+            break;
+    }
+}
+
+__device__ void slot_finish(Slot &sl, Finish &f, bool has_pi) {
+    f.qidx = sl.qidx;
+    f.src = sl.src;
+    f.job = sl.job;
+    f.has_pi = has_pi;
+    f.inv_ws_q = sl.inv_ws_q;
+    bh_trace &t = f.trace;
+    t.sel_b = sl.sel_b;
+    t.seq_b = sl.seq_b;
+    t.n_p_b = sl.n_p_b;
+    t.sel_f = sl.sel_f;
+    t.pi_iters = sl.pi_t;
+    t.n_p_f = sl.n_p;
+    t.gamma = sl.gamma;
+    t.term_b = sl.term_b;
+    t.term_f = sl.term_f;
+    t.tie_checks = sl.tie_checks;
+    t.tie_broke = sl.tie_broke;
+    t.source = sl.src;
+    t.status = 0;
+    sl.phase = PH_DONE;
+    sl.op = OP_IDLE;
+}
+
+__global__ void k_control(ControlArgs a) {
+    __shared__ int32_t s_free[MAX_B];
+    __shared__ int32_t s_fin[MAX_B];
+    __shared__ int32_t s_assign[MAX_B];
+    __shared__ int32_t s_busy;
+    const int s = threadIdx.x;
+    const int B = a.B;
+    Control *ctl = a.ctl;
+    if (ctl->active == 0 && !a.first) {
+        if (s == 0) ctl->n_fin = 0;
+        return;
+    }
+    if (s == 0) s_busy = 0;
+    Slot sl;
+    bool fin = false;
+    if (s < B) {
+        sl = a.slots[s];
+        const int op = a.first ? OP_IDLE : sl.op;
+        if (op_is_push(op)) {
+            sl.push_seq++;
+            int64_t cnt = 0, npu = 0, npv = 0;
+            int32_t any = 0;
+            double gam = 0.0, sum = 0.0;
+            for (int r = 0; r < a.part.rows_k1; r++) {
+                cnt += a.part.cnt[r * B + s];
+                npu += a.part.np_u[r * B + s];
+                gam += a.part.gamma[r * B + s];
+            }
+            for (int r = 0; r < a.part.rows_k2; r++) npv += a.part.np_v[r * B + s];
+            for (int r = 0; r < a.part.rows_k3; r++) {
+                any |= a.part.any[r * B + s];
+                sum += a.part.sum[r * B + s];
+            }
+            const int64_t worked = cnt > 0;
+            sl.n_p += npu + npv;
+            bool end_backward = false;
+            if (op == OP_BSEL_INIT || op == OP_BSEL) {
+                sl.sel_b += worked;
+                sl.last_phase = BH_PHASE_SELECTIVE;
+                sl.last_rounds = sl.sel_b;
+                if (!any) {
+                    sl.term_b = BH_TERM_THRESHOLD;
+                    end_backward = true;
+                } else if (!sl.budget) {
+                    sl.op = OP_BSEL;
+                } else if (sum <= 0.0) {
+                    sl.term_b = BH_TERM_DRAINED;
+                    end_backward = true;
+                } else if ((double)sl.n_p >= a.budget_scale * (log(1.0 / sum) / a.log_decay)) {
+                    if (sum > sl.eps_b) {  // any is true here
+                        sl.op = OP_SEQ;
+                        sl.phase = PH_SEQ;
+                    } else {
+                        sl.term_b = BH_TERM_BUDGET;
+                        end_backward = true;
+                    }
+                } else {
+                    sl.op = OP_BSEL;
+                }
+            } else if (op == OP_SEQ) {
+                sl.seq_b += worked;
+                sl.last_phase = BH_PHASE_SEQUENTIAL;
+                sl.last_rounds = sl.seq_b;
+                if (any && sum > sl.eps_b) {
+                    sl.op = OP_SEQ;
+                } else {
+                    sl.term_b = BH_TERM_BUDGET;
+                    end_backward = true;
+                }
+            } else {  // forward round
+                if (op == OP_FENTRY) sl.gamma = gam;
+                sl.sel_f += worked;
+                sl.last_phase = BH_PHASE_FORWARD;
+                sl.last_rounds = sl.sel_f;
+                if (cnt != a.n_u) sl.all_full = 0;
+                if (!any) {
+                    sl.term_f = BH_TERM_THRESHOLD;
+                    sl.pi_t = 0;
+                    fin = true;
+                    slot_finish(sl, a.fin[s], false);
+                } else if (sum <= 0.0) {
+                    sl.term_f = BH_TERM_DRAINED;
+                    sl.pi_t = 0;
+                    fin = true;
+                    slot_finish(sl, a.fin[s], false);
+                } else {
+                    bool brk;
+                    if (sl.all_full) {
+                        // Exact tie: n_p - n_p_entry == 2|E| k == budget in exact
+                        // arithmetic.  Break, unless the
+                        // caller asked to replay a reference run that continued.
+                        sl.tie_checks++;
+                        brk = sl.tie_checks > sl.tie_skip;
+                        if (brk) sl.tie_broke = 1;
+                    } else {
+                        const double budget = a.budget_scale * (log(sl.gamma / sum) / a.log_decay);
+                        brk = (double)(sl.n_p - sl.n_p_entry) >= budget;
+                    }
+                    if (brk) {
+                        sl.term_f = BH_TERM_BUDGET;
+                        sl.pi_t = required_iterations_dev(a.alpha, sl.eps_f, sum);
+                        sl.pi_done = 0;
+                        sl.phase = PH_PI;
+                        sl.op = sl.pi_t > 0 ? OP_PIENTRY : OP_PIENTRY0;
+                    } else {
+                        sl.op = OP_FSEL;
+                    }
+                }
+            }
+            if (end_backward) {
+                sl.n_p_b = sl.n_p;
+                if (sl.job == BH_JOB_SS_PUSH || sl.job == BH_JOB_SELECTIVE) {
+                    fin = true;
+                    slot_finish(sl, a.fin[s], false);
+                } else {
+                    sl.phase = PH_FWD;
+                    sl.op = OP_FENTRY;
+                    sl.n_p_entry = sl.n_p;
+                    sl.all_full = 1;
+                    sl.tie_checks = 0;
+                }
+            }
+        } else if (op == OP_PIENTRY0) {
+            sl.last_phase = -1;
+            fin = true;
+            slot_finish(sl, a.fin[s], true);
+        } else if (op == OP_PIENTRY || op == OP_PI) {
+            sl.last_phase = -1;
+            sl.pi_done++;
+            if (sl.pi_done >= sl.pi_t) {
+                fin = true;
+                slot_finish(sl, a.fin[s], true);
+            } else {
+                sl.op = OP_PI;
+            }
+        }
+        s_fin[s] = fin;
+        s_free[s] = fin || sl.op == OP_IDLE;
+    }
+    __syncthreads();
+    if (s == 0) {
+        int32_t next = ctl->next_q;
+        int32_t nf = 0;
+        for (int i = 0; i < B; i++) {
+            s_assign[i] = -1;
+            if (s_free[i] && next < ctl->n_q) s_assign[i] = next++;
+            if (s_fin[i]) ctl->fin_slots[nf++] = i;
+        }
+        ctl->next_q = next;
+        ctl->n_fin = nf;
+    }
+    __syncthreads();
+    if (s < B) {
+        if (s_assign[s] >= 0) slot_start(sl, a, s_assign[s]);
+        else if (s_free[s]) sl.qidx = -1;
+        a.slots[s] = sl;
+        if (sl.op != OP_IDLE) atomicOr(&s_busy, 1);
+    }
+    __syncthreads();
+    if (s == 0) ctl->active = s_busy;
+}
+
+}  // namespace bh

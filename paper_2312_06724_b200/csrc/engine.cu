@@ -1,0 +1,758 @@
+// engine.cu -- the slot engine and the C ABI (include/bhpp.h).
+//
+// An Engine<T, B> owns the device state of B query slots (node-major,
+// slot-minor) and drives rounds: K1 prep -> K2/K2b V pull -> K3/K3b U pull ->
+// K4 control -> K5/K6 finalize + top-k.  Query control lives on the device
+// (K4), so the host only launches rounds and polls one flag every few rounds;
+// finished slots are refilled from the batch queue inside K4.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+
+#include "control.cuh"
+#include "kernels.cuh"
+#include "topk.cuh"
+
+namespace bh {
+
+bh_graph *graph_create(int64_t, int64_t, int64_t, const int64_t *, const int32_t *, const double *,
+                       const int64_t *, const int32_t *, const double *, const double *, const double *,
+                       int32_t, int32_t);
+void graph_free_arrays(bh_graph *g);
+
+static std::atomic<int64_t> g_launches{0};
+void count_launch(int n) { g_launches += n; }
+
+static thread_local std::string t_err;
+
+template <typename X>
+static X *dalloc(size_t count) {
+    void *p = nullptr;
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(1, count * sizeof(X)));
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        throw std::bad_alloc();
+    }
+    return (X *)p;
+}
+
+// ---------------------------------------------------------------------------
+// small utility kernels
+template <typename T>
+__global__ void k_col_get(const T *X, int B, int s, int64_t n, double *out) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x)
+        out[u] = (double)X[u * B + s];
+}
+template <typename T>
+__global__ void k_col_set(T *X, int B, int s, int64_t n, const double *in) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x)
+        X[u * B + s] = (T)in[u];
+}
+
+static int grid1d(int64_t n, int threads = 256, int cap = 148 * 16) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, cap));
+}
+
+// ---------------------------------------------------------------------------
+struct RunSpec {
+    int32_t job = BH_JOB_BHPP;
+    int64_t n_q = 0;
+    const int32_t *sources = nullptr;  // device
+    const int32_t *tie = nullptr;      // device or null
+    double alpha = 0.15, lam = 1.0, eps_b = 1e-6, eps_f = 1e-6;
+    int32_t power_t = 0;
+    int64_t init_np = 0;
+    const double *x0 = nullptr;          // device [n_q][n_u] (POWER)
+    const double *ledger_r = nullptr;    // device [n_u] (PI_PUSH, slot 0)
+    const double *ledger_est = nullptr;  // device [n_u] (PI_PUSH, slot 0)
+    int32_t k = 0, exclude = 0, want_scores = 0;
+    int32_t *topk_idx = nullptr;  // device
+    double *topk_score = nullptr;
+    bh_trace *trace = nullptr;
+    double *scores = nullptr;
+    bh_round_hook hook = nullptr;
+    void *hook_user = nullptr;
+};
+
+struct EngineBase {
+    virtual ~EngineBase() = default;
+    virtual void run(const RunSpec &rs, cudaStream_t st) = 0;
+    virtual void read_ledger(int s, double *r_u_dev, double *est_dev, cudaStream_t st) = 0;
+    virtual void slot_state(int s, Slot *out, cudaStream_t st) = 0;
+    int nslots = 0;
+    int k_cap = 0;
+};
+
+template <typename T, int B>
+struct Engine final : EngineBase {
+    bh_graph *g;
+    T *R = nullptr, *P = nullptr, *XV = nullptr;
+    double *EST = nullptr, *OUTS = nullptr;
+    Slot *slots = nullptr;
+    Finish *fins = nullptr;
+    Control *ctl = nullptr;
+    Control *h_ctl = nullptr;
+    Partials part{};
+    double *scratch = nullptr;
+    uint64_t *cand_key = nullptr;
+    int64_t *cand_idx = nullptr;
+    double *hook_r = nullptr, *hook_est = nullptr;
+    int fin_chunk = 4096, n_chunks = 1;
+    int grid_prep = 1, grid_pv = 1, grid_pu = 1, grid_fv = 1, grid_fu = 1, grid_k5 = 1;
+
+    explicit Engine(bh_graph *graph) : g(graph) {
+        this->nslots = B;
+        const int64_t nu = g->n_u, nv = g->n_v;
+        R = dalloc<T>(nu * B);
+        P = dalloc<T>(nu * B);
+        XV = dalloc<T>(nv * B);
+        EST = dalloc<double>(nu * B);
+        OUTS = dalloc<double>(nu * B);
+        slots = dalloc<Slot>(B);
+        fins = dalloc<Finish>(B);
+        ctl = dalloc<Control>(1);
+        BH_CUDA(cudaMallocHost(&h_ctl, sizeof(Control)));
+        BH_CUDA(cudaMemset(R, 0, nu * B * sizeof(T)));
+        BH_CUDA(cudaMemset(P, 0, nu * B * sizeof(T)));
+        BH_CUDA(cudaMemset(XV, 0, nv * B * sizeof(T)));
+        BH_CUDA(cudaMemset(EST, 0, nu * B * sizeof(double)));
+        int dev_sms = 148;
+        BH_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, g->device));
+        int occ_v = 1, occ_u = 1;
+        BH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_v, k_pull<B, T, SIDE_V>, PULL_THREADS, 0));
+        BH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_u, k_pull<B, T, SIDE_U>, PULL_THREADS, 0));
+        occ_v = std::max(1, occ_v);
+        occ_u = std::max(1, occ_u);
+        grid_pv = (int)std::max<int64_t>(1, std::min<int64_t>((g->V.n_units + PULL_WARPS - 1) / PULL_WARPS, (int64_t)occ_v * dev_sms));
+        grid_pu = (int)std::max<int64_t>(1, std::min<int64_t>((g->U.n_units + PULL_WARPS - 1) / PULL_WARPS, (int64_t)occ_u * dev_sms));
+        grid_fv = (int)std::max<int64_t>(1, std::min<int64_t>((g->V.n_splits + PULL_WARPS - 1) / PULL_WARPS, 4 * dev_sms));
+        grid_fu = (int)std::max<int64_t>(1, std::min<int64_t>((g->U.n_splits + PULL_WARPS - 1) / PULL_WARPS, 4 * dev_sms));
+        grid_prep = grid1d(nu * B, PREP_THREADS, 8 * dev_sms);
+        n_chunks = (int)((nu + fin_chunk - 1) / fin_chunk);
+        grid_k5 = (int)std::min<int64_t>((int64_t)n_chunks * std::min(B, 8), 8 * dev_sms);
+        const int rows = std::max({grid_prep, grid_pv + grid_fv, grid_pu + grid_fu});
+        part.cnt = dalloc<int64_t>((size_t)rows * B);
+        part.np_u = dalloc<int64_t>((size_t)rows * B);
+        part.gamma = dalloc<double>((size_t)rows * B);
+        part.np_v = dalloc<int64_t>((size_t)rows * B);
+        part.any = dalloc<int32_t>((size_t)rows * B);
+        part.sum = dalloc<double>((size_t)rows * B);
+        part.wsum = part.sum;
+        part.rows_k1 = grid_prep;
+        part.rows_k2 = grid_pv + (g->V.n_splits ? grid_fv : 0);
+        part.rows_k3 = grid_pu + (g->U.n_splits ? grid_fu : 0);
+        BH_CUDA(cudaMemset(part.np_v, 0, (size_t)rows * B * sizeof(int64_t)));
+        BH_CUDA(cudaMemset(part.any, 0, (size_t)rows * B * sizeof(int32_t)));
+        BH_CUDA(cudaMemset(part.sum, 0, (size_t)rows * B * sizeof(double)));
+        const int64_t pieces = std::max<int64_t>(1, std::max(g->U.n_pieces, g->V.n_pieces));
+        scratch = dalloc<double>((size_t)pieces * B);
+        hook_r = dalloc<double>(nu);
+        hook_est = dalloc<double>(nu);
+    }
+
+    ~Engine() override {
+        cudaFree(R); cudaFree(P); cudaFree(XV); cudaFree(EST); cudaFree(OUTS);
+        cudaFree(slots); cudaFree(fins); cudaFree(ctl); cudaFreeHost(h_ctl);
+        cudaFree(part.cnt); cudaFree(part.np_u); cudaFree(part.gamma); cudaFree(part.np_v);
+        cudaFree(part.any); cudaFree(part.sum);
+        cudaFree(scratch); cudaFree(cand_key); cudaFree(cand_idx);
+        cudaFree(hook_r); cudaFree(hook_est);
+    }
+
+    void ensure_cand(int k) {
+        if (k <= k_cap) return;
+        cudaFree(cand_key);
+        cudaFree(cand_idx);
+        cand_key = dalloc<uint64_t>((size_t)B * n_chunks * k);
+        cand_idx = dalloc<int64_t>((size_t)B * n_chunks * k);
+        k_cap = k;
+    }
+
+    PullArgs<T> pull_args(int side) {
+        PullArgs<T> a{};
+        const Side &sd = side == SIDE_V ? g->V : g->U;
+        a.indptr = sd.indptr;
+        a.indices = sd.indices;
+        a.vals = (const T *)sd.vals;
+        a.units = sd.units;
+        a.n_units = sd.n_units;
+        a.splits = sd.splits;
+        a.n_splits = sd.n_splits;
+        a.scratch = scratch;
+        a.X = side == SIDE_V ? P : XV;
+        a.Y = side == SIDE_V ? XV : R;
+        a.P = P;
+        a.ws_u = g->ws_u;
+        a.inv_ws_u = g->inv_ws_u;
+        a.slots = slots;
+        a.active = &ctl->active;
+        a.part = part;
+        return a;
+    }
+
+    void launch_round(const RunSpec &rs, const ControlArgs &ca, const FinalArgs<T> &fa, cudaStream_t st) {
+        PrepArgs<T> pa{};
+        pa.n_u = g->n_u;
+        pa.R = R;
+        pa.P = P;
+        pa.EST = EST;
+        pa.deg_u = g->U.deg;
+        pa.ws_u = g->ws_u;
+        pa.inv_ws_u = g->inv_ws_u;
+        pa.x0 = rs.x0;
+        pa.slots = slots;
+        pa.active = &ctl->active;
+        pa.part = part;
+        pa.alpha = rs.alpha;
+        k_prep<B, T><<<grid_prep, PREP_THREADS, 0, st>>>(pa);
+
+        PullArgs<T> av = pull_args(SIDE_V);
+        av.one_minus_alpha = 1.0 - rs.alpha;
+        av.part_row0 = 0;
+        k_pull<B, T, SIDE_V><<<grid_pv, PULL_THREADS, 0, st>>>(av);
+        int launches = 2;
+        if (g->V.n_splits) {
+            av.part_row0 = grid_pv;
+            k_pull_finish<B, T, SIDE_V><<<grid_fv, PULL_THREADS, 0, st>>>(av);
+            launches++;
+        }
+        PullArgs<T> au = pull_args(SIDE_U);
+        au.one_minus_alpha = 1.0 - rs.alpha;
+        au.part_row0 = 0;
+        k_pull<B, T, SIDE_U><<<grid_pu, PULL_THREADS, 0, st>>>(au);
+        launches++;
+        if (g->U.n_splits) {
+            au.part_row0 = grid_pu;
+            k_pull_finish<B, T, SIDE_U><<<grid_fu, PULL_THREADS, 0, st>>>(au);
+            launches++;
+        }
+        k_control<<<1, std::max(32, B), 0, st>>>(ca);
+        k_finalize<T><<<grid_k5, TOPK_THREADS, 0, st>>>(fa);
+        k_topk_merge<T><<<B, TOPK_THREADS, 0, st>>>(fa);
+        launches += 3;
+        count_launch(launches);
+        BH_CUDA(cudaGetLastError());
+    }
+
+    void run(const RunSpec &rs, cudaStream_t st) override {
+        if (rs.k > TOPK_MAX) throw InvalidArg("k exceeds the device top-k limit (1024) of bh_query_batch");
+        if (rs.k > 0) ensure_cand(rs.k);
+        BH_CUDA(cudaMemsetAsync(slots, 0, sizeof(Slot) * B, st));
+        Control c0{};
+        c0.active = 1;
+        c0.next_q = 0;
+        c0.n_q = (int32_t)rs.n_q;
+        c0.n_fin = 0;
+        *h_ctl = c0;
+        BH_CUDA(cudaMemcpyAsync(ctl, h_ctl, sizeof(Control), cudaMemcpyHostToDevice, st));
+
+        ControlArgs ca{};
+        ca.slots = slots;
+        ca.fin = fins;
+        ca.ctl = ctl;
+        ca.part = part;
+        ca.sources = rs.sources;
+        ca.tie_skip = rs.tie;
+        ca.ws_u = g->ws_u;
+        ca.n_u = g->n_u;
+        ca.alpha = rs.alpha;
+        ca.lam = rs.lam;
+        ca.eps_b = rs.eps_b;
+        ca.eps_f = rs.eps_f;
+        ca.budget_scale = 2.0 * (double)g->n_e;
+        ca.log_decay = std::log(1.0 / (1.0 - rs.alpha));
+        ca.job = rs.job;
+        ca.power_t = rs.power_t;
+        ca.init_np = rs.init_np;
+        ca.B = B;
+        ca.first = 1;
+        k_control<<<1, std::max(32, B), 0, st>>>(ca);
+        count_launch();
+        BH_CUDA(cudaGetLastError());
+        ca.first = 0;
+        if (rs.job == BH_JOB_PI_PUSH) {  // seed ledger into slot 0 (query 0 -> slot 0)
+            k_col_set<T><<<grid1d(g->n_u), 256, 0, st>>>(R, B, 0, g->n_u, rs.ledger_r);
+            k_col_set<double><<<grid1d(g->n_u), 256, 0, st>>>(EST, B, 0, g->n_u, rs.ledger_est);
+            count_launch(2);
+        }
+
+        FinalArgs<T> fa{};
+        fa.n_u = g->n_u;
+        fa.B = B;
+        fa.k = rs.k;
+        fa.exclude = rs.exclude;
+        fa.want_scores = rs.want_scores;
+        fa.chunk = fin_chunk;
+        fa.n_chunks = n_chunks;
+        fa.EST = EST;
+        fa.P = P;
+        fa.ws_u = g->ws_u;
+        fa.alpha = rs.alpha;
+        fa.fin = fins;
+        fa.ctl = ctl;
+        fa.outs = OUTS;
+        fa.out_scores = rs.scores;
+        fa.cand_key = cand_key;
+        fa.cand_idx = cand_idx;
+        fa.topk_idx = rs.topk_idx;
+        fa.topk_score = rs.topk_score;
+        fa.trace = rs.trace;
+
+        const int poll = rs.hook ? 1 : 8;
+        int32_t last_seq = 0;
+        std::vector<double> hr, he;
+        const int64_t max_rounds = 100000000;
+        for (int64_t round = 0; round < max_rounds;) {
+            for (int i = 0; i < poll; i++, round++) {
+                launch_round(rs, ca, fa, st);
+                if (rs.hook) {
+                    Slot s0;
+                    slot_state(0, &s0, st);
+                    if (s0.push_seq != last_seq && s0.last_phase >= 0) {
+                        last_seq = s0.push_seq;
+                        hr.resize(g->n_u);
+                        he.resize(g->n_u);
+                        read_ledger(0, hook_r, hook_est, st);
+                        BH_CUDA(cudaMemcpyAsync(hr.data(), hook_r, g->n_u * sizeof(double), cudaMemcpyDeviceToHost, st));
+                        BH_CUDA(cudaMemcpyAsync(he.data(), hook_est, g->n_u * sizeof(double), cudaMemcpyDeviceToHost, st));
+                        BH_CUDA(cudaStreamSynchronize(st));
+                        rs.hook(rs.hook_user, s0.last_phase, s0.last_rounds, hr.data(), he.data(), s0.n_p);
+                    }
+                }
+            }
+            BH_CUDA(cudaMemcpyAsync(h_ctl, ctl, sizeof(Control), cudaMemcpyDeviceToHost, st));
+            BH_CUDA(cudaStreamSynchronize(st));
+            if (!h_ctl->active && h_ctl->n_fin == 0) return;
+        }
+        throw CudaError("query batch did not terminate");
+    }
+
+    void read_ledger(int s, double *r_dev, double *est_dev, cudaStream_t st) override {
+        k_col_get<T><<<grid1d(g->n_u), 256, 0, st>>>(R, B, s, g->n_u, r_dev);
+        k_col_get<double><<<grid1d(g->n_u), 256, 0, st>>>(EST, B, s, g->n_u, est_dev);
+        count_launch(2);
+        BH_CUDA(cudaGetLastError());
+    }
+
+    void slot_state(int s, Slot *out, cudaStream_t st) override {
+        BH_CUDA(cudaMemcpyAsync(out, slots + s, sizeof(Slot), cudaMemcpyDeviceToHost, st));
+        BH_CUDA(cudaStreamSynchronize(st));
+    }
+};
+
+// ---------------------------------------------------------------------------
+struct EngineCache {
+    std::map<int, std::unique_ptr<EngineBase>> by_b;
+    cudaStream_t stream = nullptr;
+    // host-call staging buffers
+    int32_t *d_src = nullptr, *d_tie = nullptr;
+    int64_t cap_q = 0, cap_tie = 0;
+    int32_t *d_tk_idx = nullptr;
+    double *d_tk_sc = nullptr;
+    int64_t cap_tk = 0, cap_tks = 0;
+    bh_trace *d_trace = nullptr;
+    int64_t cap_tr = 0;
+    double *d_scores = nullptr;
+    int64_t cap_sc = 0;
+    double *d_vec_a = nullptr, *d_vec_b = nullptr;
+    int64_t cap_vec = 0;
+    ~EngineCache() {
+        by_b.clear();
+        cudaFree(d_src); cudaFree(d_tie); cudaFree(d_tk_idx); cudaFree(d_tk_sc);
+        cudaFree(d_trace); cudaFree(d_scores); cudaFree(d_vec_a); cudaFree(d_vec_b);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+template <typename X>
+static void grow(X *&p, int64_t &cap, int64_t need) {
+    if (need <= cap) return;
+    cudaFree(p);
+    p = dalloc<X>((size_t)need);
+    cap = need;
+}
+
+static EngineCache &cache_of(bh_graph *g) {
+    if (!g->engines) {
+        auto *c = new EngineCache();
+        BH_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        g->engines = c;
+    }
+    return *(EngineCache *)g->engines;
+}
+
+template <typename T>
+static EngineBase *make_engine(bh_graph *g, int B) {
+    switch (B) {
+        case 1: return new Engine<T, 1>(g);
+        case 4: return new Engine<T, 4>(g);
+        case 16: return new Engine<T, 16>(g);
+        case 32: return new Engine<T, 32>(g);
+        case 64: return new Engine<T, 64>(g);
+        case 128: return new Engine<T, 128>(g);
+        default: throw InvalidArg("slots must be one of 1, 4, 16, 32, 64, 128");
+    }
+}
+
+static int auto_slots(const bh_graph *g, int64_t n_q) {
+    int b = n_q <= 1 ? 1 : n_q <= 4 ? 4 : n_q <= 16 ? 16 : n_q <= 32 ? 32 : 64;
+    // keep the per-slot state within a fraction of device memory
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+        const int s = g->dtype == BH_DTYPE_F32 ? 4 : 8;
+        while (b > 1 && (double)b * (g->n_u * (2.0 * s + 16) + g->n_v * (double)s) > 0.6 * free_b) b /= 4;
+        if (b == 2 || b == 8) b = b == 2 ? 1 : 4;
+    }
+    return b;
+}
+
+static EngineBase &engine_for(bh_graph *g, int B) {
+    EngineCache &c = cache_of(g);
+    auto it = c.by_b.find(B);
+    if (it != c.by_b.end()) return *it->second;
+    EngineBase *e = g->dtype == BH_DTYPE_F32 ? make_engine<float>(g, B) : make_engine<double>(g, B);
+    c.by_b[B].reset(e);
+    return *e;
+}
+
+static void check_params(double alpha, double eps_b, double eps_f, double lam) {
+    if (!(alpha > 0.0 && alpha < 1.0)) throw InvalidArg("alpha must lie strictly between 0 and 1");
+    if (!(eps_b > 0.0) || !(eps_f > 0.0)) throw InvalidArg("epsilon shares must be positive");
+    if (!(lam > 0.0)) throw InvalidArg("lam must be positive");
+}
+
+}  // namespace bh
+
+// ===========================================================================
+// C ABI
+using namespace bh;
+
+template <class F>
+static int guarded(F &&f) {
+    try {
+        f();
+        return BH_OK;
+    } catch (const InvalidArg &e) {
+        t_err = e.what();
+        return BH_EINVAL;
+    } catch (const std::bad_alloc &) {
+        t_err = "device or host allocation failed";
+        return BH_ENOMEM;
+    } catch (const CudaError &e) {
+        t_err = e.what();
+        return BH_ECUDA;
+    } catch (const std::exception &e) {
+        t_err = e.what();
+        return BH_ECUDA;
+    }
+}
+
+extern "C" {
+
+const char *bh_last_error(void) { return t_err.c_str(); }
+int bh_version(void) { return 1; }
+int64_t bh_kernel_launches(void) { return g_launches.load(); }
+
+int bh_graph_create(int64_t n_u, int64_t n_v, int64_t n_e, const int64_t *u_indptr, const int32_t *u_indices,
+                    const double *u_weights, const int64_t *v_indptr, const int32_t *v_indices,
+                    const double *v_weights, const double *ws_u, const double *ws_v, int32_t device,
+                    int32_t dtype, bh_graph **out) {
+    return guarded([&] {
+        if (!out) throw InvalidArg("out is null");
+        *out = graph_create(n_u, n_v, n_e, u_indptr, u_indices, u_weights, v_indptr, v_indices, v_weights, ws_u,
+                            ws_v, device, dtype);
+    });
+}
+
+void bh_graph_destroy(bh_graph *g) {
+    if (!g) return;
+    cudaSetDevice(g->device);
+    delete (EngineCache *)g->engines;
+    g->engines = nullptr;
+    graph_free_arrays(g);
+    delete g;
+}
+
+int bh_graph_get_info(const bh_graph *g, bh_graph_info *out) {
+    return guarded([&] {
+        if (!g || !out) throw InvalidArg("null argument");
+        out->n_u = g->n_u;
+        out->n_v = g->n_v;
+        out->n_e = g->n_e;
+        out->dtype = g->dtype;
+        out->device = g->device;
+        out->device_bytes = g->device_bytes;
+        out->units_u = g->U.n_units;
+        out->units_v = g->V.n_units;
+        out->split_rows_u = g->U.n_splits;
+        out->split_rows_v = g->V.n_splits;
+        out->chunk_edges = g->chunk;
+        out->reserved = 0;
+    });
+}
+
+int bh_query_batch(bh_graph *g, const bh_query_params *p, const int32_t *sources, int64_t n_q,
+                   const int32_t *tie_skip, int32_t *topk_idx, double *topk_score, bh_trace *trace,
+                   double *scores, void *stream) {
+    return guarded([&] {
+        if (!g || !p || !trace) throw InvalidArg("null argument");
+        if (n_q < 0 || n_q > (1LL << 31) - 1) throw InvalidArg("bad query count");
+        if (n_q == 0) return;
+        check_params(p->alpha, p->eps_b, p->eps_f, p->lam);
+        if (p->k < 0) throw InvalidArg("k must be nonnegative");
+        std::lock_guard<std::mutex> lock(g->mu);
+        BH_CUDA(cudaSetDevice(g->device));
+        EngineCache &c = cache_of(g);
+        cudaStream_t st = stream ? (cudaStream_t)stream : c.stream;
+        const int B = p->slots > 0 ? p->slots : auto_slots(g, n_q);
+        EngineBase &e = engine_for(g, B);
+        RunSpec rs;
+        rs.job = BH_JOB_BHPP;
+        rs.n_q = n_q;
+        rs.alpha = p->alpha;
+        rs.lam = p->lam;
+        rs.eps_b = p->eps_b;
+        rs.eps_f = p->eps_f;
+        rs.k = p->k;
+        rs.exclude = p->exclude_query;
+        rs.want_scores = p->want_scores && scores;
+        if (p->on_device) {
+            rs.sources = sources;
+            rs.tie = tie_skip;
+            rs.topk_idx = topk_idx;
+            rs.topk_score = topk_score;
+            rs.trace = trace;
+            rs.scores = scores;
+            e.run(rs, st);
+            return;
+        }
+        // host pointers: validate, stage in, run, stage out
+        for (int64_t i = 0; i < n_q; i++)
+            if (sources[i] < 0 || sources[i] >= g->n_u) throw InvalidArg("node index out of range");
+        grow(c.d_src, c.cap_q, n_q);
+        BH_CUDA(cudaMemcpyAsync(c.d_src, sources, n_q * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+        if (tie_skip) {
+            grow(c.d_tie, c.cap_tie, n_q);
+            BH_CUDA(cudaMemcpyAsync(c.d_tie, tie_skip, n_q * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+        }
+        grow(c.d_trace, c.cap_tr, n_q);
+        rs.sources = c.d_src;
+        rs.tie = tie_skip ? c.d_tie : nullptr;
+        rs.trace = c.d_trace;
+        if (p->k > 0 && topk_idx) {
+            grow(c.d_tk_idx, c.cap_tk, n_q * p->k);
+            grow(c.d_tk_sc, c.cap_tks, n_q * p->k);
+            rs.topk_idx = c.d_tk_idx;
+            rs.topk_score = c.d_tk_sc;
+        }
+        if (rs.want_scores) {
+            grow(c.d_scores, c.cap_sc, n_q * g->n_u);
+            rs.scores = c.d_scores;
+        }
+        e.run(rs, st);
+        BH_CUDA(cudaMemcpyAsync(trace, c.d_trace, n_q * sizeof(bh_trace), cudaMemcpyDeviceToHost, st));
+        if (rs.topk_idx) {
+            BH_CUDA(cudaMemcpyAsync(topk_idx, c.d_tk_idx, n_q * p->k * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+            if (topk_score)
+                BH_CUDA(cudaMemcpyAsync(topk_score, c.d_tk_sc, n_q * p->k * sizeof(double), cudaMemcpyDeviceToHost, st));
+        }
+        if (rs.want_scores)
+            BH_CUDA(cudaMemcpyAsync(scores, c.d_scores, n_q * g->n_u * sizeof(double), cudaMemcpyDeviceToHost, st));
+        BH_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int bh_push_run(bh_graph *g, int32_t job, int32_t source, double alpha, double lam, double eps_b, double eps_f,
+                int32_t tie_skip, double *residue_u, double *estimate, int64_t *n_p, double *scores,
+                bh_trace *trace, bh_round_hook hook, void *user) {
+    return guarded([&] {
+        if (!g || !trace) throw InvalidArg("null argument");
+        if (job < BH_JOB_BHPP || job > BH_JOB_PI_PUSH) throw InvalidArg("bad job");
+        if (!(alpha > 0.0 && alpha < 1.0)) throw InvalidArg("alpha must lie strictly between 0 and 1");
+        if (source < 0 || source >= g->n_u) throw InvalidArg("node index out of range");
+        if (job != BH_JOB_PI_PUSH && !(eps_b > 0.0)) throw InvalidArg("epsilon_b must be positive");
+        if ((job == BH_JOB_PI_PUSH || job == BH_JOB_BHPP) && !(eps_f > 0.0)) throw InvalidArg("epsilon_f must be positive");
+        if ((job == BH_JOB_PI_PUSH || job == BH_JOB_BHPP) && !(lam > 0.0)) throw InvalidArg("lam must be positive");
+        std::lock_guard<std::mutex> lock(g->mu);
+        BH_CUDA(cudaSetDevice(g->device));
+        EngineCache &c = cache_of(g);
+        cudaStream_t st = c.stream;
+        EngineBase &e = engine_for(g, 1);
+        const int64_t nu = g->n_u;
+        grow(c.d_src, c.cap_q, 1);
+        grow(c.d_trace, c.cap_tr, 1);
+        if (c.cap_vec < nu) {
+            cudaFree(c.d_vec_a);
+            cudaFree(c.d_vec_b);
+            c.d_vec_a = dalloc<double>(nu);
+            c.d_vec_b = dalloc<double>(nu);
+            c.cap_vec = nu;
+        }
+        grow(c.d_scores, c.cap_sc, nu);
+        BH_CUDA(cudaMemcpyAsync(c.d_src, &source, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+        RunSpec rs;
+        rs.job = job;
+        rs.n_q = 1;
+        rs.sources = c.d_src;
+        int32_t tie_h = tie_skip;
+        grow(c.d_tie, c.cap_tie, 1);
+        BH_CUDA(cudaMemcpyAsync(c.d_tie, &tie_h, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+        rs.tie = c.d_tie;
+        rs.alpha = alpha;
+        rs.lam = lam > 0 ? lam : 1.0;
+        rs.eps_b = eps_b > 0 ? eps_b : 1.0;
+        rs.eps_f = eps_f > 0 ? eps_f : 1.0;
+        rs.trace = c.d_trace;
+        rs.want_scores = 1;
+        rs.scores = c.d_scores;
+        rs.hook = hook;
+        rs.hook_user = user;
+        if (job == BH_JOB_PI_PUSH) {
+            BH_CUDA(cudaMemcpyAsync(c.d_vec_a, residue_u, nu * sizeof(double), cudaMemcpyHostToDevice, st));
+            BH_CUDA(cudaMemcpyAsync(c.d_vec_b, estimate, nu * sizeof(double), cudaMemcpyHostToDevice, st));
+            rs.ledger_r = c.d_vec_a;
+            rs.ledger_est = c.d_vec_b;
+            rs.init_np = *n_p;
+        }
+        e.run(rs, st);
+        BH_CUDA(cudaStreamSynchronize(st));
+        // ledger out (slot 0)
+        e.read_ledger(0, c.d_vec_a, c.d_vec_b, st);
+        BH_CUDA(cudaMemcpyAsync(residue_u, c.d_vec_a, nu * sizeof(double), cudaMemcpyDeviceToHost, st));
+        BH_CUDA(cudaMemcpyAsync(estimate, c.d_vec_b, nu * sizeof(double), cudaMemcpyDeviceToHost, st));
+        BH_CUDA(cudaMemcpyAsync(trace, c.d_trace, sizeof(bh_trace), cudaMemcpyDeviceToHost, st));
+        if (scores && (job == BH_JOB_BHPP || job == BH_JOB_PI_PUSH))
+            BH_CUDA(cudaMemcpyAsync(scores, c.d_scores, nu * sizeof(double), cudaMemcpyDeviceToHost, st));
+        BH_CUDA(cudaStreamSynchronize(st));
+        *n_p = job == BH_JOB_SS_PUSH || job == BH_JOB_SELECTIVE ? trace->n_p_b : trace->n_p_f;
+    });
+}
+
+int bh_power_iteration(bh_graph *g, const double *start, int64_t n_vec, double alpha, int32_t t, double *out) {
+    return guarded([&] {
+        if (!g || !start || !out) throw InvalidArg("null argument");
+        if (!(alpha > 0.0 && alpha < 1.0)) throw InvalidArg("alpha must lie strictly between 0 and 1");
+        if (t < 0) throw InvalidArg("iteration count must be nonnegative");
+        if (n_vec <= 0) return;
+        std::lock_guard<std::mutex> lock(g->mu);
+        BH_CUDA(cudaSetDevice(g->device));
+        EngineCache &c = cache_of(g);
+        cudaStream_t st = c.stream;
+        const int64_t nu = g->n_u;
+        const int B = auto_slots(g, n_vec);
+        EngineBase &e = engine_for(g, B);
+        grow(c.d_src, c.cap_q, n_vec);
+        std::vector<int32_t> zeros((size_t)n_vec, 0);
+        BH_CUDA(cudaMemcpyAsync(c.d_src, zeros.data(), n_vec * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+        grow(c.d_trace, c.cap_tr, n_vec);
+        double *d_x0 = dalloc<double>((size_t)n_vec * nu);
+        double *d_out = dalloc<double>((size_t)n_vec * nu);
+        try {
+            BH_CUDA(cudaMemcpyAsync(d_x0, start, n_vec * nu * sizeof(double), cudaMemcpyHostToDevice, st));
+            RunSpec rs;
+            rs.job = BH_JOB_POWER;
+            rs.n_q = n_vec;
+            rs.sources = c.d_src;
+            rs.alpha = alpha;
+            rs.power_t = t;
+            rs.x0 = d_x0;
+            rs.trace = c.d_trace;
+            rs.want_scores = 1;
+            rs.scores = d_out;
+            e.run(rs, st);
+            BH_CUDA(cudaMemcpyAsync(out, d_out, n_vec * nu * sizeof(double), cudaMemcpyDeviceToHost, st));
+            BH_CUDA(cudaStreamSynchronize(st));
+        } catch (...) {
+            cudaFree(d_x0);
+            cudaFree(d_out);
+            throw;
+        }
+        cudaFree(d_x0);
+        cudaFree(d_out);
+    });
+}
+
+int bh_topk(const double *scores, int64_t n, int64_t k, int64_t exclude, int64_t *out_idx, double *out_score,
+            int64_t *out_count) {
+    return guarded([&] {
+        if (!scores || !out_idx || !out_score || !out_count) throw InvalidArg("null argument");
+        if (k <= 0) throw InvalidArg("k must be positive");
+        *out_count = 0;
+        if (n <= 0) return;
+        cudaStream_t st = nullptr;
+        double *dx = dalloc<double>(n);
+        int64_t *didx = nullptr, *dcnt = nullptr;
+        double *dsc = nullptr;
+        uint64_t *ck = nullptr;
+        int64_t *ci = nullptr;
+        void *tmp = nullptr;
+        auto cleanup = [&] {
+            cudaFree(dx); cudaFree(didx); cudaFree(dcnt); cudaFree(dsc); cudaFree(ck); cudaFree(ci); cudaFree(tmp);
+        };
+        try {
+            BH_CUDA(cudaMemcpyAsync(dx, scores, n * sizeof(double), cudaMemcpyHostToDevice, st));
+            const int64_t kk = std::min(k, n);
+            if (kk <= TOPK_MAX) {
+                const int64_t chunk = 8192;
+                const int64_t nch = (n + chunk - 1) / chunk;
+                ck = dalloc<uint64_t>(nch * kk);
+                ci = dalloc<int64_t>(nch * kk);
+                didx = dalloc<int64_t>(kk);
+                dsc = dalloc<double>(kk);
+                dcnt = dalloc<int64_t>(1);
+                k_vec_topk_chunks<<<(unsigned)nch, TOPK_THREADS, 0, st>>>(dx, n, kk, exclude, chunk, ck, ci);
+                k_vec_topk_merge<<<1, TOPK_THREADS, 0, st>>>(nch * kk, kk, ck, ci, didx, dsc, dcnt);
+                count_launch(2);
+                BH_CUDA(cudaGetLastError());
+                int64_t m = 0;
+                BH_CUDA(cudaMemcpyAsync(&m, dcnt, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+                BH_CUDA(cudaStreamSynchronize(st));
+                BH_CUDA(cudaMemcpy(out_idx, didx, m * sizeof(int64_t), cudaMemcpyDeviceToHost));
+                BH_CUDA(cudaMemcpy(out_score, dsc, m * sizeof(double), cudaMemcpyDeviceToHost));
+                *out_count = m;
+            } else {
+                // large k: stable radix sort of (order key desc, index) pairs
+                uint64_t *keys_in = dalloc<uint64_t>(n), *keys_out = dalloc<uint64_t>(n);
+                int64_t *v_in = dalloc<int64_t>(n), *v_out = dalloc<int64_t>(n);
+                std::vector<int64_t> iota((size_t)n);
+                std::vector<uint64_t> hk((size_t)n);
+                for (int64_t i = 0; i < n; i++) {
+                    iota[i] = i;
+                    uint64_t b;
+                    std::memcpy(&b, &scores[i], 8);
+                    hk[i] = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+                }
+                BH_CUDA(cudaMemcpy(keys_in, hk.data(), n * 8, cudaMemcpyHostToDevice));
+                BH_CUDA(cudaMemcpy(v_in, iota.data(), n * 8, cudaMemcpyHostToDevice));
+                size_t tb = 0;
+                cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, keys_in, keys_out, v_in, v_out, (int)n);
+                tmp = dalloc<char>(tb);
+                cub::DeviceRadixSort::SortPairsDescending(tmp, tb, keys_in, keys_out, v_in, v_out, (int)n);
+                count_launch(4);
+                BH_CUDA(cudaGetLastError());
+                std::vector<int64_t> order((size_t)n);
+                BH_CUDA(cudaMemcpy(order.data(), v_out, n * 8, cudaMemcpyDeviceToHost));
+                cudaFree(keys_in); cudaFree(keys_out); cudaFree(v_in); cudaFree(v_out);
+                int64_t m = 0;
+                for (int64_t i = 0; i < n && m < k; i++) {
+                    if (order[i] == exclude) continue;
+                    out_idx[m] = order[i];
+                    out_score[m] = scores[order[i]];
+                    m++;
+                }
+                *out_count = m;
+            }
+        } catch (...) {
+            cleanup();
+            throw;
+        }
+        cleanup();
+    });
+}
+
+}  // extern "C"

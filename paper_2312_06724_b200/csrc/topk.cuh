@@ -1,0 +1,315 @@
+// topk.cuh -- K5/K6: BHPP combine + per-query top-k (K-T in SURVEY.md sec. 2).
+//
+// K5 (one CTA per (finished slot, chunk of U)): beta = (w_ratio * est
+//     [+ alpha * acc_t]) + est, w_ratio = ws(u) / ws(q)  (bhpp_query.py:189,
+//     push_engine.py:245-249), written contiguously per query; then the chunk's
+//     top-k candidates by a radix select on the order-preserving key bits.
+// K6 (one CTA per finished slot): merge the chunk candidates with the same
+//     select, sort the k winners by (score desc, index asc) -- the order of
+//     np.argsort(-scores, kind="stable") in topk (bhpp_query.py:206-218) --
+//     and write them plus the phase trace at the query's batch index.
+#pragma once
+
+#include "kernels.cuh"
+
+namespace bh {
+
+__device__ __forceinline__ uint64_t order_key(double x) {
+    uint64_t b = (uint64_t)__double_as_longlong(x);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double key_value(uint64_t k) {
+    uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+    return __longlong_as_double((long long)b);
+}
+
+constexpr int TOPK_THREADS = 256;
+constexpr int TOPK_MAX = 1024;
+
+struct SelectSmem {
+    uint32_t hist[256];
+    unsigned long long cnt;
+    uint64_t prefix;
+    int64_t krem;
+    int32_t out_n;
+};
+
+// Select exactly min(k, #valid) elements that are largest under (key desc,
+// idx asc) among n candidates given by acc(i, &key, &idx) -> valid.  Output
+// order is arbitrary.  All threads of the block must call it.
+template <class Acc>
+__device__ int64_t block_select(int64_t n, int64_t k, Acc acc, SelectSmem &sm, uint64_t *out_key,
+                                int64_t *out_idx) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    if (tid == 0) {
+        sm.cnt = 0;
+        sm.out_n = 0;
+    }
+    __syncthreads();
+    unsigned long long c = 0;
+    for (int64_t i = tid; i < n; i += nt) {
+        uint64_t kk;
+        int64_t ii;
+        c += acc(i, kk, ii);
+    }
+    atomicAdd(&sm.cnt, c);
+    __syncthreads();
+    const int64_t n_valid = (int64_t)sm.cnt;
+    if (n_valid <= k) {
+        for (int64_t i = tid; i < n; i += nt) {
+            uint64_t kk;
+            int64_t ii;
+            if (acc(i, kk, ii)) {
+                int p = atomicAdd(&sm.out_n, 1);
+                out_key[p] = kk;
+                out_idx[p] = ii;
+            }
+        }
+        __syncthreads();
+        return n_valid;
+    }
+    // 8 passes over the key bits, most significant digit first
+    uint64_t prefix = 0, mask = 0;
+    if (tid == 0) sm.krem = k;
+    for (int shift = 56; shift >= 0; shift -= 8) {
+        for (int d = tid; d < 256; d += nt) sm.hist[d] = 0;
+        __syncthreads();
+        for (int64_t i = tid; i < n; i += nt) {
+            uint64_t kk;
+            int64_t ii;
+            if (acc(i, kk, ii) && (kk & mask) == prefix) atomicAdd(&sm.hist[(kk >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int64_t cum = 0;
+            for (int d = 255; d >= 0; d--) {
+                if (cum + sm.hist[d] >= sm.krem) {
+                    sm.krem -= cum;
+                    sm.prefix = prefix | ((uint64_t)d << shift);
+                    break;
+                }
+                cum += sm.hist[d];
+            }
+        }
+        __syncthreads();
+        prefix = sm.prefix;
+        mask |= (0xffull << shift);
+    }
+    const uint64_t kstar = prefix;
+    // ties at kstar: the smallest indices (4 passes over 32-bit indices)
+    uint64_t ipre = 0, imask = 0;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        for (int d = tid; d < 256; d += nt) sm.hist[d] = 0;
+        __syncthreads();
+        for (int64_t i = tid; i < n; i += nt) {
+            uint64_t kk;
+            int64_t ii;
+            if (acc(i, kk, ii) && kk == kstar && (((uint64_t)ii) & imask) == ipre)
+                atomicAdd(&sm.hist[(((uint64_t)ii) >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int64_t cum = 0;
+            for (int d = 0; d < 256; d++) {
+                if (cum + sm.hist[d] >= sm.krem) {
+                    sm.krem -= cum;
+                    sm.prefix = ipre | ((uint64_t)d << shift);
+                    break;
+                }
+                cum += sm.hist[d];
+            }
+        }
+        __syncthreads();
+        ipre = sm.prefix;
+        imask |= (0xffull << shift);
+    }
+    const uint64_t istar = ipre;
+    for (int64_t i = tid; i < n; i += nt) {
+        uint64_t kk;
+        int64_t ii;
+        if (acc(i, kk, ii) && (kk > kstar || (kk == kstar && (uint64_t)ii <= istar))) {
+            int p = atomicAdd(&sm.out_n, 1);
+            out_key[p] = kk;
+            out_idx[p] = ii;
+        }
+    }
+    __syncthreads();
+    return k;
+}
+
+// Bitonic sort of P (power of two) (key, idx) pairs in shared memory into
+// (key desc, idx asc) order.
+__device__ void block_sort_pairs(uint64_t *key, int64_t *idx, int P) {
+    for (int size = 2; size <= P; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            __syncthreads();
+            for (int i = threadIdx.x; i < P; i += blockDim.x) {
+                int j = i ^ stride;
+                if (j > i) {
+                    bool up = (i & size) == 0;  // ascending in "goes first" order
+                    uint64_t ka = key[i], kb = key[j];
+                    int64_t ia = idx[i], ib = idx[j];
+                    bool a_first = ka > kb || (ka == kb && ia < ib);
+                    if (up ? !a_first : a_first) {
+                        key[i] = kb;
+                        key[j] = ka;
+                        idx[i] = ib;
+                        idx[j] = ia;
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+}
+
+template <typename T>
+struct FinalArgs {
+    int64_t n_u;
+    int32_t B, k, exclude, want_scores;
+    int32_t chunk, n_chunks;
+    const double *EST;
+    const T *P;
+    const double *ws_u;
+    double alpha;
+    const Finish *fin;
+    const Control *ctl;
+    double *outs;        // [B][n_u] per-slot score rows
+    double *out_scores;  // [n_q][n_u] or null
+    uint64_t *cand_key;  // [B][n_chunks][k]
+    int64_t *cand_idx;
+    int32_t *topk_idx;   // [n_q][k]
+    double *topk_score;  // [n_q][k]
+    bh_trace *trace;     // [n_q]
+};
+
+template <typename T>
+__device__ __forceinline__ double *score_row(const FinalArgs<T> &a, int s, const Finish &f) {
+    return a.want_scores ? a.out_scores + (int64_t)f.qidx * a.n_u : a.outs + (int64_t)s * a.n_u;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(TOPK_THREADS) k_finalize(FinalArgs<T> a) {
+    const int n_fin = a.ctl->n_fin;
+    if (n_fin == 0) return;
+    __shared__ SelectSmem sm;
+    const int B = a.B;
+    for (int64_t p = blockIdx.x; p < (int64_t)n_fin * a.n_chunks; p += gridDim.x) {
+        const int fi = (int)(p / a.n_chunks);
+        const int c = (int)(p % a.n_chunks);
+        const int s = a.ctl->fin_slots[fi];
+        const Finish f = a.fin[s];
+        if (f.job == BH_JOB_SS_PUSH || f.job == BH_JOB_SELECTIVE) continue;
+        double *dst = score_row(a, s, f);
+        const int64_t u0 = (int64_t)c * a.chunk;
+        const int64_t u1 = imin64(a.n_u, u0 + a.chunk);
+        for (int64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
+            const double est = a.EST[u * B + s];
+            const double ws = a.ws_u[u];
+            double v;
+            if (f.job == BH_JOB_POWER) {
+                v = a.alpha * (ws * (double)a.P[u * B + s]);
+            } else {
+                v = (ws * f.inv_ws_q) * est;                                  // w_ratio * est
+                if (f.has_pi) v = v + a.alpha * (ws * (double)a.P[u * B + s]);  // + alpha acc_t
+                if (f.job == BH_JOB_BHPP) v = v + est;                         // + backward est
+            }
+            dst[u] = v;
+        }
+        if (a.k <= 0) continue;
+        __syncthreads();
+        const int64_t excl = (a.exclude && f.job == BH_JOB_BHPP) ? f.src : -1;
+        auto acc = [&](int64_t i, uint64_t &kk, int64_t &ii) -> bool {
+            ii = u0 + i;
+            kk = order_key(dst[ii]);
+            return ii != excl;
+        };
+        uint64_t *ck = a.cand_key + ((int64_t)s * a.n_chunks + c) * a.k;
+        int64_t *ci = a.cand_idx + ((int64_t)s * a.n_chunks + c) * a.k;
+        const int64_t m = block_select(u1 - u0, a.k, acc, sm, ck, ci);
+        for (int64_t i = m + threadIdx.x; i < a.k; i += blockDim.x) ci[i] = -1;
+        __syncthreads();
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(TOPK_THREADS) k_topk_merge(FinalArgs<T> a) {
+    const int n_fin = a.ctl->n_fin;
+    if ((int)blockIdx.x >= n_fin) return;
+    __shared__ SelectSmem sm;
+    __shared__ uint64_t skey[TOPK_MAX];
+    __shared__ int64_t sidx[TOPK_MAX];
+    const int s = a.ctl->fin_slots[blockIdx.x];
+    const Finish f = a.fin[s];
+    if (threadIdx.x == 0) a.trace[f.qidx] = f.trace;
+    if (a.k <= 0 || f.job == BH_JOB_SS_PUSH || f.job == BH_JOB_SELECTIVE || !a.topk_idx) return;
+    const uint64_t *ck = a.cand_key + (int64_t)s * a.n_chunks * a.k;
+    const int64_t *ci = a.cand_idx + (int64_t)s * a.n_chunks * a.k;
+    auto acc = [&](int64_t i, uint64_t &kk, int64_t &ii) -> bool {
+        ii = ci[i];
+        kk = ck[i];
+        return ii >= 0;
+    };
+    int P = 1;
+    while (P < a.k) P <<= 1;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        skey[i] = 0;
+        sidx[i] = INT64_MAX;
+    }
+    __syncthreads();
+    const int64_t m = block_select((int64_t)a.n_chunks * a.k, a.k, acc, sm, skey, sidx);
+    block_sort_pairs(skey, sidx, P);
+    for (int i = threadIdx.x; i < a.k; i += blockDim.x) {
+        const bool ok = i < m;
+        a.topk_idx[(int64_t)f.qidx * a.k + i] = ok ? (int32_t)sidx[i] : -1;
+        if (a.topk_score) a.topk_score[(int64_t)f.qidx * a.k + i] = ok ? key_value(skey[i]) : 0.0;
+    }
+}
+
+// Standalone top-k of one device vector (bh_topk): chunk select + merge.
+__global__ void __launch_bounds__(TOPK_THREADS) k_vec_topk_chunks(const double *x, int64_t n, int64_t k,
+                                                                  int64_t exclude, int64_t chunk,
+                                                                  uint64_t *ck, int64_t *ci) {
+    __shared__ SelectSmem sm;
+    const int64_t u0 = (int64_t)blockIdx.x * chunk;
+    const int64_t u1 = imin64(n, u0 + chunk);
+    auto acc = [&](int64_t i, uint64_t &kk, int64_t &ii) -> bool {
+        ii = u0 + i;
+        const double v = x[ii];
+        kk = order_key(v);
+        return ii != exclude && v == v;
+    };
+    uint64_t *okey = ck + (int64_t)blockIdx.x * k;
+    int64_t *oidx = ci + (int64_t)blockIdx.x * k;
+    const int64_t m = block_select(u1 - u0, k, acc, sm, okey, oidx);
+    for (int64_t i = m + threadIdx.x; i < k; i += blockDim.x) oidx[i] = -1;
+}
+
+__global__ void __launch_bounds__(TOPK_THREADS) k_vec_topk_merge(int64_t n_cand, int64_t k, const uint64_t *ck,
+                                                                 const int64_t *ci, int64_t *out_idx,
+                                                                 double *out_score, int64_t *out_count) {
+    __shared__ SelectSmem sm;
+    __shared__ uint64_t skey[TOPK_MAX];
+    __shared__ int64_t sidx[TOPK_MAX];
+    auto acc = [&](int64_t i, uint64_t &kk, int64_t &ii) -> bool {
+        ii = ci[i];
+        kk = ck[i];
+        return ii >= 0;
+    };
+    int P = 1;
+    while (P < k) P <<= 1;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        skey[i] = 0;
+        sidx[i] = INT64_MAX;
+    }
+    __syncthreads();
+    const int64_t m = block_select(n_cand, k, acc, sm, skey, sidx);
+    block_sort_pairs(skey, sidx, P);
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        out_idx[i] = sidx[i];
+        out_score[i] = key_value(skey[i]);
+    }
+    if (threadIdx.x == 0) *out_count = m;
+}
+
+}  // namespace bh
