@@ -137,6 +137,22 @@ int bh_power_iteration(bh_graph *g, const double *start, int64_t n_vec, double a
 int bh_topk(const double *scores, int64_t n, int64_t k, int64_t exclude, int64_t *out_idx,
             double *out_score, int64_t *out_count);
 
+/* ---- measurement ---------------------------------------------------------- */
+typedef struct bh_run_stats {
+    int64_t rounds;        /* rounds launched by the last run on this graph      */
+    int64_t launches;      /* kernels launched by it                             */
+    int64_t slots;         /* query-block width B it used                        */
+    int64_t profiled;      /* 1 if the ms_* fields below were measured           */
+    double ms_prep;        /* sum of K1 (prep) durations, CUDA events            */
+    double ms_vpull;       /* sum of K2 + K2b (V pull) durations                 */
+    double ms_upull;       /* sum of K3 + K3b (U pull) durations                 */
+    double ms_control;     /* sum of K4..K6 (control, finalize, top-k)           */
+} bh_run_stats;
+/* on != 0: bracket every round's kernels with CUDA events on the launch stream
+ * (process-wide switch; costs one event record per kernel group). */
+int bh_set_profiling(int32_t on);
+int bh_last_run_stats(bh_graph *g, bh_run_stats *out);
+
 /* ---- misc ----------------------------------------------------------------- */
 const char *bh_last_error(void);
 int bh_version(void);

@@ -26,6 +26,7 @@ PHASES = ("selective", "sequential", "forward-selective")
 EXPORTS = (
     "bh_graph_create", "bh_graph_destroy", "bh_graph_get_info", "bh_query_batch", "bh_push_run",
     "bh_power_iteration", "bh_topk", "bh_last_error", "bh_version", "bh_kernel_launches",
+    "bh_set_profiling", "bh_last_run_stats",
 )
 
 
@@ -62,6 +63,13 @@ class GraphInfo(C.Structure):
         ("dtype", C.c_int32), ("device", C.c_int32), ("device_bytes", C.c_int64),
         ("units_u", C.c_int32), ("units_v", C.c_int32), ("split_rows_u", C.c_int32),
         ("split_rows_v", C.c_int32), ("chunk_edges", C.c_int32), ("reserved", C.c_int32),
+    ]
+
+
+class RunStats(C.Structure):
+    _fields_ = [
+        ("rounds", C.c_int64), ("launches", C.c_int64), ("slots", C.c_int64), ("profiled", C.c_int64),
+        ("ms_prep", C.c_double), ("ms_vpull", C.c_double), ("ms_upull", C.c_double), ("ms_control", C.c_double),
     ]
 
 
@@ -105,6 +113,10 @@ def lib():
         L.bh_last_error.argtypes = []
         L.bh_version.restype = C.c_int
         L.bh_kernel_launches.restype = C.c_int64
+        L.bh_set_profiling.restype = C.c_int
+        L.bh_set_profiling.argtypes = [C.c_int32]
+        L.bh_last_run_stats.restype = C.c_int
+        L.bh_last_run_stats.argtypes = [P, C.POINTER(RunStats)]
         _lib = L
     return _lib
 
@@ -158,6 +170,15 @@ class DeviceGraph:
 
     def close(self):
         self._fin()
+
+    def last_run_stats(self) -> dict:
+        st = RunStats()
+        check(lib().bh_last_run_stats(self.h, C.byref(st)))
+        return {f: getattr(st, f) for f, _ in RunStats._fields_}
+
+
+def set_profiling(on: bool) -> None:
+    check(lib().bh_set_profiling(1 if on else 0))
 
 
 _graph_cache: dict = {}

@@ -231,12 +231,31 @@ def bhpp_query_batch(g, meta: IndexMeta, sources, epsilon: float, k: int | None 
     t0 = time.perf_counter()
     _capi.check(_capi.lib().bh_query_batch(
         dg.h, C.byref(prm), _capi.ptr(src), n_q, _capi.ptr(ties), _capi.ptr(tk_idx) if kk else None,
-        _capi.ptr(tk_sc) if kk else None, _capi.ptr(traces), _capi.ptr(scores), stream))
+        _capi.ptr(tk_sc) if kk else None, _capi.ptr(traces), _capi.ptr(scores),
+        C.c_void_p(stream) if stream else None))
     t1 = time.perf_counter()
     if kk == 0:
         tk_idx, tk_sc = tk_idx[:, :0], tk_sc[:, :0]
     return BatchResult(sources=src, epsilon=epsilon, epsilon_b=eps_b, epsilon_f=eps_f, k=kk, topk_index=tk_idx,
                        topk_score=tk_sc, traces=traces, scores=scores, timing={"total": t1 - t0}, dtype=dtype)
+
+
+def query_batch_device(dg, meta: IndexMeta, eps_b: float, eps_f: float, sources_ptr: int, n_q: int, k: int,
+                       topk_idx_ptr: int, topk_score_ptr: int, trace_ptr: int, scores_ptr: int = 0,
+                       exclude_query: bool = False, slots: int | None = None, tie_ptr: int = 0,
+                       stream: int | None = None) -> None:
+    """bh_query_batch with every buffer already resident on the device (raw
+    device pointers, e.g. torch ``data_ptr()``); nothing crosses PCIe.  The
+    caller owns the stream ordering (``stream`` = cudaStream_t handle)."""
+    import ctypes as C
+
+    prm = _capi.QueryParams(alpha=meta.alpha, lam=meta.lam, eps_b=eps_b, eps_f=eps_f, k=int(k),
+                            exclude_query=int(bool(exclude_query)), want_scores=int(bool(scores_ptr)),
+                            slots=int(slots or 0), on_device=1)
+    vp = lambda x: C.c_void_p(x) if x else None  # noqa: E731
+    _capi.check(_capi.lib().bh_query_batch(dg.h, C.byref(prm), vp(sources_ptr), int(n_q), vp(tie_ptr),
+                                           vp(topk_idx_ptr), vp(topk_score_ptr), vp(trace_ptr), vp(scores_ptr),
+                                           vp(stream)))
 
 
 def topk(result: QueryResult, k: int, exclude_query: bool = False) -> list[tuple[str, float]]:

@@ -146,6 +146,7 @@ struct Control {
     int32_t next_q;    // next query index to start
     int32_t n_q;       // queries in this batch
     int32_t n_fin;     // slots finishing this round
+    int32_t rounds_active;  // rounds K4 processed with work in flight
     int32_t fin_slots[256];
 };
 

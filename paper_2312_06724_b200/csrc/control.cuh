@@ -106,7 +106,10 @@ __global__ void k_control(ControlArgs a) {
         if (s == 0) ctl->n_fin = 0;
         return;
     }
-    if (s == 0) s_busy = 0;
+    if (s == 0) {
+        s_busy = 0;
+        if (!a.first) ctl->rounds_active++;
+    }
     Slot sl;
     bool fin = false;
     if (s < B) {

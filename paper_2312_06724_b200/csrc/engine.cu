@@ -79,8 +79,11 @@ struct RunSpec {
     void *hook_user = nullptr;
 };
 
+static std::atomic<int> g_profiling{0};
+
 struct EngineBase {
     virtual ~EngineBase() = default;
+    bh_run_stats stats{};
     virtual void run(const RunSpec &rs, cudaStream_t st) = 0;
     virtual void read_ledger(int s, double *r_u_dev, double *est_dev, cudaStream_t st) = 0;
     virtual void slot_state(int s, Slot *out, cudaStream_t st) = 0;
@@ -102,6 +105,7 @@ struct Engine final : EngineBase {
     uint64_t *cand_key = nullptr;
     int64_t *cand_idx = nullptr;
     double *hook_r = nullptr, *hook_est = nullptr;
+    std::vector<cudaEvent_t> evpool;
     int fin_chunk = 4096, n_chunks = 1;
     int grid_prep = 1, grid_pv = 1, grid_pu = 1, grid_fv = 1, grid_fu = 1, grid_k5 = 1;
 
@@ -162,6 +166,16 @@ struct Engine final : EngineBase {
         cudaFree(part.any); cudaFree(part.sum);
         cudaFree(scratch); cudaFree(cand_key); cudaFree(cand_idx);
         cudaFree(hook_r); cudaFree(hook_est);
+        for (auto e : evpool) cudaEventDestroy(e);
+    }
+
+    cudaEvent_t ev(size_t i) {
+        while (evpool.size() <= i) {
+            cudaEvent_t e;
+            BH_CUDA(cudaEventCreate(&e));
+            evpool.push_back(e);
+        }
+        return evpool[i];
     }
 
     void ensure_cand(int k) {
@@ -195,7 +209,10 @@ struct Engine final : EngineBase {
         return a;
     }
 
-    void launch_round(const RunSpec &rs, const ControlArgs &ca, const FinalArgs<T> &fa, cudaStream_t st) {
+    void launch_round(const RunSpec &rs, const ControlArgs &ca, const FinalArgs<T> &fa, cudaStream_t st,
+                      int64_t round, bool prof) {
+        const size_t e0 = (size_t)round * 5;
+        if (prof) BH_CUDA(cudaEventRecord(ev(e0), st));
         PrepArgs<T> pa{};
         pa.n_u = g->n_u;
         pa.R = R;
@@ -210,6 +227,7 @@ struct Engine final : EngineBase {
         pa.part = part;
         pa.alpha = rs.alpha;
         k_prep<B, T><<<grid_prep, PREP_THREADS, 0, st>>>(pa);
+        if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 1), st));
 
         PullArgs<T> av = pull_args(SIDE_V);
         av.one_minus_alpha = 1.0 - rs.alpha;
@@ -221,6 +239,7 @@ struct Engine final : EngineBase {
             k_pull_finish<B, T, SIDE_V><<<grid_fv, PULL_THREADS, 0, st>>>(av);
             launches++;
         }
+        if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 2), st));
         PullArgs<T> au = pull_args(SIDE_U);
         au.one_minus_alpha = 1.0 - rs.alpha;
         au.part_row0 = 0;
@@ -231,12 +250,31 @@ struct Engine final : EngineBase {
             k_pull_finish<B, T, SIDE_U><<<grid_fu, PULL_THREADS, 0, st>>>(au);
             launches++;
         }
+        if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 3), st));
         k_control<<<1, std::max(32, B), 0, st>>>(ca);
         k_finalize<T><<<grid_k5, TOPK_THREADS, 0, st>>>(fa);
         k_topk_merge<T><<<B, TOPK_THREADS, 0, st>>>(fa);
+        if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 4), st));
         launches += 3;
         count_launch(launches);
+        stats.launches += launches;
         BH_CUDA(cudaGetLastError());
+    }
+
+    void collect_profile(int64_t rounds) {
+        double t[4] = {0, 0, 0, 0};
+        for (int64_t r = 0; r < rounds; r++) {
+            for (int j = 0; j < 4; j++) {
+                float ms = 0.f;
+                BH_CUDA(cudaEventElapsedTime(&ms, ev((size_t)r * 5 + j), ev((size_t)r * 5 + j + 1)));
+                t[j] += ms;
+            }
+        }
+        stats.ms_prep = t[0];
+        stats.ms_vpull = t[1];
+        stats.ms_upull = t[2];
+        stats.ms_control = t[3];
+        stats.profiled = 1;
     }
 
     void run(const RunSpec &rs, cudaStream_t st) override {
@@ -304,12 +342,16 @@ struct Engine final : EngineBase {
         fa.trace = rs.trace;
 
         const int poll = rs.hook ? 1 : 8;
+        const bool prof = g_profiling.load() != 0;
+        stats = bh_run_stats{};
+        stats.slots = B;
+        stats.launches = 1;
         int32_t last_seq = 0;
         std::vector<double> hr, he;
         const int64_t max_rounds = 100000000;
         for (int64_t round = 0; round < max_rounds;) {
             for (int i = 0; i < poll; i++, round++) {
-                launch_round(rs, ca, fa, st);
+                launch_round(rs, ca, fa, st, round, prof);
                 if (rs.hook) {
                     Slot s0;
                     slot_state(0, &s0, st);
@@ -327,7 +369,11 @@ struct Engine final : EngineBase {
             }
             BH_CUDA(cudaMemcpyAsync(h_ctl, ctl, sizeof(Control), cudaMemcpyDeviceToHost, st));
             BH_CUDA(cudaStreamSynchronize(st));
-            if (!h_ctl->active && h_ctl->n_fin == 0) return;
+            if (!h_ctl->active && h_ctl->n_fin == 0) {
+                stats.rounds = h_ctl->rounds_active;
+                if (prof) collect_profile(round);
+                return;
+            }
         }
         throw CudaError("query batch did not terminate");
     }
@@ -348,6 +394,7 @@ struct Engine final : EngineBase {
 // ---------------------------------------------------------------------------
 struct EngineCache {
     std::map<int, std::unique_ptr<EngineBase>> by_b;
+    EngineBase *last = nullptr;
     cudaStream_t stream = nullptr;
     // host-call staging buffers
     int32_t *d_src = nullptr, *d_tie = nullptr;
@@ -458,6 +505,20 @@ const char *bh_last_error(void) { return t_err.c_str(); }
 int bh_version(void) { return 1; }
 int64_t bh_kernel_launches(void) { return g_launches.load(); }
 
+int bh_set_profiling(int32_t on) {
+    g_profiling = on ? 1 : 0;
+    return BH_OK;
+}
+
+int bh_last_run_stats(bh_graph *g, bh_run_stats *out) {
+    return guarded([&] {
+        if (!g || !out) throw InvalidArg("null argument");
+        std::lock_guard<std::mutex> lock(g->mu);
+        EngineCache &c = cache_of(g);
+        *out = c.last ? c.last->stats : bh_run_stats{};
+    });
+}
+
 int bh_graph_create(int64_t n_u, int64_t n_v, int64_t n_e, const int64_t *u_indptr, const int32_t *u_indices,
                     const double *u_weights, const int64_t *v_indptr, const int32_t *v_indices,
                     const double *v_weights, const double *ws_u, const double *ws_v, int32_t device,
@@ -511,6 +572,7 @@ int bh_query_batch(bh_graph *g, const bh_query_params *p, const int32_t *sources
         cudaStream_t st = stream ? (cudaStream_t)stream : c.stream;
         const int B = p->slots > 0 ? p->slots : auto_slots(g, n_q);
         EngineBase &e = engine_for(g, B);
+        c.last = &e;
         RunSpec rs;
         rs.job = BH_JOB_BHPP;
         rs.n_q = n_q;
