@@ -94,22 +94,57 @@ __device__ void slot_finish(Slot &sl, Finish &f, bool has_pi) {
     sl.op = OP_IDLE;
 }
 
-__global__ void k_control(ControlArgs a) {
+constexpr int CONTROL_THREADS = 1024;
+
+__global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
     __shared__ int32_t s_free[MAX_B];
     __shared__ int32_t s_fin[MAX_B];
     __shared__ int32_t s_assign[MAX_B];
     __shared__ int32_t s_busy;
-    const int s = threadIdx.x;
+    // deterministic two-level reduction of the per-block partial rows:
+    // TPS threads per slot sum strided rows in order, then lane order
+    __shared__ int64_t r_cnt[CONTROL_THREADS];
+    __shared__ int64_t r_np[CONTROL_THREADS];
+    __shared__ double r_gam[CONTROL_THREADS];
+    __shared__ double r_sum[CONTROL_THREADS];
+    __shared__ int32_t r_any[CONTROL_THREADS];
+    const int tid = threadIdx.x;
     const int B = a.B;
     Control *ctl = a.ctl;
     if (ctl->active == 0 && !a.first) {
-        if (s == 0) ctl->n_fin = 0;
+        if (tid == 0) ctl->n_fin = 0;
         return;
     }
-    if (s == 0) {
+    if (tid == 0) {
         s_busy = 0;
         if (!a.first) ctl->rounds_active++;
     }
+    const int TPS = CONTROL_THREADS / B;
+    {
+        const int slot = tid / TPS, lane = tid % TPS;
+        int64_t cnt = 0, np = 0;
+        double gam = 0.0, sum = 0.0;
+        int32_t any = 0;
+        if (!a.first && slot < B) {
+            for (int r = lane; r < a.part.rows_k1; r += TPS) {
+                cnt += a.part.cnt[r * B + slot];
+                np += a.part.np_u[r * B + slot];
+                gam += a.part.gamma[r * B + slot];
+            }
+            for (int r = lane; r < a.part.rows_k2; r += TPS) np += a.part.np_v[r * B + slot];
+            for (int r = lane; r < a.part.rows_k3; r += TPS) {
+                any |= a.part.any[r * B + slot];
+                sum += a.part.sum[r * B + slot];
+            }
+        }
+        r_cnt[tid] = cnt;
+        r_np[tid] = np;
+        r_gam[tid] = gam;
+        r_sum[tid] = sum;
+        r_any[tid] = any;
+    }
+    __syncthreads();
+    const int s = tid;
     Slot sl;
     bool fin = false;
     if (s < B) {
@@ -117,19 +152,18 @@ __global__ void k_control(ControlArgs a) {
         const int op = a.first ? OP_IDLE : sl.op;
         if (op_is_push(op)) {
             sl.push_seq++;
-            int64_t cnt = 0, npu = 0, npv = 0;
+            int64_t cnt = 0, npt = 0;
             int32_t any = 0;
             double gam = 0.0, sum = 0.0;
-            for (int r = 0; r < a.part.rows_k1; r++) {
-                cnt += a.part.cnt[r * B + s];
-                npu += a.part.np_u[r * B + s];
-                gam += a.part.gamma[r * B + s];
+            for (int l = 0; l < TPS; l++) {
+                const int t = s * TPS + l;
+                cnt += r_cnt[t];
+                npt += r_np[t];
+                gam += r_gam[t];
+                sum += r_sum[t];
+                any |= r_any[t];
             }
-            for (int r = 0; r < a.part.rows_k2; r++) npv += a.part.np_v[r * B + s];
-            for (int r = 0; r < a.part.rows_k3; r++) {
-                any |= a.part.any[r * B + s];
-                sum += a.part.sum[r * B + s];
-            }
+            const int64_t npu = npt, npv = 0;
             const int64_t worked = cnt > 0;
             sl.n_p += npu + npv;
             bool end_backward = false;

@@ -136,7 +136,7 @@ struct Engine final : EngineBase {
         grid_pu = (int)std::max<int64_t>(1, std::min<int64_t>((g->U.n_units + PULL_WARPS - 1) / PULL_WARPS, (int64_t)occ_u * dev_sms));
         grid_fv = (int)std::max<int64_t>(1, std::min<int64_t>((g->V.n_splits + PULL_WARPS - 1) / PULL_WARPS, 4 * dev_sms));
         grid_fu = (int)std::max<int64_t>(1, std::min<int64_t>((g->U.n_splits + PULL_WARPS - 1) / PULL_WARPS, 4 * dev_sms));
-        grid_prep = grid1d(nu * B, PREP_THREADS, 8 * dev_sms);
+        grid_prep = grid1d(nu * B, PREP_THREADS, 2 * dev_sms);
         n_chunks = (int)((nu + fin_chunk - 1) / fin_chunk);
         grid_k5 = (int)std::min<int64_t>((int64_t)n_chunks * std::min(B, 8), 8 * dev_sms);
         const int rows = std::max({grid_prep, grid_pv + grid_fv, grid_pu + grid_fu});
@@ -251,7 +251,7 @@ struct Engine final : EngineBase {
             launches++;
         }
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 3), st));
-        k_control<<<1, std::max(32, B), 0, st>>>(ca);
+        k_control<<<1, CONTROL_THREADS, 0, st>>>(ca);
         k_finalize<T><<<grid_k5, TOPK_THREADS, 0, st>>>(fa);
         k_topk_merge<T><<<B, TOPK_THREADS, 0, st>>>(fa);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 4), st));
@@ -309,7 +309,7 @@ struct Engine final : EngineBase {
         ca.init_np = rs.init_np;
         ca.B = B;
         ca.first = 1;
-        k_control<<<1, std::max(32, B), 0, st>>>(ca);
+        k_control<<<1, CONTROL_THREADS, 0, st>>>(ca);
         count_launch();
         BH_CUDA(cudaGetLastError());
         ca.first = 0;
