@@ -89,8 +89,7 @@ typedef struct bh_graph_info {
     int64_t n_u, n_v, n_e;
     int32_t dtype, device;
     int64_t device_bytes;   /* graph store footprint                         */
-    int32_t units_u, units_v, split_rows_u, split_rows_v;
-    int32_t chunk_edges, reserved;
+    int64_t max_deg_u, max_deg_v;
 } bh_graph_info;
 
 /* Called after every push round of slot 0 in bh_push_run (the reference's

@@ -61,8 +61,7 @@ class GraphInfo(C.Structure):
     _fields_ = [
         ("n_u", C.c_int64), ("n_v", C.c_int64), ("n_e", C.c_int64),
         ("dtype", C.c_int32), ("device", C.c_int32), ("device_bytes", C.c_int64),
-        ("units_u", C.c_int32), ("units_v", C.c_int32), ("split_rows_u", C.c_int32),
-        ("split_rows_v", C.c_int32), ("chunk_edges", C.c_int32), ("reserved", C.c_int32),
+        ("max_deg_u", C.c_int64), ("max_deg_v", C.c_int64),
     ]
 
 

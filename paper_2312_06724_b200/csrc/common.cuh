@@ -32,23 +32,22 @@ struct InvalidArg : std::runtime_error {
 void count_launch(int n = 1);
 
 // ---------------------------------------------------------------------------
-// Work schedule of one pull side (rows = this side's nodes).  A unit is either
-// up to 32 whole rows holding <= chunk edges, or one piece (<= chunk edges) of
-// a row longer than `chunk`; pieces write fp64 partial sums to scratch and a
-// finisher warp adds them in piece order, so every row sum is deterministic.
-struct Unit {
-    int32_t row0;   // first row
-    int32_t nrows;  // rows in this unit (1 for a piece)
-    int64_t e0;     // first edge
-    int64_t e1;     // one past the last edge
-    int32_t piece;  // global piece index, -1 for whole rows
+// Static per-warp work of one pull side (rows = this side's nodes): a
+// contiguous edge range [e0, e1) chosen by a merge-path split of rows + edges.
+// Rows that straddle a range boundary ("cut rows") get one fp64 partial per
+// warp; the last warp to arrive adds them in warp order and finishes the row.
+struct WarpWork {
+    int64_t e0, e1;
+    int32_t r0;           // row containing e0
+    int32_t cut0, part0;  // cut-row index / partial slot of the first row (-1: whole)
+    int32_t cut1, part1;  // same for the last row when it differs from the first
     int32_t pad;
 };
 
-struct SplitRow {
+struct CutRow {
     int32_t row;
-    int32_t first_piece;
-    int32_t n_pieces;
+    int32_t n_parts;
+    int32_t first_part;
     int32_t pad;
 };
 
@@ -58,9 +57,7 @@ struct Side {
     int32_t *indices = nullptr;  // [E] column (other side) index
     void *vals = nullptr;        // [E] T, w / ws(row)
     int32_t *deg = nullptr;      // [n_rows]
-    Unit *units = nullptr;
-    SplitRow *splits = nullptr;
-    int32_t n_units = 0, n_splits = 0, n_pieces = 0;
+    std::vector<int64_t> h_indptr;  // host copy for the per-engine partition
 };
 
 }  // namespace bh
@@ -69,7 +66,6 @@ struct bh_graph {
     int device = 0;
     int dtype = BH_DTYPE_F64;
     int64_t n_u = 0, n_v = 0, n_e = 0;
-    int32_t chunk = 128;
     bh::Side U;  // rows u: cols v, vals w/ws(u)   (u_step, bigraph.py:148-155)
     bh::Side V;  // rows v: cols u, vals w/ws(v)   (v_step, bigraph.py:157-164)
     double *ws_u = nullptr;
@@ -94,6 +90,7 @@ enum Op : int32_t {
     OP_PIENTRY = 6,    // y0 := residue * ysc, first power iteration
     OP_PIENTRY0 = 7,   // y0 only (t == 0)
     OP_PI = 8,         // power iteration
+    OP_MEASURE = 9,    // reductions of the uploaded ledger only (pi_push entry gamma)
 };
 
 enum Phase : int32_t { PH_IDLE = 0, PH_BSEL, PH_SEQ, PH_FWD, PH_PI, PH_DONE };
@@ -131,13 +128,12 @@ struct Finish {
 
 // Deterministic per-round reductions: one row per producing block.
 struct Partials {
-    int64_t *cnt;    // [rows][B] |A| (K1)
-    int64_t *np_u;   // [rows][B] sum deg(A) (K1)
-    double *gamma;   // [rows][B] sum w_ratio * r (K1, FENTRY)
-    int64_t *np_v;   // [rows][B] sum deg over r_v > 0 (K2)
-    int32_t *any;    // [rows][B] any(r > threshold) (K3)
-    double *sum;     // [rows][B] sum r (K3, backward)
-    double *wsum;    // [rows][B] sum w_ratio * r (K3, forward)
+    int64_t *cnt;    // [rows_k1][B] |A| (K1 push)
+    int64_t *np_u;   // [rows_k1][B] sum deg(A) (K1 push)
+    int64_t *np_v;   // [rows_k2][B] sum deg over r_v > 0 (K2, one row per warp)
+    int32_t *any;    // [rows_k3][B] any(r > threshold) (K1a combine)
+    double *sum;     // [rows_k3][B] sum r (K1a)
+    double *wsum;    // [rows_k3][B] sum w_ratio * r (K1a)
     int rows_k1, rows_k2, rows_k3;  // valid rows (set by host per launch geometry)
 };
 
@@ -147,7 +143,9 @@ struct Control {
     int32_t n_q;       // queries in this batch
     int32_t n_fin;     // slots finishing this round
     int32_t rounds_active;  // rounds K4 processed with work in flight
+    int32_t arrive;         // K4 block arrival counter (last block assigns queries)
     int32_t fin_slots[256];
+    int32_t free_slot[256];
 };
 
 constexpr int MAX_B = 128;

@@ -55,7 +55,7 @@ __device__ void slot_start(Slot &sl, const ControlArgs &a, int32_t q) {
             sl.n_p_entry = a.init_np;
             sl.all_full = 1;
             sl.phase = PH_FWD;
-            sl.op = OP_FENTRY;
+            sl.op = OP_MEASURE;  // gamma of the seed ledger first, then forward rounds
             break;
         case BH_JOB_POWER:
             sl.phase = PH_PI;
@@ -94,78 +94,80 @@ __device__ void slot_finish(Slot &sl, Finish &f, bool has_pi) {
     sl.op = OP_IDLE;
 }
 
-constexpr int CONTROL_THREADS = 1024;
+constexpr int CONTROL_THREADS = 256;
 
+// One block per slot: deterministic reduction of the slot's partial rows, the
+// slot's state transition, then the last block to arrive refills free slots
+// from the query queue in slot order and publishes the round's flags.
 __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
-    __shared__ int32_t s_free[MAX_B];
-    __shared__ int32_t s_fin[MAX_B];
-    __shared__ int32_t s_assign[MAX_B];
-    __shared__ int32_t s_busy;
-    // deterministic two-level reduction of the per-block partial rows:
-    // TPS threads per slot sum strided rows in order, then lane order
     __shared__ int64_t r_cnt[CONTROL_THREADS];
     __shared__ int64_t r_np[CONTROL_THREADS];
-    __shared__ double r_gam[CONTROL_THREADS];
     __shared__ double r_sum[CONTROL_THREADS];
+    __shared__ double r_wsum[CONTROL_THREADS];
     __shared__ int32_t r_any[CONTROL_THREADS];
+    __shared__ int32_t s_last;
     const int tid = threadIdx.x;
+    const int s = blockIdx.x;
     const int B = a.B;
     Control *ctl = a.ctl;
     if (ctl->active == 0 && !a.first) {
-        if (tid == 0) ctl->n_fin = 0;
+        if (s == 0 && tid == 0) ctl->n_fin = 0;
         return;
     }
-    if (tid == 0) {
-        s_busy = 0;
-        if (!a.first) ctl->rounds_active++;
-    }
-    const int TPS = CONTROL_THREADS / B;
     {
-        const int slot = tid / TPS, lane = tid % TPS;
         int64_t cnt = 0, np = 0;
-        double gam = 0.0, sum = 0.0;
+        double sum = 0.0, wsum = 0.0;
         int32_t any = 0;
-        if (!a.first && slot < B) {
-            for (int r = lane; r < a.part.rows_k1; r += TPS) {
-                cnt += a.part.cnt[r * B + slot];
-                np += a.part.np_u[r * B + slot];
-                gam += a.part.gamma[r * B + slot];
+        if (!a.first) {
+            // partial rows are stored slot-major: [slot][row]
+            const int64_t *pc = a.part.cnt + (int64_t)s * a.part.rows_k1;
+            const int64_t *pn = a.part.np_u + (int64_t)s * a.part.rows_k1;
+            for (int r = tid; r < a.part.rows_k1; r += CONTROL_THREADS) {
+                cnt += pc[r];
+                np += pn[r];
             }
-            for (int r = lane; r < a.part.rows_k2; r += TPS) np += a.part.np_v[r * B + slot];
-            for (int r = lane; r < a.part.rows_k3; r += TPS) {
-                any |= a.part.any[r * B + slot];
-                sum += a.part.sum[r * B + slot];
+            const int64_t *pv = a.part.np_v + (int64_t)s * a.part.rows_k2;
+            for (int r = tid; r < a.part.rows_k2; r += CONTROL_THREADS) np += pv[r];
+            const int32_t *pa = a.part.any + (int64_t)s * a.part.rows_k3;
+            const double *ps = a.part.sum + (int64_t)s * a.part.rows_k3;
+            const double *pw = a.part.wsum + (int64_t)s * a.part.rows_k3;
+            for (int r = tid; r < a.part.rows_k3; r += CONTROL_THREADS) {
+                any |= pa[r];
+                sum += ps[r];
+                wsum += pw[r];
             }
         }
         r_cnt[tid] = cnt;
         r_np[tid] = np;
-        r_gam[tid] = gam;
         r_sum[tid] = sum;
+        r_wsum[tid] = wsum;
         r_any[tid] = any;
     }
     __syncthreads();
-    const int s = tid;
-    Slot sl;
-    bool fin = false;
-    if (s < B) {
-        sl = a.slots[s];
+    for (int off = CONTROL_THREADS / 2; off > 0; off >>= 1) {  // fixed-shape tree
+        if (tid < off) {
+            r_cnt[tid] += r_cnt[tid + off];
+            r_np[tid] += r_np[tid + off];
+            r_sum[tid] += r_sum[tid + off];
+            r_wsum[tid] += r_wsum[tid + off];
+            r_any[tid] |= r_any[tid + off];
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        Slot sl = a.slots[s];
+        bool fin = false;
         const int op = a.first ? OP_IDLE : sl.op;
-        if (op_is_push(op)) {
+        const int64_t cnt = r_cnt[0];
+        const int32_t any = r_any[0];
+        const double sum = r_sum[0], wsum = r_wsum[0];
+        if (op == OP_MEASURE) {  // pi_push entry: gamma of the uploaded ledger (push_engine.py:222)
+            sl.gamma = wsum;
+            sl.op = OP_FENTRY;
+        } else if (op_is_push(op)) {
             sl.push_seq++;
-            int64_t cnt = 0, npt = 0;
-            int32_t any = 0;
-            double gam = 0.0, sum = 0.0;
-            for (int l = 0; l < TPS; l++) {
-                const int t = s * TPS + l;
-                cnt += r_cnt[t];
-                npt += r_np[t];
-                gam += r_gam[t];
-                sum += r_sum[t];
-                any |= r_any[t];
-            }
-            const int64_t npu = npt, npv = 0;
             const int64_t worked = cnt > 0;
-            sl.n_p += npu + npv;
+            sl.n_p += r_np[0];
             bool end_backward = false;
             if (op == OP_BSEL_INIT || op == OP_BSEL) {
                 sl.sel_b += worked;
@@ -201,7 +203,6 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
                     end_backward = true;
                 }
             } else {  // forward round
-                if (op == OP_FENTRY) sl.gamma = gam;
                 sl.sel_f += worked;
                 sl.last_phase = BH_PHASE_FORWARD;
                 sl.last_rounds = sl.sel_f;
@@ -211,7 +212,7 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
                     sl.pi_t = 0;
                     fin = true;
                     slot_finish(sl, a.fin[s], false);
-                } else if (sum <= 0.0) {
+                } else if (wsum <= 0.0) {
                     sl.term_f = BH_TERM_DRAINED;
                     sl.pi_t = 0;
                     fin = true;
@@ -226,12 +227,12 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
                         brk = sl.tie_checks > sl.tie_skip;
                         if (brk) sl.tie_broke = 1;
                     } else {
-                        const double budget = a.budget_scale * (log(sl.gamma / sum) / a.log_decay);
+                        const double budget = a.budget_scale * (log(sl.gamma / wsum) / a.log_decay);
                         brk = (double)(sl.n_p - sl.n_p_entry) >= budget;
                     }
                     if (brk) {
                         sl.term_f = BH_TERM_BUDGET;
-                        sl.pi_t = required_iterations_dev(a.alpha, sl.eps_f, sum);
+                        sl.pi_t = required_iterations_dev(a.alpha, sl.eps_f, wsum);
                         sl.pi_done = 0;
                         sl.phase = PH_PI;
                         sl.op = sl.pi_t > 0 ? OP_PIENTRY : OP_PIENTRY0;
@@ -248,6 +249,7 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
                 } else {
                     sl.phase = PH_FWD;
                     sl.op = OP_FENTRY;
+                    sl.gamma = wsum;  // gamma at PI-Push entry (push_engine.py:222)
                     sl.n_p_entry = sl.n_p;
                     sl.all_full = 1;
                     sl.tie_checks = 0;
@@ -267,30 +269,62 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
                 sl.op = OP_PI;
             }
         }
-        s_fin[s] = fin;
-        s_free[s] = fin || sl.op == OP_IDLE;
-    }
-    __syncthreads();
-    if (s == 0) {
-        int32_t next = ctl->next_q;
-        int32_t nf = 0;
-        for (int i = 0; i < B; i++) {
-            s_assign[i] = -1;
-            if (s_free[i] && next < ctl->n_q) s_assign[i] = next++;
-            if (s_fin[i]) ctl->fin_slots[nf++] = i;
-        }
-        ctl->next_q = next;
-        ctl->n_fin = nf;
-    }
-    __syncthreads();
-    if (s < B) {
-        if (s_assign[s] >= 0) slot_start(sl, a, s_assign[s]);
-        else if (s_free[s]) sl.qidx = -1;
+        const bool free_now = fin || sl.op == OP_IDLE;
+        if (free_now) sl.qidx = fin ? sl.qidx : -1;
         a.slots[s] = sl;
-        if (sl.op != OP_IDLE) atomicOr(&s_busy, 1);
+        ctl->free_slot[s] = (free_now ? 1 : 0) | (fin ? 2 : 0);
+        __threadfence();
+        s_last = atomicAdd(&ctl->arrive, 1) == B - 1;
     }
     __syncthreads();
-    if (s == 0) ctl->active = s_busy;
+    if (!s_last) return;
+    // last block: refill free slots in slot order (prefix count), publish flags
+    __threadfence();
+    __shared__ int32_t f_free[MAX_B], f_fin[MAX_B], pre_free[MAX_B], pre_fin[MAX_B];
+    volatile Control *vc = ctl;
+    if (tid < B) {
+        const int32_t f = vc->free_slot[tid];
+        f_free[tid] = f & 1;
+        f_fin[tid] = (f >> 1) & 1;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int32_t a1 = 0, a2 = 0;
+        for (int i = 0; i < B; i++) {
+            pre_free[i] = a1;
+            pre_fin[i] = a2;
+            a1 += f_free[i];
+            a2 += f_fin[i];
+        }
+        s_last = a2;  // reuse: number finishing
+    }
+    __syncthreads();
+    const int32_t next0 = vc->next_q, n_q = vc->n_q;
+    int32_t busy = 0;
+    if (tid < B) {
+        if (f_fin[tid]) ctl->fin_slots[pre_fin[tid]] = tid;
+        const int32_t q = next0 + pre_free[tid];
+        if (f_free[tid] && q < n_q) {
+            Slot ns;
+            slot_start(ns, a, q);
+            a.slots[tid] = ns;
+            busy = ns.op != OP_IDLE;
+        } else {
+            if (f_free[tid]) a.slots[tid].qidx = -1;
+            busy = *(volatile int32_t *)&a.slots[tid].op != OP_IDLE;
+        }
+    }
+    busy = __syncthreads_or(busy);
+    if (tid == 0) {
+        int32_t nfree = 0;
+        for (int i = 0; i < B; i++) nfree += f_free[i];
+        ctl->next_q = min(n_q, next0 + nfree);
+        ctl->n_fin = s_last;
+        ctl->active = busy;
+        ctl->arrive = 0;
+        if (!a.first) ctl->rounds_active++;
+        __threadfence();
+    }
 }
 
 }  // namespace bh

@@ -91,10 +91,83 @@ struct EngineBase {
     int k_cap = 0;
 };
 
+// Merge-path partition of one pull side into n_warps contiguous edge ranges
+// balanced on (edges + ROWCOST * rows); rows cut by a boundary get one partial
+// slot per warp touching them (SURVEY.md sec. 7 hard part 3: hub rows of
+// ~1e6 edges must not serialise).
+struct SidePlan {
+    WarpWork *work = nullptr;
+    CutRow *cuts = nullptr;
+    int32_t *cut_count = nullptr;
+    int32_t n_warps = 0, n_cuts = 0, n_parts = 0;
+    int grid = 1;
+    void free_all() {
+        cudaFree(work);
+        cudaFree(cuts);
+        cudaFree(cut_count);
+        work = nullptr;
+        cuts = nullptr;
+        cut_count = nullptr;
+    }
+};
+
+static void build_plan(const Side &sd, int64_t n_e, int n_warps, SidePlan &pl) {
+    constexpr int64_t ROWCOST = 2;
+    const std::vector<int64_t> &ip = sd.h_indptr;
+    const int64_t n = sd.n_rows;
+    const int64_t total = n_e + ROWCOST * n;
+    std::vector<int64_t> eb((size_t)n_warps + 1);
+    eb[0] = 0;
+    eb[n_warps] = n_e;
+    for (int w = 1; w < n_warps; w++) {
+        const int64_t d = (int64_t)((__int128)total * w / n_warps);
+        int64_t lo = 0, hi = n;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) / 2;
+            if (ip[mid] + ROWCOST * mid <= d) lo = mid; else hi = mid - 1;
+        }
+        int64_t e = lo >= n ? n_e : std::min(std::max(d - ROWCOST * lo, ip[lo]), ip[lo + 1]);
+        eb[w] = std::max(e, eb[w - 1]);
+    }
+    std::vector<WarpWork> work((size_t)n_warps);
+    std::vector<CutRow> cuts;
+    int32_t parts = 0;
+    auto add_part = [&](int64_t row, int32_t &ci, int32_t &pi) {
+        if (cuts.empty() || cuts.back().row != (int32_t)row) cuts.push_back({(int32_t)row, 0, parts, 0});
+        ci = (int32_t)cuts.size() - 1;
+        pi = parts++;
+        cuts.back().n_parts++;
+    };
+    for (int w = 0; w < n_warps; w++) {
+        WarpWork &wk = work[w];
+        wk.e0 = eb[w];
+        wk.e1 = eb[w + 1];
+        wk.cut0 = wk.part0 = wk.cut1 = wk.part1 = -1;
+        wk.r0 = 0;
+        wk.pad = 0;
+        if (wk.e0 >= wk.e1) continue;
+        const int64_t r0 = std::upper_bound(ip.begin(), ip.end(), wk.e0) - ip.begin() - 1;
+        const int64_t rl = std::upper_bound(ip.begin(), ip.end(), wk.e1 - 1) - ip.begin() - 1;
+        wk.r0 = (int32_t)r0;
+        if (ip[r0] < wk.e0 || ip[r0 + 1] > wk.e1) add_part(r0, wk.cut0, wk.part0);
+        if (rl != r0 && ip[rl + 1] > wk.e1) add_part(rl, wk.cut1, wk.part1);
+    }
+    pl.n_warps = n_warps;
+    pl.n_cuts = (int32_t)cuts.size();
+    pl.n_parts = parts;
+    pl.work = dalloc<WarpWork>(work.size());
+    BH_CUDA(cudaMemcpy(pl.work, work.data(), work.size() * sizeof(WarpWork), cudaMemcpyHostToDevice));
+    pl.cuts = dalloc<CutRow>(std::max<size_t>(1, cuts.size()));
+    if (!cuts.empty()) BH_CUDA(cudaMemcpy(pl.cuts, cuts.data(), cuts.size() * sizeof(CutRow), cudaMemcpyHostToDevice));
+    pl.cut_count = dalloc<int32_t>(std::max<size_t>(1, cuts.size()));
+    BH_CUDA(cudaMemset(pl.cut_count, 0, std::max<size_t>(1, cuts.size()) * sizeof(int32_t)));
+}
+
 template <typename T, int B>
 struct Engine final : EngineBase {
+    static constexpr bool WIDE = B >= 32;
     bh_graph *g;
-    T *R = nullptr, *P = nullptr, *XV = nullptr;
+    T *R = nullptr, *P = nullptr, *XV = nullptr, *Y = nullptr;
     double *EST = nullptr, *OUTS = nullptr;
     Slot *slots = nullptr;
     Finish *fins = nullptr;
@@ -106,14 +179,22 @@ struct Engine final : EngineBase {
     int64_t *cand_idx = nullptr;
     double *hook_r = nullptr, *hook_est = nullptr;
     std::vector<cudaEvent_t> evpool;
+    SidePlan plan_v, plan_u;
+    size_t pull_smem = 0;
     int fin_chunk = 4096, n_chunks = 1;
-    int grid_prep = 1, grid_pv = 1, grid_pu = 1, grid_fv = 1, grid_fu = 1, grid_k5 = 1;
+    int grid_elem = 1, grid_k5 = 1;
+
+    static void pull_kernel(int side, void **fn) {
+        if constexpr (WIDE) *fn = side == SIDE_V ? (void *)k_pull<B, T, SIDE_V> : (void *)k_pull<B, T, SIDE_U>;
+        else *fn = side == SIDE_V ? (void *)k_pull_small<B, T, SIDE_V> : (void *)k_pull_small<B, T, SIDE_U>;
+    }
 
     explicit Engine(bh_graph *graph) : g(graph) {
         this->nslots = B;
         const int64_t nu = g->n_u, nv = g->n_v;
         R = dalloc<T>(nu * B);
         P = dalloc<T>(nu * B);
+        Y = dalloc<T>(nu * B);
         XV = dalloc<T>(nv * B);
         EST = dalloc<double>(nu * B);
         OUTS = dalloc<double>(nu * B);
@@ -123,49 +204,60 @@ struct Engine final : EngineBase {
         BH_CUDA(cudaMallocHost(&h_ctl, sizeof(Control)));
         BH_CUDA(cudaMemset(R, 0, nu * B * sizeof(T)));
         BH_CUDA(cudaMemset(P, 0, nu * B * sizeof(T)));
+        BH_CUDA(cudaMemset(Y, 0, nu * B * sizeof(T)));
         BH_CUDA(cudaMemset(XV, 0, nv * B * sizeof(T)));
         BH_CUDA(cudaMemset(EST, 0, nu * B * sizeof(double)));
-        int dev_sms = 148;
-        BH_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, g->device));
-        int occ_v = 1, occ_u = 1;
-        BH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_v, k_pull<B, T, SIDE_V>, PULL_THREADS, 0));
-        BH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_u, k_pull<B, T, SIDE_U>, PULL_THREADS, 0));
-        occ_v = std::max(1, occ_v);
-        occ_u = std::max(1, occ_u);
-        grid_pv = (int)std::max<int64_t>(1, std::min<int64_t>((g->V.n_units + PULL_WARPS - 1) / PULL_WARPS, (int64_t)occ_v * dev_sms));
-        grid_pu = (int)std::max<int64_t>(1, std::min<int64_t>((g->U.n_units + PULL_WARPS - 1) / PULL_WARPS, (int64_t)occ_u * dev_sms));
-        grid_fv = (int)std::max<int64_t>(1, std::min<int64_t>((g->V.n_splits + PULL_WARPS - 1) / PULL_WARPS, 4 * dev_sms));
-        grid_fu = (int)std::max<int64_t>(1, std::min<int64_t>((g->U.n_splits + PULL_WARPS - 1) / PULL_WARPS, 4 * dev_sms));
-        grid_prep = grid1d(nu * B, PREP_THREADS, 2 * dev_sms);
+        BH_CUDA(cudaMemset(ctl, 0, sizeof(Control)));
+        int sms = 148;
+        BH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
+        if constexpr (WIDE) pull_smem = (size_t)PULL_WARPS * Pipe<B, T>::WARP_SMEM;
+        for (int side = 0; side < 2; side++) {
+            void *fn;
+            pull_kernel(side, &fn);
+            if (pull_smem > 48 * 1024)
+                BH_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pull_smem));
+            int occ = 1;
+            BH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, PULL_THREADS, pull_smem));
+            occ = std::max(1, occ);
+            const Side &sd = side == SIDE_V ? g->V : g->U;
+            SidePlan &pl = side == SIDE_V ? plan_v : plan_u;
+            // one resident wave of warps, fewer if the side is tiny
+            int64_t grid = (int64_t)occ * sms;
+            const int64_t want = (g->n_e + 2 * sd.n_rows) / 64 / PULL_WARPS + 1;
+            grid = std::max<int64_t>(1, std::min(grid, want));
+            pl.grid = (int)grid;
+            build_plan(sd, g->n_e, (int)grid * PULL_WARPS, pl);
+        }
+        grid_elem = grid1d(nu * (B / ElemGeo<B>::EV), ELEM_THREADS, 4 * sms);
         n_chunks = (int)((nu + fin_chunk - 1) / fin_chunk);
-        grid_k5 = (int)std::min<int64_t>((int64_t)n_chunks * std::min(B, 8), 8 * dev_sms);
-        const int rows = std::max({grid_prep, grid_pv + grid_fv, grid_pu + grid_fu});
-        part.cnt = dalloc<int64_t>((size_t)rows * B);
-        part.np_u = dalloc<int64_t>((size_t)rows * B);
-        part.gamma = dalloc<double>((size_t)rows * B);
-        part.np_v = dalloc<int64_t>((size_t)rows * B);
-        part.any = dalloc<int32_t>((size_t)rows * B);
-        part.sum = dalloc<double>((size_t)rows * B);
-        part.wsum = part.sum;
-        part.rows_k1 = grid_prep;
-        part.rows_k2 = grid_pv + (g->V.n_splits ? grid_fv : 0);
-        part.rows_k3 = grid_pu + (g->U.n_splits ? grid_fu : 0);
-        BH_CUDA(cudaMemset(part.np_v, 0, (size_t)rows * B * sizeof(int64_t)));
-        BH_CUDA(cudaMemset(part.any, 0, (size_t)rows * B * sizeof(int32_t)));
-        BH_CUDA(cudaMemset(part.sum, 0, (size_t)rows * B * sizeof(double)));
-        const int64_t pieces = std::max<int64_t>(1, std::max(g->U.n_pieces, g->V.n_pieces));
-        scratch = dalloc<double>((size_t)pieces * B);
+        grid_k5 = (int)std::min<int64_t>((int64_t)n_chunks * std::min(B, 8), 8 * sms);
+        part.rows_k1 = grid_elem;
+        part.rows_k2 = plan_v.n_warps;
+        part.rows_k3 = grid_elem;
+        part.cnt = dalloc<int64_t>((size_t)grid_elem * B);
+        part.np_u = dalloc<int64_t>((size_t)grid_elem * B);
+        part.np_v = dalloc<int64_t>((size_t)plan_v.n_warps * B);
+        part.any = dalloc<int32_t>((size_t)grid_elem * B);
+        part.sum = dalloc<double>((size_t)grid_elem * B);
+        part.wsum = dalloc<double>((size_t)grid_elem * B);
+        BH_CUDA(cudaMemset(part.np_v, 0, (size_t)plan_v.n_warps * B * sizeof(int64_t)));
+        BH_CUDA(cudaMemset(part.cnt, 0, (size_t)grid_elem * B * sizeof(int64_t)));
+        BH_CUDA(cudaMemset(part.np_u, 0, (size_t)grid_elem * B * sizeof(int64_t)));
+        const int64_t parts = std::max<int64_t>(1, std::max(plan_u.n_parts, plan_v.n_parts));
+        scratch = dalloc<double>((size_t)parts * B);
         hook_r = dalloc<double>(nu);
         hook_est = dalloc<double>(nu);
     }
 
     ~Engine() override {
-        cudaFree(R); cudaFree(P); cudaFree(XV); cudaFree(EST); cudaFree(OUTS);
+        cudaFree(R); cudaFree(P); cudaFree(Y); cudaFree(XV); cudaFree(EST); cudaFree(OUTS);
         cudaFree(slots); cudaFree(fins); cudaFree(ctl); cudaFreeHost(h_ctl);
-        cudaFree(part.cnt); cudaFree(part.np_u); cudaFree(part.gamma); cudaFree(part.np_v);
-        cudaFree(part.any); cudaFree(part.sum);
+        cudaFree(part.cnt); cudaFree(part.np_u); cudaFree(part.np_v);
+        cudaFree(part.any); cudaFree(part.sum); cudaFree(part.wsum);
         cudaFree(scratch); cudaFree(cand_key); cudaFree(cand_idx);
         cudaFree(hook_r); cudaFree(hook_est);
+        plan_u.free_all();
+        plan_v.free_all();
         for (auto e : evpool) cudaEventDestroy(e);
     }
 
@@ -187,93 +279,88 @@ struct Engine final : EngineBase {
         k_cap = k;
     }
 
-    PullArgs<T> pull_args(int side) {
+    PullArgs<T> pull_args(int side, double one_minus_alpha) {
         PullArgs<T> a{};
         const Side &sd = side == SIDE_V ? g->V : g->U;
+        const SidePlan &pl = side == SIDE_V ? plan_v : plan_u;
         a.indptr = sd.indptr;
+        a.n_rows = sd.n_rows;
         a.indices = sd.indices;
         a.vals = (const T *)sd.vals;
-        a.units = sd.units;
-        a.n_units = sd.n_units;
-        a.splits = sd.splits;
-        a.n_splits = sd.n_splits;
+        a.work = pl.work;
+        a.cuts = pl.cuts;
+        a.cut_count = pl.cut_count;
         a.scratch = scratch;
+        a.n_warps = pl.n_warps;
         a.X = side == SIDE_V ? P : XV;
-        a.Y = side == SIDE_V ? XV : R;
-        a.P = P;
-        a.ws_u = g->ws_u;
-        a.inv_ws_u = g->inv_ws_u;
+        a.Y = side == SIDE_V ? XV : Y;
         a.slots = slots;
         a.active = &ctl->active;
-        a.part = part;
+        a.np_v = part.np_v;
+        a.one_minus_alpha = one_minus_alpha;
         return a;
+    }
+
+    void launch_pull(int side, const PullArgs<T> &a, cudaStream_t st) {
+        const int grid = side == SIDE_V ? plan_v.grid : plan_u.grid;
+        if constexpr (WIDE) {
+            if (side == SIDE_V) k_pull<B, T, SIDE_V><<<grid, PULL_THREADS, pull_smem, st>>>(a);
+            else k_pull<B, T, SIDE_U><<<grid, PULL_THREADS, pull_smem, st>>>(a);
+        } else {
+            if (side == SIDE_V) k_pull_small<B, T, SIDE_V><<<grid, PULL_THREADS, 0, st>>>(a);
+            else k_pull_small<B, T, SIDE_U><<<grid, PULL_THREADS, 0, st>>>(a);
+        }
     }
 
     void launch_round(const RunSpec &rs, const ControlArgs &ca, const FinalArgs<T> &fa, cudaStream_t st,
                       int64_t round, bool prof) {
-        const size_t e0 = (size_t)round * 5;
+        const size_t e0 = (size_t)round * 6;
+        ElemArgs<T> ea{};
+        ea.n_u = g->n_u;
+        ea.R = R;
+        ea.P = P;
+        ea.Y = Y;
+        ea.EST = EST;
+        ea.deg_u = g->U.deg;
+        ea.ws_u = g->ws_u;
+        ea.inv_ws_u = g->inv_ws_u;
+        ea.x0 = rs.x0;
+        ea.slots = slots;
+        ea.active = &ctl->active;
+        ea.part = part;
+        ea.alpha = rs.alpha;
         if (prof) BH_CUDA(cudaEventRecord(ev(e0), st));
-        PrepArgs<T> pa{};
-        pa.n_u = g->n_u;
-        pa.R = R;
-        pa.P = P;
-        pa.EST = EST;
-        pa.deg_u = g->U.deg;
-        pa.ws_u = g->ws_u;
-        pa.inv_ws_u = g->inv_ws_u;
-        pa.x0 = rs.x0;
-        pa.slots = slots;
-        pa.active = &ctl->active;
-        pa.part = part;
-        pa.alpha = rs.alpha;
-        k_prep<B, T><<<grid_prep, PREP_THREADS, 0, st>>>(pa);
+        k_push<B, T><<<grid_elem, ELEM_THREADS, 0, st>>>(ea);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 1), st));
-
-        PullArgs<T> av = pull_args(SIDE_V);
-        av.one_minus_alpha = 1.0 - rs.alpha;
-        av.part_row0 = 0;
-        k_pull<B, T, SIDE_V><<<grid_pv, PULL_THREADS, 0, st>>>(av);
-        int launches = 2;
-        if (g->V.n_splits) {
-            av.part_row0 = grid_pv;
-            k_pull_finish<B, T, SIDE_V><<<grid_fv, PULL_THREADS, 0, st>>>(av);
-            launches++;
-        }
+        launch_pull(SIDE_V, pull_args(SIDE_V, 1.0 - rs.alpha), st);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 2), st));
-        PullArgs<T> au = pull_args(SIDE_U);
-        au.one_minus_alpha = 1.0 - rs.alpha;
-        au.part_row0 = 0;
-        k_pull<B, T, SIDE_U><<<grid_pu, PULL_THREADS, 0, st>>>(au);
-        launches++;
-        if (g->U.n_splits) {
-            au.part_row0 = grid_pu;
-            k_pull_finish<B, T, SIDE_U><<<grid_fu, PULL_THREADS, 0, st>>>(au);
-            launches++;
-        }
+        launch_pull(SIDE_U, pull_args(SIDE_U, 1.0 - rs.alpha), st);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 3), st));
-        k_control<<<1, CONTROL_THREADS, 0, st>>>(ca);
+        k_combine<B, T><<<grid_elem, ELEM_THREADS, 0, st>>>(ea);
+        if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 4), st));
+        k_control<<<B, CONTROL_THREADS, 0, st>>>(ca);
         k_finalize<T><<<grid_k5, TOPK_THREADS, 0, st>>>(fa);
         k_topk_merge<T><<<B, TOPK_THREADS, 0, st>>>(fa);
-        if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 4), st));
-        launches += 3;
+        if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 5), st));
+        const int launches = 7;
         count_launch(launches);
         stats.launches += launches;
         BH_CUDA(cudaGetLastError());
     }
 
     void collect_profile(int64_t rounds) {
-        double t[4] = {0, 0, 0, 0};
+        double t[5] = {0, 0, 0, 0, 0};
         for (int64_t r = 0; r < rounds; r++) {
-            for (int j = 0; j < 4; j++) {
+            for (int j = 0; j < 5; j++) {
                 float ms = 0.f;
-                BH_CUDA(cudaEventElapsedTime(&ms, ev((size_t)r * 5 + j), ev((size_t)r * 5 + j + 1)));
+                BH_CUDA(cudaEventElapsedTime(&ms, ev((size_t)r * 6 + j), ev((size_t)r * 6 + j + 1)));
                 t[j] += ms;
             }
         }
-        stats.ms_prep = t[0];
+        stats.ms_prep = t[0] + t[3];
         stats.ms_vpull = t[1];
         stats.ms_upull = t[2];
-        stats.ms_control = t[3];
+        stats.ms_control = t[4];
         stats.profiled = 1;
     }
 
@@ -283,9 +370,7 @@ struct Engine final : EngineBase {
         BH_CUDA(cudaMemsetAsync(slots, 0, sizeof(Slot) * B, st));
         Control c0{};
         c0.active = 1;
-        c0.next_q = 0;
         c0.n_q = (int32_t)rs.n_q;
-        c0.n_fin = 0;
         *h_ctl = c0;
         BH_CUDA(cudaMemcpyAsync(ctl, h_ctl, sizeof(Control), cudaMemcpyHostToDevice, st));
 
@@ -309,7 +394,7 @@ struct Engine final : EngineBase {
         ca.init_np = rs.init_np;
         ca.B = B;
         ca.first = 1;
-        k_control<<<1, CONTROL_THREADS, 0, st>>>(ca);
+        k_control<<<B, CONTROL_THREADS, 0, st>>>(ca);
         count_launch();
         BH_CUDA(cudaGetLastError());
         ca.first = 0;
@@ -548,12 +633,11 @@ int bh_graph_get_info(const bh_graph *g, bh_graph_info *out) {
         out->dtype = g->dtype;
         out->device = g->device;
         out->device_bytes = g->device_bytes;
-        out->units_u = g->U.n_units;
-        out->units_v = g->V.n_units;
-        out->split_rows_u = g->U.n_splits;
-        out->split_rows_v = g->V.n_splits;
-        out->chunk_edges = g->chunk;
-        out->reserved = 0;
+        int64_t mu = 0, mv = 0;
+        for (int64_t r = 0; r < g->n_u; r++) mu = std::max(mu, g->U.h_indptr[r + 1] - g->U.h_indptr[r]);
+        for (int64_t r = 0; r < g->n_v; r++) mv = std::max(mv, g->V.h_indptr[r + 1] - g->V.h_indptr[r]);
+        out->max_deg_u = mu;
+        out->max_deg_v = mv;
     });
 }
 

@@ -60,47 +60,9 @@ X *dmalloc(size_t count, int64_t &acc) {
     return (X *)p;
 }
 
-void build_schedule(Side &s, const int64_t *h_indptr, int32_t chunk, int64_t &acc) {
-    std::vector<Unit> units;
-    std::vector<SplitRow> splits;
-    int32_t piece = 0;
-    const int64_t n = s.n_rows;
-    units.reserve((size_t)(n / 8 + 16));
-    int64_t r = 0;
-    while (r < n) {
-        int64_t d = h_indptr[r + 1] - h_indptr[r];
-        if (d > chunk) {
-            int32_t np = (int32_t)((d + chunk - 1) / chunk);
-            splits.push_back({(int32_t)r, piece, np, 0});
-            for (int32_t p = 0; p < np; p++) {
-                int64_t e0 = h_indptr[r] + (int64_t)p * chunk;
-                int64_t e1 = std::min<int64_t>(e0 + chunk, h_indptr[r + 1]);
-                units.push_back({(int32_t)r, 1, e0, e1, piece++, 0});
-            }
-            r++;
-            continue;
-        }
-        int64_t r0 = r, e0 = h_indptr[r];
-        while (r < n && r - r0 < 32) {
-            int64_t dd = h_indptr[r + 1] - h_indptr[r];
-            if (dd > chunk || h_indptr[r + 1] - e0 > chunk) break;
-            r++;
-        }
-        units.push_back({(int32_t)r0, (int32_t)(r - r0), e0, h_indptr[r], -1, 0});
-    }
-    s.n_units = (int32_t)units.size();
-    s.n_splits = (int32_t)splits.size();
-    s.n_pieces = piece;
-    s.units = dmalloc<Unit>(units.size(), acc);
-    BH_CUDA(cudaMemcpy(s.units, units.data(), units.size() * sizeof(Unit), cudaMemcpyHostToDevice));
-    s.splits = dmalloc<SplitRow>(std::max<size_t>(1, splits.size()), acc);
-    if (!splits.empty())
-        BH_CUDA(cudaMemcpy(s.splits, splits.data(), splits.size() * sizeof(SplitRow), cudaMemcpyHostToDevice));
-}
-
 template <typename T>
 void upload_side(Side &s, int64_t n_rows, int64_t n_e, const int64_t *indptr, const int32_t *indices,
-                 const double *w, const double *ws_rows, int32_t chunk, int64_t &acc) {
+                 const double *w, const double *ws_rows, int64_t &acc) {
     s.n_rows = n_rows;
     s.indptr = dmalloc<int64_t>(n_rows + 1, acc);
     s.indices = dmalloc<int32_t>(n_e, acc);
@@ -122,7 +84,7 @@ void upload_side(Side &s, int64_t n_rows, int64_t n_e, const int64_t *indptr, co
     BH_CUDA(cudaDeviceSynchronize());
     cudaFree(dw);
     cudaFree(dws);
-    build_schedule(s, indptr, chunk, acc);
+    s.h_indptr.assign(indptr, indptr + n_rows + 1);
 }
 
 void free_side(Side &s) {
@@ -130,17 +92,7 @@ void free_side(Side &s) {
     cudaFree(s.indices);
     cudaFree(s.vals);
     cudaFree(s.deg);
-    cudaFree(s.units);
-    cudaFree(s.splits);
     s = Side{};
-}
-
-int32_t pick_chunk(int64_t n_e) {
-    // ~9.5k units of work for 148 SMs x 32 resident warps x 2, as a power of two
-    int64_t target = n_e / 9472;
-    int32_t c = 32;
-    while (c < target && c < 2048) c <<= 1;
-    return c;
 }
 
 void validate(int64_t n_u, int64_t n_v, int64_t n_e, const int64_t *u_indptr, const int32_t *u_indices,
@@ -178,15 +130,14 @@ bh_graph *graph_create(int64_t n_u, int64_t n_v, int64_t n_e, const int64_t *u_i
     g->n_u = n_u;
     g->n_v = n_v;
     g->n_e = n_e;
-    g->chunk = pick_chunk(n_e);
     try {
         int64_t acc = 0;
         if (dtype == BH_DTYPE_F64) {
-            upload_side<double>(g->U, n_u, n_e, u_indptr, u_indices, u_weights, ws_u, g->chunk, acc);
-            upload_side<double>(g->V, n_v, n_e, v_indptr, v_indices, v_weights, ws_v, g->chunk, acc);
+            upload_side<double>(g->U, n_u, n_e, u_indptr, u_indices, u_weights, ws_u, acc);
+            upload_side<double>(g->V, n_v, n_e, v_indptr, v_indices, v_weights, ws_v, acc);
         } else {
-            upload_side<float>(g->U, n_u, n_e, u_indptr, u_indices, u_weights, ws_u, g->chunk, acc);
-            upload_side<float>(g->V, n_v, n_e, v_indptr, v_indices, v_weights, ws_v, g->chunk, acc);
+            upload_side<float>(g->U, n_u, n_e, u_indptr, u_indices, u_weights, ws_u, acc);
+            upload_side<float>(g->V, n_v, n_e, v_indptr, v_indices, v_weights, ws_v, acc);
         }
         g->ws_u = dmalloc<double>(n_u, acc);
         g->inv_ws_u = dmalloc<double>(n_u, acc);

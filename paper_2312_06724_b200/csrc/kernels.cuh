@@ -1,23 +1,29 @@
 // kernels.cuh -- device kernels of one push / power-iteration round over a
 // block of B query slots (node-major, slot-minor state: X[node * B + slot]).
 //
-// Round = K1 prep -> K2 V-pull (+K2b finisher) -> K3 U-pull (+K3b) -> K4 control
+// Round = K1 push -> K2 V-pull -> K3 U-pull -> K1a combine -> K4 control
 //         [-> K5 finalize/score chunks -> K6 top-k merge, when a slot finishes]
 //
 // Reference semantics (pkg/src/bipush/push_engine.py):
-//   K1  _push_u bookkeeping (294-309): A = {r_u > theta}, est[A] += alpha r_u,
-//       r_u[A] = 0, n_p += sum deg(A); the pushed amounts go to P.
-//   K2  _push_u's r_v += (1-alpha) * v_step @ dense (303-306) as a pull over
-//       V-CSR; n_p += deg(v) for r_v > 0 (the flushed set, 312-324).
-//   K3  _flush_v's r_u += u_step @ r_v (322) as a pull over U-CSR, plus the
-//       per-query reductions the round's exit tests need (any r_u > theta,
-//       sum r_u, sum w_ratio r_u; 168-177, 234-243).
+//   K1   _push_u bookkeeping (294-309): A = {r_u > theta}, est[A] += alpha r_u,
+//        r_u[A] = 0, n_p += sum deg(A); the pushed amounts go to P.
+//   K2   _push_u's r_v = (1-alpha) * v_step @ dense (303-306) as a pull over
+//        V-CSR; n_p += deg(v) for r_v > 0 (the flushed set, 312-324).
+//   K3   _flush_v's u_step @ r_v (322) as a pull over U-CSR -> Y.
+//   K1a  r_u += Y, plus the per-query reductions the exit tests need
+//        (any r_u > theta, sum r_u, sum w_ratio r_u; 168-177, 234-243).
 //   Power iteration (101-117) runs the same K2/K3 pair on a = acc / ws:
-//       a <- y0 + U (1-alpha) V a   (detailed balance).
-// Every row sum is a sequential fp64 accumulation in CSR order; long rows are
-// split into pieces whose partials a finisher adds in piece order, and every
-// per-query reduction goes through per-block partial rows summed in order by
-// K4.  Results are therefore bitwise deterministic run to run.
+//        a <- y0 + U (1-alpha) V a   (detailed balance).
+//
+// The pulls are gather-bound SpMMs: every edge reads one B-wide operand row
+// (B * sizeof(T) bytes).  Each warp owns a contiguous, cost-balanced edge range
+// (merge-path over rows + edges, built per engine) and streams the operand
+// rows through a per-warp shared-memory ring with cp.async, S edges deep, so
+// the gathers of the next S edges are in flight while the current one is
+// accumulated in fp64.  Rows cut by a range boundary are finished by the last
+// warp to arrive, which adds the fp64 partials in warp order.  Every row sum is
+// therefore a fixed-order fp64 accumulation and every per-query reduction goes
+// through per-block partial rows summed in a fixed order: bitwise deterministic.
 #pragma once
 
 #include "common.cuh"
@@ -27,22 +33,19 @@ namespace bh {
 // ---------------------------------------------------------------------------
 // small helpers
 
+__device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+
 template <typename T, int VEC>
 struct VecIO;
 
 template <>
 struct VecIO<float, 1> {
-    static __device__ __forceinline__ void ld(const float *p, float (&v)[1]) { v[0] = __ldg(p); }
-    static __device__ __forceinline__ void ldc(const float *p, float (&v)[1]) { v[0] = *p; }
+    static __device__ __forceinline__ void ld(const float *p, float (&v)[1]) { v[0] = *p; }
     static __device__ __forceinline__ void st(float *p, const float (&v)[1]) { *p = v[0]; }
 };
 template <>
 struct VecIO<float, 2> {
     static __device__ __forceinline__ void ld(const float *p, float (&v)[2]) {
-        float2 t = __ldg(reinterpret_cast<const float2 *>(p));
-        v[0] = t.x; v[1] = t.y;
-    }
-    static __device__ __forceinline__ void ldc(const float *p, float (&v)[2]) {
         float2 t = *reinterpret_cast<const float2 *>(p);
         v[0] = t.x; v[1] = t.y;
     }
@@ -53,10 +56,6 @@ struct VecIO<float, 2> {
 template <>
 struct VecIO<float, 4> {
     static __device__ __forceinline__ void ld(const float *p, float (&v)[4]) {
-        float4 t = __ldg(reinterpret_cast<const float4 *>(p));
-        v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
-    }
-    static __device__ __forceinline__ void ldc(const float *p, float (&v)[4]) {
         float4 t = *reinterpret_cast<const float4 *>(p);
         v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
     }
@@ -66,17 +65,12 @@ struct VecIO<float, 4> {
 };
 template <>
 struct VecIO<double, 1> {
-    static __device__ __forceinline__ void ld(const double *p, double (&v)[1]) { v[0] = __ldg(p); }
-    static __device__ __forceinline__ void ldc(const double *p, double (&v)[1]) { v[0] = *p; }
+    static __device__ __forceinline__ void ld(const double *p, double (&v)[1]) { v[0] = *p; }
     static __device__ __forceinline__ void st(double *p, const double (&v)[1]) { *p = v[0]; }
 };
 template <>
 struct VecIO<double, 2> {
     static __device__ __forceinline__ void ld(const double *p, double (&v)[2]) {
-        double2 t = __ldg(reinterpret_cast<const double2 *>(p));
-        v[0] = t.x; v[1] = t.y;
-    }
-    static __device__ __forceinline__ void ldc(const double *p, double (&v)[2]) {
         double2 t = *reinterpret_cast<const double2 *>(p);
         v[0] = t.x; v[1] = t.y;
     }
@@ -87,11 +81,6 @@ struct VecIO<double, 2> {
 template <>
 struct VecIO<double, 4> {
     static __device__ __forceinline__ void ld(const double *p, double (&v)[4]) {
-        double2 a = __ldg(reinterpret_cast<const double2 *>(p));
-        double2 b = __ldg(reinterpret_cast<const double2 *>(p) + 1);
-        v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
-    }
-    static __device__ __forceinline__ void ldc(const double *p, double (&v)[4]) {
         double2 a = *reinterpret_cast<const double2 *>(p);
         double2 b = *(reinterpret_cast<const double2 *>(p) + 1);
         v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
@@ -102,25 +91,25 @@ struct VecIO<double, 4> {
     }
 };
 
-__device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
-
 __device__ __forceinline__ bool op_is_push(int op) { return op >= OP_BSEL_INIT && op <= OP_FSEL; }
 __device__ __forceinline__ bool op_is_fwd(int op) { return op == OP_FENTRY || op == OP_FSEL; }
 
-// ---------------------------------------------------------------------------
-// Launch geometry shared by host and device.
-template <int B>
-struct Geo {
-    static constexpr int G = B < 32 ? B : 32;     // lanes per edge group
-    static constexpr int EPW = 32 / G;            // edges in flight per warp step
-    static constexpr int VEC = B / G;             // slots per lane
-};
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-constexpr int PULL_THREADS = 256;
-constexpr int PULL_WARPS = PULL_THREADS / 32;
-constexpr int PREP_THREADS = 256;
+template <int BYTES>
+__device__ __forceinline__ void cp_async(uint32_t dst, const void *src) {
+    if constexpr (BYTES == 16)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+    else if constexpr (BYTES == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-// Per-slot constants staged in shared memory by every round kernel.
+// Per-slot constants staged in shared memory by the round kernels.
 struct SlotSmem {
     int32_t op[MAX_B];
     int32_t qidx[MAX_B];
@@ -148,12 +137,21 @@ __device__ __forceinline__ void load_slot_smem(SlotSmem &sm, const Slot *__restr
 }
 
 // ---------------------------------------------------------------------------
-// K1: prep.  Elementwise over [n_u x B].
+// Elementwise kernels over [n_u x B]: one thread per (node, EV consecutive slots).
+constexpr int ELEM_THREADS = 256;
+
+template <int B>
+struct ElemGeo {
+    static constexpr int EV = B >= 4 ? 4 : B;   // slots per thread
+    static constexpr int TPN = B / EV;          // threads per node
+};
+
 template <typename T>
-struct PrepArgs {
+struct ElemArgs {
     int64_t n_u;
     T *R;
     T *P;
+    T *Y;
     double *EST;
     const int32_t *deg_u;
     const double *ws_u;
@@ -165,365 +163,509 @@ struct PrepArgs {
     double alpha;
 };
 
+// K1: push (and ledger init / power-iteration entry) for the coming round.
 template <int B, typename T>
-__global__ void __launch_bounds__(PREP_THREADS) k_prep(PrepArgs<T> a) {
+__global__ void __launch_bounds__(ELEM_THREADS) k_push(ElemArgs<T> a) {
     if (*a.active == 0) return;
+    using EG = ElemGeo<B>;
+    constexpr int EV = EG::EV, TPN = EG::TPN;
     __shared__ SlotSmem sm;
-    __shared__ int64_t red_cnt[PREP_THREADS];
-    __shared__ int64_t red_np[PREP_THREADS];
-    __shared__ double red_g[PREP_THREADS];
+    __shared__ int64_t red_cnt[ELEM_THREADS * EV];
+    __shared__ int64_t red_np[ELEM_THREADS * EV];
     load_slot_smem<B>(sm, a.slots);
     __syncthreads();
-    const int s = threadIdx.x & (B - 1);
-    const int op = sm.op[s];
-    const bool push = op_is_push(op);
-    const bool init = op == OP_BSEL_INIT;
-    const bool fentry = op == OP_FENTRY;
-    const bool fwd = op_is_fwd(op);
-    const bool pientry = op == OP_PIENTRY || op == OP_PIENTRY0;
-    const double eps_b = sm.eps_b[s];
-    const double thc = sm.thc[s], wsq = sm.wsq[s], iwsq = sm.iwsq[s], ysc = sm.ysc[s];
-    const int src = sm.src[s];
-    const double *x0 = (a.x0 && sm.qidx[s] >= 0) ? a.x0 + (int64_t)sm.qidx[s] * a.n_u : nullptr;
-    int64_t cnt = 0, npu = 0;
-    double gam = 0.0;
-    if (push || pientry) {
-        const int64_t total = a.n_u * B;
-        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-             i += (int64_t)gridDim.x * blockDim.x) {
-            const int64_t u = i / B;
-            double r = init ? (u == src ? 1.0 : 0.0) : (double)a.R[i];
-            if (pientry) {
-                if (x0) {  // raw power iteration: y0 = start / ws (push_engine.py:112, in a = acc / ws)
-                    const T y = (T)(x0[u] * a.inv_ws_u[u]);
-                    a.R[i] = y;
-                    a.P[i] = y;
-                } else {  // PI-Push tail: y0 = (w_ratio r) / ws = r / ws(q)  (push_engine.py:246)
-                    a.P[i] = (T)(r * ysc);
+    const int j0 = (threadIdx.x % TPN) * EV;  // first slot of this thread (fixed: blockDim % TPN == 0)
+    int op[EV];
+    bool any_work = false;
+#pragma unroll
+    for (int v = 0; v < EV; v++) {
+        op[v] = sm.op[j0 + v];
+        any_work |= op_is_push(op[v]) || op[v] == OP_PIENTRY || op[v] == OP_PIENTRY0;
+    }
+    int64_t cnt[EV], npu[EV];
+#pragma unroll
+    for (int v = 0; v < EV; v++) cnt[v] = npu[v] = 0;
+    if (any_work) {
+        const int64_t total = a.n_u * TPN;
+        for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+             t += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t u = t / TPN;
+            const int64_t i = u * B + j0;
+            T rv[EV];
+            VecIO<T, EV>::ld(a.R + i, rv);
+            const double iws = a.inv_ws_u[u];
+            const int32_t deg = a.deg_u[u];
+            T pv[EV];
+            bool wrote_r = false;
+#pragma unroll
+            for (int v = 0; v < EV; v++) {
+                const int s = j0 + v;
+                const int o = op[v];
+                pv[v] = (T)0;
+                if (o == OP_PIENTRY || o == OP_PIENTRY0) {
+                    const double *x0 = (a.x0 && sm.qidx[s] >= 0) ? a.x0 + (int64_t)sm.qidx[s] * a.n_u : nullptr;
+                    if (x0) {  // raw power iteration: y0 = start / ws  (push_engine.py:112, on a = acc / ws)
+                        const T y = (T)(x0[u] * iws);
+                        rv[v] = y;
+                        pv[v] = y;
+                        wrote_r = true;
+                    } else {   // PI-Push tail: y0 = (w_ratio r) / ws = r / ws(q)  (push_engine.py:246)
+                        pv[v] = (T)((double)rv[v] * sm.ysc[s]);
+                    }
+                } else if (op_is_push(o)) {
+                    const bool init = o == OP_BSEL_INIT;
+                    const double r = init ? (u == sm.src[s] ? 1.0 : 0.0) : (double)rv[v];
+                    double th;
+                    if (op_is_fwd(o)) th = (sm.wsq[s] * iws) * sm.thc[s];  // (ws_q / ws_i)(eps_f / lam)
+                    else th = (o == OP_SEQ) ? 0.0 : sm.eps_b[s];
+                    const bool act = r > th;
+                    if (act) {
+                        pv[v] = (T)r;
+                        rv[v] = (T)0;
+                        a.EST[i + v] = (init ? 0.0 : a.EST[i + v]) + a.alpha * r;
+                        cnt[v] += 1;
+                        npu[v] += deg;
+                        wrote_r = true;
+                    } else if (init) {
+                        rv[v] = (T)r;
+                        a.EST[i + v] = 0.0;
+                        wrote_r = true;
+                    }
+                } else {
+                    pv[v] = a.P[i + v];  // keep (power-iteration iterate / idle)
                 }
-                continue;
             }
-            double th;
-            if (fwd) th = (wsq * a.inv_ws_u[u]) * thc;   // (ws_q / ws_i) * (eps_f / lam)
-            else th = (op == OP_SEQ) ? 0.0 : eps_b;
-            if (fentry) gam += (a.ws_u[u] * iwsq) * r;     // gamma, push_engine.py:222
-            const bool act = r > th;
-            a.P[i] = act ? (T)r : (T)0;
-            if (act) {
-                a.R[i] = (T)0;
-                a.EST[i] = (init ? 0.0 : a.EST[i]) + a.alpha * r;
-                cnt += 1;
-                npu += a.deg_u[u];
-            } else if (init) {
-                a.R[i] = (T)r;
-                a.EST[i] = 0.0;
-            }
+            VecIO<T, EV>::st(a.P + i, pv);
+            if (wrote_r) VecIO<T, EV>::st(a.R + i, rv);
         }
     }
-    red_cnt[threadIdx.x] = cnt;
-    red_np[threadIdx.x] = npu;
-    red_g[threadIdx.x] = gam;
+#pragma unroll
+    for (int v = 0; v < EV; v++) {
+        red_cnt[threadIdx.x * EV + v] = cnt[v];
+        red_np[threadIdx.x * EV + v] = npu[v];
+    }
     __syncthreads();
-    for (int t = threadIdx.x; t < B; t += blockDim.x) {
+    // slot s is owned by the threads t with t % TPN == s / EV
+    for (int s = threadIdx.x; s < B; s += blockDim.x) {
         int64_t c = 0, n = 0;
-        double gg = 0.0;
-        for (int j = t; j < PREP_THREADS; j += B) {
-            c += red_cnt[j];
-            n += red_np[j];
-            gg += red_g[j];
+        for (int t = s / EV; t < ELEM_THREADS; t += TPN) {
+            c += red_cnt[t * EV + s % EV];
+            n += red_np[t * EV + s % EV];
         }
-        a.part.cnt[blockIdx.x * B + t] = c;
-        a.part.np_u[blockIdx.x * B + t] = n;
-        a.part.gamma[blockIdx.x * B + t] = gg;
+        a.part.cnt[(int64_t)s * gridDim.x + blockIdx.x] = c;
+        a.part.np_u[(int64_t)s * gridDim.x + blockIdx.x] = n;
+    }
+}
+
+// K1a: combine r_u += Y (push slots) / a = y0 + Y (power-iteration slots), and
+// the exit-test reductions of the round that just ran.
+template <int B, typename T>
+__global__ void __launch_bounds__(ELEM_THREADS) k_combine(ElemArgs<T> a) {
+    if (*a.active == 0) return;
+    using EG = ElemGeo<B>;
+    constexpr int EV = EG::EV, TPN = EG::TPN;
+    __shared__ SlotSmem sm;
+    __shared__ double red_sum[ELEM_THREADS * EV];
+    __shared__ double red_wsum[ELEM_THREADS * EV];
+    __shared__ int32_t red_any[ELEM_THREADS * EV];
+    load_slot_smem<B>(sm, a.slots);
+    __syncthreads();
+    const int j0 = (threadIdx.x % TPN) * EV;
+    int op[EV];
+    bool any_work = false;
+#pragma unroll
+    for (int v = 0; v < EV; v++) {
+        op[v] = sm.op[j0 + v];
+        any_work |= op_is_push(op[v]) || op[v] == OP_PIENTRY || op[v] == OP_PI || op[v] == OP_MEASURE;
+    }
+    double sum[EV], wsum[EV];
+    int32_t any[EV];
+#pragma unroll
+    for (int v = 0; v < EV; v++) {
+        sum[v] = wsum[v] = 0.0;
+        any[v] = 0;
+    }
+    if (any_work) {
+        const int64_t total = a.n_u * TPN;
+        for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+             t += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t u = t / TPN;
+            const int64_t i = u * B + j0;
+            T rv[EV], yv[EV];
+            VecIO<T, EV>::ld(a.R + i, rv);
+            VecIO<T, EV>::ld(a.Y + i, yv);
+            const double ws = a.ws_u[u], iws = a.inv_ws_u[u];
+            bool wrote_r = false;
+#pragma unroll
+            for (int v = 0; v < EV; v++) {
+                const int s = j0 + v;
+                const int o = op[v];
+                if (op_is_push(o) || o == OP_MEASURE) {
+                    T nr = rv[v];
+                    if (o != OP_MEASURE) {
+                        nr = (T)((double)rv[v] + (double)yv[v]);
+                        rv[v] = nr;
+                        wrote_r = true;
+                    }
+                    const double r = (double)nr;
+                    sum[v] += r;
+                    wsum[v] += (ws * sm.iwsq[s]) * r;  // w_ratio * r  (push_engine.py:220,237)
+                    const double th =
+                        (op_is_fwd(o) || o == OP_MEASURE) ? (sm.wsq[s] * iws) * sm.thc[s] : sm.eps_b[s];
+                    any[v] |= r > th;
+                } else if (o == OP_PIENTRY || o == OP_PI) {
+                    a.P[i + v] = (T)((double)rv[v] * sm.ysc[s] + (double)yv[v]);
+                }
+            }
+            if (wrote_r) VecIO<T, EV>::st(a.R + i, rv);
+        }
+    }
+#pragma unroll
+    for (int v = 0; v < EV; v++) {
+        red_sum[threadIdx.x * EV + v] = sum[v];
+        red_wsum[threadIdx.x * EV + v] = wsum[v];
+        red_any[threadIdx.x * EV + v] = any[v];
+    }
+    __syncthreads();
+    for (int s = threadIdx.x; s < B; s += blockDim.x) {
+        double su = 0.0, ws = 0.0;
+        int32_t an = 0;
+        for (int t = s / EV; t < ELEM_THREADS; t += TPN) {
+            su += red_sum[t * EV + s % EV];
+            ws += red_wsum[t * EV + s % EV];
+            an |= red_any[t * EV + s % EV];
+        }
+        a.part.sum[(int64_t)s * gridDim.x + blockIdx.x] = su;
+        a.part.wsum[(int64_t)s * gridDim.x + blockIdx.x] = ws;
+        a.part.any[(int64_t)s * gridDim.x + blockIdx.x] = an;
     }
 }
 
 // ---------------------------------------------------------------------------
-// K2 / K3: pull SpMM with fused round epilogue.
+// K2 / K3: pipelined pull SpMM.
 enum : int { SIDE_V = 0, SIDE_U = 1 };
+
+constexpr int PULL_THREADS = 256;
+constexpr int PULL_WARPS = PULL_THREADS / 32;
+
+template <int B, typename T>
+struct Pipe {
+    static constexpr int ROW = B * (int)sizeof(T);                 // operand row bytes
+    static constexpr int CHUNKS = ROW / 16;                        // 16-byte pieces per row
+    static constexpr int LPE = CHUNKS < 32 ? CHUNKS : 32;          // lanes copying one edge
+    static constexpr int CPE = CHUNKS / LPE;                       // copy instructions per edge
+    static constexpr int EPI = 32 / LPE;                           // edges per issue step
+    static constexpr int S = (4096 / ROW) < EPI ? EPI : (4096 / ROW);  // ring depth (edges)
+    static constexpr int VEC = B / 32;                             // slots per lane
+    static constexpr int WARP_SMEM = S * ROW + S * (int)sizeof(T);
+};
 
 template <typename T>
 struct PullArgs {
     const int64_t *indptr;
+    int64_t n_rows;
     const int32_t *indices;
     const T *vals;
-    const Unit *units;
-    int32_t n_units;
-    const SplitRow *splits;
-    int32_t n_splits;
-    double *scratch;  // [n_pieces][B]
-    const T *X;       // operand: P (V pull) or XV (U pull)
-    T *Y;             // V pull: XV ; U pull: R (in/out)
-    T *P;             // U pull: P for power-iteration slots
-    const double *ws_u;
-    const double *inv_ws_u;
+    const WarpWork *work;  // [n_warps]
+    const CutRow *cuts;
+    int32_t *cut_count;    // [n_cuts], zero between launches
+    double *scratch;       // [n_parts][B]
+    int32_t n_warps;
+    const T *X;            // operand: P (V pull) or XV (U pull)
+    T *Y;                  // V pull: XV ; U pull: Y
     const Slot *slots;
     const int32_t *active;
-    Partials part;
-    int32_t part_row0;
+    int64_t *np_v;         // [n_warps][B] (V pull)
     double one_minus_alpha;
 };
 
-template <int B, typename T, int SIDE>
-struct Epi {
-    static constexpr int VEC = Geo<B>::VEC;
-    // per-lane reductions
-    int64_t np[SIDE == SIDE_V ? VEC : 1];
-    int32_t any[SIDE == SIDE_U ? VEC : 1];
-    double red[SIDE == SIDE_U ? VEC : 1];
-
-    __device__ __forceinline__ void init() {
+template <int B, typename T, int SIDE, int VEC>
+__device__ __forceinline__ void pull_row_final(const PullArgs<T> &a, const int32_t *s_op, int64_t row, int32_t deg,
+                                               int slot0, const double (&acc)[VEC], int64_t (&np)[VEC]) {
+    T out[VEC];
+    if constexpr (SIDE == SIDE_V) {
 #pragma unroll
-        for (int j = 0; j < (SIDE == SIDE_V ? VEC : 1); j++) np[j] = 0;
-#pragma unroll
-        for (int j = 0; j < (SIDE == SIDE_U ? VEC : 1); j++) {
-            any[j] = 0;
-            red[j] = 0.0;
+        for (int v = 0; v < VEC; v++) {
+            out[v] = (T)(a.one_minus_alpha * acc[v]);
+            if (op_is_push(s_op[slot0 + v]) && (double)out[v] > 0.0) np[v] += deg;
         }
+    } else {
+#pragma unroll
+        for (int v = 0; v < VEC; v++) out[v] = (T)acc[v];
     }
+    VecIO<T, VEC>::st(a.Y + row * B + slot0, out);
+}
 
-    // Final value of one row for the lane's VEC slots starting at slot0.
-    __device__ __forceinline__ void row(const PullArgs<T> &a, const SlotSmem &sm, int64_t row, int32_t deg,
-                                        int slot0, const double (&acc)[VEC]) {
-        if constexpr (SIDE == SIDE_V) {
-            T out[VEC];
-#pragma unroll
-            for (int j = 0; j < VEC; j++) {
-                out[j] = (T)(a.one_minus_alpha * acc[j]);
-                if (op_is_push(sm.op[slot0 + j]) && (double)out[j] > 0.0) np[j] += deg;
-            }
-            VecIO<T, VEC>::st(a.Y + row * B + slot0, out);
-        } else {
-            T r[VEC];
-            VecIO<T, VEC>::ldc(a.Y + row * B + slot0, r);
-            const double wsr = a.ws_u[row];
-            const double iwsr = a.inv_ws_u[row];
-#pragma unroll
-            for (int j = 0; j < VEC; j++) {
-                const int s = slot0 + j;
-                const int op = sm.op[s];
-                if (op_is_push(op)) {
-                    const T nr = (T)((double)r[j] + acc[j]);
-                    r[j] = nr;
-                    const double v = (double)nr;
-                    if (op_is_fwd(op)) {
-                        const double th = (sm.wsq[s] * iwsr) * sm.thc[s];
-                        any[j] |= v > th;
-                        red[j] += (wsr * sm.iwsq[s]) * v;
-                    } else {
-                        any[j] |= v > sm.eps_b[s];
-                        red[j] += v;
-                    }
-                } else if (op == OP_PIENTRY || op == OP_PI) {
-                    const double y0 = (double)r[j] * sm.ysc[s];
-                    a.P[row * B + s] = (T)(y0 + acc[j]);
-                }
-            }
-            VecIO<T, VEC>::st(a.Y + row * B + slot0, r);
-        }
-    }
-
-    // Write this lane's reductions to the block partial row.
-    __device__ __forceinline__ void flush(const PullArgs<T> &a, bool owner, int slot0, int warp,
-                                          double *sh_d, int64_t *sh_i, int32_t *sh_a) {
-        if (owner) {
-#pragma unroll
-            for (int j = 0; j < VEC; j++) {
-                if constexpr (SIDE == SIDE_V) {
-                    sh_i[warp * B + slot0 + j] = np[j];
-                } else {
-                    sh_a[warp * B + slot0 + j] = any[j];
-                    sh_d[warp * B + slot0 + j] = red[j];
-                }
-            }
-        }
-    }
+template <int VEC>
+struct DVec {
+    double v[VEC];
+};
+template <int VEC>
+struct IVec {
+    int64_t v[VEC];
 };
 
-template <int B, typename T, int SIDE>
-__device__ __forceinline__ void block_partials(const PullArgs<T> &a, int nwarps, double *sh_d, int64_t *sh_i,
-                                               int32_t *sh_a, int row_index) {
-    __syncthreads();
-    for (int s = threadIdx.x; s < B; s += blockDim.x) {
-        if constexpr (SIDE == SIDE_V) {
-            int64_t n = 0;
-            for (int w = 0; w < nwarps; w++) n += sh_i[w * B + s];
-            a.part.np_v[(int64_t)row_index * B + s] = n;
-        } else {
-            int32_t an = 0;
-            double r = 0.0;
-            for (int w = 0; w < nwarps; w++) {
-                an |= sh_a[w * B + s];
-                r += sh_d[w * B + s];
-            }
-            a.part.any[(int64_t)row_index * B + s] = an;
-            a.part.sum[(int64_t)row_index * B + s] = r;
-        }
-    }
+// A row cut by this warp's range boundary: publish the fp64 partial; the last
+// warp to arrive adds all partials in warp order and finishes the row.  Kept
+// out of line (rare path) so the streaming loop keeps its registers; returns
+// the n_p increments of the finished row (V pull).
+template <int B, typename T, int SIDE, int VEC>
+__device__ __noinline__ IVec<VEC> pull_cut_row(const PullArgs<T> &a, const int32_t *s_op, int ci, int pi, int slot0,
+                                               DVec<VEC> acc) {
+    const int lane = threadIdx.x & 31;
+    IVec<VEC> inc;
+#pragma unroll
+    for (int v = 0; v < VEC; v++) inc.v[v] = 0;
+#pragma unroll
+    for (int v = 0; v < VEC; v++) a.scratch[(int64_t)pi * B + slot0 + v] = acc.v[v];
+    __threadfence();
+    __syncwarp();
+    const CutRow cr = a.cuts[ci];
+    int last = 0;
+    if (lane == 0) last = atomicAdd(a.cut_count + ci, 1) == cr.n_parts - 1;
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (!last) return inc;
+    __threadfence();
+    double tot[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; v++) tot[v] = 0.0;
+    for (int p = 0; p < cr.n_parts; p++)
+#pragma unroll
+        for (int v = 0; v < VEC; v++) tot[v] += __ldcg(a.scratch + (int64_t)(cr.first_part + p) * B + slot0 + v);
+    const int32_t deg = (int32_t)(__ldg(a.indptr + cr.row + 1) - __ldg(a.indptr + cr.row));
+    pull_row_final<B, T, SIDE, VEC>(a, s_op, cr.row, deg, slot0, tot, inc.v);
+    if (lane == 0) a.cut_count[ci] = 0;
+    return inc;
 }
 
-template <int B, typename T, int SIDE>
-__global__ void __launch_bounds__(PULL_THREADS) k_pull(PullArgs<T> a) {
-    if (*a.active == 0) return;
-    using GE = Geo<B>;
-    constexpr int G = GE::G, EPW = GE::EPW, VEC = GE::VEC;
-    __shared__ SlotSmem sm;
-    __shared__ double sh_d[PULL_WARPS * B];
-    __shared__ int64_t sh_i[PULL_WARPS * B];
-    __shared__ int32_t sh_a[PULL_WARPS * B];
-    load_slot_smem<B>(sm, a.slots);
-    __syncthreads();
+// fp64 mode accumulates each product with DFMA.  fp32 mode multiplies and adds
+// in fp32 over at most FLUSH consecutive edges of a row, then adds that short
+// partial into the fp64 row sum (SURVEY.md sec. 7 hard part 2: fp32 storage
+// with fp64 row accumulation; the chunked form avoids a conversion per edge).
+template <typename T>
+struct Acc;
+template <>
+struct Acc<double> {
+    static constexpr int FLUSH = 1 << 30;
+};
+template <>
+struct Acc<float> {
+    static constexpr int FLUSH = 16;
+};
 
+// B >= 32: lanes own slots; the warp streams its edge range through the ring.
+template <int B, typename T, int SIDE>
+__global__ void __launch_bounds__(PULL_THREADS, 2) k_pull(PullArgs<T> a) {
+    if (*a.active == 0) return;
+    using PC = Pipe<B, T>;
+    constexpr int VEC = PC::VEC, ROW = PC::ROW, LPE = PC::LPE, CPE = PC::CPE, EPI = PC::EPI, S = PC::S;
+    extern __shared__ __align__(16) unsigned char dsm[];
+    __shared__ int32_t s_op[MAX_B];
+    for (int s = threadIdx.x; s < B; s += blockDim.x) s_op[s] = a.slots[s].op;
+    __syncthreads();
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int grp = lane / G;
-    const int slot0 = (lane % G) * VEC;
-    const int64_t gwarp = (int64_t)blockIdx.x * PULL_WARPS + warp;
-    const int64_t nwarps_total = (int64_t)gridDim.x * PULL_WARPS;
-    Epi<B, T, SIDE> epi;
-    epi.init();
+    const int gw = blockIdx.x * PULL_WARPS + warp;
+    const int slot0 = lane * VEC;
+    int64_t np[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; v++) np[v] = 0;
+    unsigned char *ring = dsm + (size_t)warp * PC::WARP_SMEM;
+    const T *rval = reinterpret_cast<const T *>(ring + S * ROW);
+    const T *xlane = reinterpret_cast<const T *>(ring) + slot0;
+    const uint32_t ring_u32 = smem_u32(ring);
+    const uint32_t rval_u32 = smem_u32(rval);
 
-    for (int64_t ui = gwarp; ui < a.n_units; ui += nwarps_total) {
-        const Unit un = a.units[ui];
-        const bool piece = un.piece >= 0;
-        if constexpr (EPW == 1) {
-            // ---- B >= 32: lanes own slots, the warp walks the unit's edge stream
-            const int64_t my_rend = (!piece && lane < un.nrows) ? a.indptr[un.row0 + lane + 1] : 0;
-            int rr = 0;
-            int64_t rstart = un.e0;
-            int64_t rend = piece ? un.e1 : __shfl_sync(0xffffffffu, my_rend, 0);
+    if (gw < a.n_warps) {
+        const WarpWork wk = a.work[gw];
+        const int64_t e0 = wk.e0;
+        const int n = (int)(wk.e1 - e0);
+        if (n > 0) {
+            const int32_t *cols = a.indices + e0;
+            const T *vals = a.vals + e0;
+            // ---- issue side: column indices in 32-edge windows (double buffered)
+            int ib = 0;
+            int icol = lane < n ? __ldg(cols + lane) : 0;
+            int icol_nx = 32 + lane < n ? __ldg(cols + 32 + lane) : 0;
+            const int grp = lane / LPE, q = lane % LPE;
+            const uint32_t qoff = (uint32_t)q * 16;
+            auto issue = [&](int io) {  // edges [io, io + EPI)
+                if (io >= ib + 32) {
+                    ib += 32;
+                    icol = icol_nx;
+                    icol_nx = ib + 32 + lane < n ? __ldg(cols + ib + 32 + lane) : 0;
+                }
+                const int o = io + grp;
+                const int c = __shfl_sync(0xffffffffu, icol, (o - ib) & 31);
+                if (o < n) {
+                    const uint32_t st = (uint32_t)(o & (S - 1));
+                    const unsigned char *src = reinterpret_cast<const unsigned char *>(a.X + (int64_t)c * B) + qoff;
+                    const uint32_t dst = ring_u32 + st * ROW + qoff;
+#pragma unroll
+                    for (int k = 0; k < CPE; k++) cp_async<16>(dst + k * LPE * 16, src + k * LPE * 16);
+                    if (q == 0) cp_async<(int)sizeof(T)>(rval_u32 + st * (uint32_t)sizeof(T), vals + o);
+                }
+                cp_async_commit();
+            };
+#pragma unroll
+            for (int p = 0; p < S / EPI; p++) issue(p * EPI);
+
+            // ---- consume side: rows in order, row ends in 32-row windows
+            int64_t row = wk.r0;
+            int64_t rwin = row;
+            auto rend_of = [&](int64_t r) { return __ldg(a.indptr + (r <= a.n_rows ? r : a.n_rows)); };
+            int64_t my_rend = rend_of(rwin + lane + 1);
+            const int64_t rs0 = __ldg(a.indptr + row);
+            int64_t rend_abs = __shfl_sync(0xffffffffu, my_rend, 0);
+            int64_t rstart_abs = rs0;
+            int oend = (int)imin64(rend_abs - e0, n);  // end offset of the current row (clipped)
             double acc[VEC];
+            T acc_s[VEC];
+            int since = 0;
 #pragma unroll
-            for (int j = 0; j < VEC; j++) acc[j] = 0.0;
-            for (int64_t cb = un.e0; cb < un.e1; cb += 32) {
-                const int n = (int)imin64(32, un.e1 - cb);
-                const int my_col = lane < n ? __ldg(a.indices + cb + lane) : 0;
-                const T my_val = lane < n ? __ldg(a.vals + cb + lane) : (T)0;
-                constexpr int UNR = 8;
-                for (int j0 = 0; j0 < n; j0 += UNR) {
-                    T xs[UNR][VEC];
-                    T wv[UNR];
+            for (int v = 0; v < VEC; v++) {
+                acc[v] = 0.0;
+                acc_s[v] = (T)0;
+            }
+            for (int co = 0; co < n; co += EPI) {
+                cp_async_wait<S / EPI - 1>();
+                __syncwarp();
 #pragma unroll
-                    for (int t = 0; t < UNR; t++) {
-                        const int j = j0 + t;
-                        const int c = __shfl_sync(0xffffffffu, my_col, j & 31);
-                        wv[t] = __shfl_sync(0xffffffffu, my_val, j & 31);
-                        if (j < n) {
-                            VecIO<T, VEC>::ld(a.X + (int64_t)c * B + slot0, xs[t]);
+                for (int t = 0; t < EPI; t++) {
+                    const int o = co + t;
+                    if (o < n) {
+                        const int st = o & (S - 1);
+                        T xv[VEC];
+                        VecIO<T, VEC>::ld(xlane + st * (ROW / (int)sizeof(T)), xv);
+                        const T w = rval[st];
+                        if constexpr (Acc<T>::FLUSH >= (1 << 30)) {
+#pragma unroll
+                            for (int v = 0; v < VEC; v++) acc[v] = fma((double)w, (double)xv[v], acc[v]);
                         } else {
 #pragma unroll
-                            for (int v = 0; v < VEC; v++) xs[t][v] = (T)0;
-                        }
-                    }
+                            for (int v = 0; v < VEC; v++) acc_s[v] = fmaf(w, xv[v], acc_s[v]);
+                            if (++since == Acc<T>::FLUSH) {
 #pragma unroll
-                    for (int t = 0; t < UNR; t++) {
-                        const int j = j0 + t;
-                        if (j < n) {
-#pragma unroll
-                            for (int v = 0; v < VEC; v++) acc[v] = fma((double)wv[t], (double)xs[t][v], acc[v]);
-                            if (cb + j + 1 == rend) {
-                                if (piece) {
-#pragma unroll
-                                    for (int v = 0; v < VEC; v++) a.scratch[(int64_t)un.piece * B + slot0 + v] = acc[v];
-                                } else {
-                                    epi.row(a, sm, un.row0 + rr, (int32_t)(rend - rstart), slot0, acc);
-                                    rr++;
-                                    rstart = rend;
-                                    rend = __shfl_sync(0xffffffffu, my_rend, rr & 31);
+                                for (int v = 0; v < VEC; v++) {
+                                    acc[v] += (double)acc_s[v];
+                                    acc_s[v] = (T)0;
                                 }
-#pragma unroll
-                                for (int v = 0; v < VEC; v++) acc[v] = 0.0;
+                                since = 0;
                             }
                         }
-                    }
-                }
-            }
-        } else {
-            // ---- B < 32: EPW edge groups of G lanes split each row
-            const int nrows = piece ? 1 : un.nrows;
-            for (int rr = 0; rr < nrows; rr++) {
-                const int64_t row = un.row0 + rr;
-                const int64_t e_s = piece ? un.e0 : a.indptr[row];
-                const int64_t e_e = piece ? un.e1 : a.indptr[row + 1];
-                double acc[VEC];
+                        if (o + 1 == oend) {
+                            if constexpr (Acc<T>::FLUSH < (1 << 30)) {
 #pragma unroll
-                for (int j = 0; j < VEC; j++) acc[j] = 0.0;
-                constexpr int UNR = 4;
-                for (int64_t e = e_s + grp; e < e_e; e += EPW * UNR) {
-                    T xs[UNR][VEC];
-                    T wv[UNR];
+                                for (int v = 0; v < VEC; v++) {
+                                    acc[v] += (double)acc_s[v];
+                                    acc_s[v] = (T)0;
+                                }
+                                since = 0;
+                            }
+                            const bool cut = rstart_abs < e0 || rend_abs > wk.e1;
+                            if (!cut) {
+                                pull_row_final<B, T, SIDE, VEC>(a, s_op, row, (int32_t)(rend_abs - rstart_abs), slot0,
+                                                                acc, np);
+                            } else {
+                                const bool first = row == wk.r0;
+                                DVec<VEC> av;
 #pragma unroll
-                    for (int t = 0; t < UNR; t++) {
-                        const int64_t ee = e + (int64_t)t * EPW;
-                        if (ee < e_e) {
-                            const int c = __ldg(a.indices + ee);
-                            wv[t] = __ldg(a.vals + ee);
-                            VecIO<T, VEC>::ld(a.X + (int64_t)c * B + slot0, xs[t]);
-                        } else {
-                            wv[t] = (T)0;
+                                for (int v = 0; v < VEC; v++) av.v[v] = acc[v];
+                                const IVec<VEC> inc = pull_cut_row<B, T, SIDE, VEC>(
+                                    a, s_op, first ? wk.cut0 : wk.cut1, first ? wk.part0 : wk.part1, slot0, av);
 #pragma unroll
-                            for (int v = 0; v < VEC; v++) xs[t][v] = (T)0;
+                                for (int v = 0; v < VEC; v++) np[v] += inc.v[v];
+                            }
+#pragma unroll
+                            for (int v = 0; v < VEC; v++) acc[v] = 0.0;
+                            row++;
+                            rstart_abs = rend_abs;
+                            if (row - rwin >= 32) {
+                                rwin = row;
+                                my_rend = rend_of(rwin + lane + 1);
+                            }
+                            rend_abs = __shfl_sync(0xffffffffu, my_rend, (int)(row - rwin) & 31);
+                            oend = (int)imin64(rend_abs - e0, n);
                         }
                     }
-#pragma unroll
-                    for (int t = 0; t < UNR; t++)
-#pragma unroll
-                        for (int v = 0; v < VEC; v++) acc[v] = fma((double)wv[t], (double)xs[t][v], acc[v]);
                 }
-                // combine the EPW groups in a fixed butterfly order
-#pragma unroll
-                for (int off = G; off < 32; off <<= 1)
-#pragma unroll
-                    for (int v = 0; v < VEC; v++) acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], off);
-                if (grp == 0) {
-                    if (piece) {
-#pragma unroll
-                        for (int v = 0; v < VEC; v++) a.scratch[(int64_t)un.piece * B + slot0 + v] = acc[v];
-                    } else {
-                        epi.row(a, sm, row, (int32_t)(e_e - e_s), slot0, acc);
-                    }
-                }
+                __syncwarp();
+                issue(co + S);
             }
+            cp_async_wait<0>();
         }
     }
-    epi.flush(a, grp == 0, slot0, warp, sh_d, sh_i, sh_a);
-    block_partials<B, T, SIDE>(a, PULL_WARPS, sh_d, sh_i, sh_a, a.part_row0 + blockIdx.x);
+    if constexpr (SIDE == SIDE_V) {
+        if (gw < a.n_warps)
+#pragma unroll
+            for (int v = 0; v < VEC; v++) a.np_v[(int64_t)(slot0 + v) * a.n_warps + gw] = np[v];
+    }
 }
 
-// Finisher: one warp per split row, adds its pieces in order, runs the epilogue.
+// B < 32 (single-query and small blocks): G lanes per edge group, 32/G groups
+// split each row; plain loads.  Same partition, cut rows and epilogue.
 template <int B, typename T, int SIDE>
-__global__ void __launch_bounds__(PULL_THREADS) k_pull_finish(PullArgs<T> a) {
+__global__ void __launch_bounds__(PULL_THREADS) k_pull_small(PullArgs<T> a) {
     if (*a.active == 0) return;
-    using GE = Geo<B>;
-    constexpr int G = GE::G, VEC = GE::VEC;
-    __shared__ SlotSmem sm;
-    __shared__ double sh_d[PULL_WARPS * B];
-    __shared__ int64_t sh_i[PULL_WARPS * B];
-    __shared__ int32_t sh_a[PULL_WARPS * B];
-    load_slot_smem<B>(sm, a.slots);
+    constexpr int G = B, EPW = 32 / B;
+    __shared__ int32_t s_op[MAX_B];
+    for (int s = threadIdx.x; s < B; s += blockDim.x) s_op[s] = a.slots[s].op;
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int grp = lane / G;
-    const int slot0 = (lane % G) * VEC;
-    Epi<B, T, SIDE> epi;
-    epi.init();
-    for (int64_t si = (int64_t)blockIdx.x * PULL_WARPS + warp; si < a.n_splits;
-         si += (int64_t)gridDim.x * PULL_WARPS) {
-        const SplitRow sr = a.splits[si];
-        if (grp != 0) continue;
-        double acc[VEC];
+    const int gw = blockIdx.x * PULL_WARPS + warp;
+    const int grp = lane / G, slot = lane % G;
+    int64_t np = 0;
+    if (gw < a.n_warps) {
+        const WarpWork wk = a.work[gw];
+        const int64_t e0 = wk.e0, e1 = wk.e1;
+        int64_t row = wk.r0;
+        for (int64_t guard = 0; e0 < e1 && guard <= a.n_rows; guard++) {
+            const int64_t rs = __ldg(a.indptr + row), re = __ldg(a.indptr + row + 1);
+            const int64_t s0 = rs > e0 ? rs : e0, s1 = re < e1 ? re : e1;
+            double acc = 0.0;
+            for (int64_t e = s0 + grp; e < s1; e += EPW)
+                acc = fma((double)__ldg(a.vals + e), (double)__ldg(a.X + (int64_t)__ldg(a.indices + e) * B + slot), acc);
 #pragma unroll
-        for (int v = 0; v < VEC; v++) acc[v] = 0.0;
-        for (int p = 0; p < sr.n_pieces; p++) {
-#pragma unroll
-            for (int v = 0; v < VEC; v++) acc[v] += a.scratch[(int64_t)(sr.first_piece + p) * B + slot0 + v];
+            for (int off = G; off < 32; off <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+            const bool cut = rs < e0 || re > e1;
+            double fin = acc;
+            bool do_final = !cut;
+            if (cut) {
+                const int ci = (row == wk.r0) ? wk.cut0 : wk.cut1;
+                const int pi = (row == wk.r0) ? wk.part0 : wk.part1;
+                if (grp == 0) a.scratch[(int64_t)pi * B + slot] = acc;
+                __threadfence();
+                __syncwarp();
+                const CutRow cr = a.cuts[ci];
+                int last = 0;
+                if (lane == 0) last = atomicAdd(a.cut_count + ci, 1) == cr.n_parts - 1;
+                last = __shfl_sync(0xffffffffu, last, 0);
+                if (last) {
+                    __threadfence();
+                    fin = 0.0;
+                    for (int p = 0; p < cr.n_parts; p++) fin += __ldcg(a.scratch + (int64_t)(cr.first_part + p) * B + slot);
+                    do_final = true;
+                    if (lane == 0) a.cut_count[ci] = 0;
+                }
+            }
+            if (do_final && grp == 0) {
+                T out;
+                if constexpr (SIDE == SIDE_V) {
+                    out = (T)(a.one_minus_alpha * fin);
+                    if (op_is_push(s_op[slot]) && (double)out > 0.0) np += (int32_t)(re - rs);
+                } else {
+                    out = (T)fin;
+                }
+                a.Y[row * B + slot] = out;
+            }
+            if (re >= e1) break;
+            row++;
         }
-        const int32_t deg = (int32_t)(a.indptr[sr.row + 1] - a.indptr[sr.row]);
-        epi.row(a, sm, sr.row, deg, slot0, acc);
     }
-    epi.flush(a, grp == 0, slot0, warp, sh_d, sh_i, sh_a);
-    block_partials<B, T, SIDE>(a, PULL_WARPS, sh_d, sh_i, sh_a, a.part_row0 + blockIdx.x);
+    if constexpr (SIDE == SIDE_V) {
+        if (gw < a.n_warps && grp == 0) a.np_v[(int64_t)slot * a.n_warps + gw] = np;
+    }
 }
 
 }  // namespace bh
