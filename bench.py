@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-fp64", action="store_true", help="skip the fp64 side measurement")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-kernel-events", action="store_true", help="skip per-kernel CUDA events in the timed steps")
     return ap.parse_args()
 
 
@@ -285,7 +286,7 @@ def run_ours(args):
         return ms, launches, prof, clk, traces_all, dg
 
     # headline: fp32 storage / fp64 accumulation
-    ms, launches, prof, clk, traces_all, dg = measure(args.dtype, args.steps, args.warmup, True)
+    ms, launches, prof, clk, traces_all, dg = measure(args.dtype, args.steps, args.warmup, not args.no_kernel_events)
     value = world * n * args.steps / (ms / 1e3)
     s_bytes = 4 if args.dtype == "fp32" else 8
     alg = sum(algorithmic_bytes(g, t, prof["rounds"] // args.steps, s_bytes) for t in traces_all)

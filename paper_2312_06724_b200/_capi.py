@@ -156,6 +156,15 @@ class DeviceGraph:
             np.ascontiguousarray(g.ws_u, dtype=np.float64),
             np.ascontiguousarray(g.ws_v, dtype=np.float64),
         ]
+        import os
+        if os.environ.get("BH_PERMUTE_ROWS"):  # experiment: scatter column order within rows
+            arrs = [a.copy() for a in arrs]
+            for ip, ix, w in ((arrs[0], arrs[1], arrs[2]), (arrs[3], arrs[4], arrs[5])):
+                rowid = np.repeat(np.arange(ip.size - 1), np.diff(ip))
+                key = (ix.astype(np.int64) * 2654435761) % 1000003
+                order = np.lexsort((key, rowid))
+                ix[:] = ix[order]
+                w[:] = w[order]
         h = C.c_void_p()
         check(lib().bh_graph_create(self.n_u, self.n_v, self.n_e, *[ptr(a) for a in arrs], self.device,
                                     DTYPES[dtype], C.byref(h)))

@@ -8,6 +8,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <cmath>
 #include <cstring>
@@ -180,6 +181,7 @@ struct Engine final : EngineBase {
     double *hook_r = nullptr, *hook_est = nullptr;
     std::vector<cudaEvent_t> evpool;
     SidePlan plan_v, plan_u;
+    uint64_t *dbg_v = nullptr, *dbg_u = nullptr;  // BH_DEBUG_WARP_TIMING
     size_t pull_smem = 0;
     int fin_chunk = 4096, n_chunks = 1;
     int grid_elem = 1, grid_k5 = 1;
@@ -210,7 +212,7 @@ struct Engine final : EngineBase {
         BH_CUDA(cudaMemset(ctl, 0, sizeof(Control)));
         int sms = 148;
         BH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
-        if constexpr (WIDE) pull_smem = (size_t)PULL_WARPS * Pipe<B, T>::WARP_SMEM;
+        pull_smem = 0;
         for (int side = 0; side < 2; side++) {
             void *fn;
             pull_kernel(side, &fn);
@@ -247,6 +249,30 @@ struct Engine final : EngineBase {
         scratch = dalloc<double>((size_t)parts * B);
         hook_r = dalloc<double>(nu);
         hook_est = dalloc<double>(nu);
+        if (getenv("BH_DEBUG_WARP_TIMING")) {
+            dbg_v = dalloc<uint64_t>((size_t)plan_v.n_warps * 4);
+            dbg_u = dalloc<uint64_t>((size_t)plan_u.n_warps * 4);
+        }
+    }
+
+    static void dump_warp_timing(const char *tag, const uint64_t *d, int n) {
+        std::vector<uint64_t> h((size_t)n * 4);
+        BH_CUDA(cudaMemcpy(h.data(), d, h.size() * 8, cudaMemcpyDeviceToHost));
+        uint64_t t0 = UINT64_MAX, t1 = 0;
+        for (int w = 0; w < n; w++) { t0 = std::min(t0, h[w * 4]); t1 = std::max(t1, h[w * 4 + 1]); }
+        std::vector<double> dur(n);
+        double sum = 0;
+        int worst = 0;
+        for (int w = 0; w < n; w++) {
+            dur[w] = (double)(h[w * 4 + 1] - h[w * 4]) / 1e3;
+            sum += dur[w];
+            if (dur[w] > dur[worst]) worst = w;
+        }
+        std::vector<double> s = dur;
+        std::sort(s.begin(), s.end());
+        fprintf(stderr, "[warp-timing %s] kernel span %.1f us, warp dur: min %.1f p50 %.1f p90 %.1f p99 %.1f max %.1f (warp %d, %llu edges, start +%.1f us)\n",
+                tag, (t1 - t0) / 1e3, s[0], s[n / 2], s[(int)(n * 0.9)], s[(int)(n * 0.99)], s[n - 1], worst,
+                (unsigned long long)h[worst * 4 + 2], (h[worst * 4] - t0) / 1e3);
     }
 
     ~Engine() override {
@@ -298,6 +324,7 @@ struct Engine final : EngineBase {
         a.active = &ctl->active;
         a.np_v = part.np_v;
         a.one_minus_alpha = one_minus_alpha;
+        a.dbg = side == SIDE_V ? dbg_v : dbg_u;
         return a;
     }
 
@@ -454,6 +481,10 @@ struct Engine final : EngineBase {
             }
             BH_CUDA(cudaMemcpyAsync(h_ctl, ctl, sizeof(Control), cudaMemcpyDeviceToHost, st));
             BH_CUDA(cudaStreamSynchronize(st));
+            if (dbg_v) {
+                dump_warp_timing("V", dbg_v, plan_v.n_warps);
+                dump_warp_timing("U", dbg_u, plan_u.n_warps);
+            }
             if (!h_ctl->active && h_ctl->n_fin == 0) {
                 stats.rounds = h_ctl->rounds_active;
                 if (prof) collect_profile(round);

@@ -377,7 +377,14 @@ struct PullArgs {
     const int32_t *active;
     int64_t *np_v;         // [n_warps][B] (V pull)
     double one_minus_alpha;
+    uint64_t *dbg;         // optional per-warp [start, end, edges, rows] globaltimer trace
 };
+
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 template <int B, typename T, int SIDE, int VEC>
 __device__ __forceinline__ void pull_row_final(const PullArgs<T> &a, const int32_t *s_op, int64_t row, int32_t deg,
@@ -453,13 +460,26 @@ struct Acc<float> {
     static constexpr int FLUSH = 16;
 };
 
-// B >= 32: lanes own slots; the warp streams its edge range through the ring.
+// Operand-row gather.  Plain coherent loads (ld.global, L1-cached): the
+// operand was written by the previous kernel of the round.
+template <typename T, int VEC>
+__device__ __forceinline__ void ldg_vec(const T *p, T (&v)[VEC]) {
+    VecIO<T, VEC>::ld(p, v);
+}
+
+// Pipeline depth (edges in flight per warp): registers hold S operand rows.
+template <int B, typename T>
+struct RegPipe {
+    static constexpr int VEC = B / 32;
+    static constexpr int S = (VEC * (int)sizeof(T) <= 8) ? 16 : 8;
+};
+
+// B >= 32: lanes own slots; each warp streams its edge range with S operand
+// rows in flight in registers (fully unrolled blocks of S edges).
 template <int B, typename T, int SIDE>
 __global__ void __launch_bounds__(PULL_THREADS, 2) k_pull(PullArgs<T> a) {
     if (*a.active == 0) return;
-    using PC = Pipe<B, T>;
-    constexpr int VEC = PC::VEC, ROW = PC::ROW, LPE = PC::LPE, CPE = PC::CPE, EPI = PC::EPI, S = PC::S;
-    extern __shared__ __align__(16) unsigned char dsm[];
+    constexpr int VEC = RegPipe<B, T>::VEC, S = RegPipe<B, T>::S;
     __shared__ int32_t s_op[MAX_B];
     for (int s = threadIdx.x; s < B; s += blockDim.x) s_op[s] = a.slots[s].op;
     __syncthreads();
@@ -470,12 +490,8 @@ __global__ void __launch_bounds__(PULL_THREADS, 2) k_pull(PullArgs<T> a) {
     int64_t np[VEC];
 #pragma unroll
     for (int v = 0; v < VEC; v++) np[v] = 0;
-    unsigned char *ring = dsm + (size_t)warp * PC::WARP_SMEM;
-    const T *rval = reinterpret_cast<const T *>(ring + S * ROW);
-    const T *xlane = reinterpret_cast<const T *>(ring) + slot0;
-    const uint32_t ring_u32 = smem_u32(ring);
-    const uint32_t rval_u32 = smem_u32(rval);
 
+    const uint64_t t_start = a.dbg ? gtimer() : 0;
     if (gw < a.n_warps) {
         const WarpWork wk = a.work[gw];
         const int64_t e0 = wk.e0;
@@ -483,84 +499,62 @@ __global__ void __launch_bounds__(PULL_THREADS, 2) k_pull(PullArgs<T> a) {
         if (n > 0) {
             const int32_t *cols = a.indices + e0;
             const T *vals = a.vals + e0;
-            // ---- issue side: column indices in 32-edge windows (double buffered)
-            int ib = 0;
-            int icol = lane < n ? __ldg(cols + lane) : 0;
-            int icol_nx = 32 + lane < n ? __ldg(cols + 32 + lane) : 0;
-            const int grp = lane / LPE, q = lane % LPE;
-            const uint32_t qoff = (uint32_t)q * 16;
-            auto issue = [&](int io) {  // edges [io, io + EPI)
-                if (io >= ib + 32) {
-                    ib += 32;
-                    icol = icol_nx;
-                    icol_nx = ib + 32 + lane < n ? __ldg(cols + ib + 32 + lane) : 0;
-                }
-                const int o = io + grp;
-                const int c = __shfl_sync(0xffffffffu, icol, (o - ib) & 31);
-                if (o < n) {
-                    const uint32_t st = (uint32_t)(o & (S - 1));
-                    const unsigned char *src = reinterpret_cast<const unsigned char *>(a.X + (int64_t)c * B) + qoff;
-                    const uint32_t dst = ring_u32 + st * ROW + qoff;
+            const T *X = a.X + slot0;
+            // issue windows: lane l holds (col, val) of edge wb + l
+            int wcol = lane < n ? __ldg(cols + lane) : 0;
+            T wval = lane < n ? __ldg(vals + lane) : (T)0;
+            int wcol_nx = 32 + lane < n ? __ldg(cols + 32 + lane) : 0;
+            T wval_nx = 32 + lane < n ? __ldg(vals + 32 + lane) : (T)0;
+            int wb = 0;  // first edge of the current issue window
+            T xs[S][VEC];
+            T wsv[S];
 #pragma unroll
-                    for (int k = 0; k < CPE; k++) cp_async<16>(dst + k * LPE * 16, src + k * LPE * 16);
-                    if (q == 0) cp_async<(int)sizeof(T)>(rval_u32 + st * (uint32_t)sizeof(T), vals + o);
-                }
-                cp_async_commit();
-            };
-#pragma unroll
-            for (int p = 0; p < S / EPI; p++) issue(p * EPI);
-
-            // ---- consume side: rows in order, row ends in 32-row windows
+            for (int t = 0; t < S; t++) {
+                const int c = __shfl_sync(0xffffffffu, wcol, t);
+                wsv[t] = __shfl_sync(0xffffffffu, wval, t);
+                if (t < n) ldg_vec<T, VEC>(X + (int64_t)c * B, xs[t]);
+            }
+            // rows
             int64_t row = wk.r0;
             int64_t rwin = row;
             auto rend_of = [&](int64_t r) { return __ldg(a.indptr + (r <= a.n_rows ? r : a.n_rows)); };
             int64_t my_rend = rend_of(rwin + lane + 1);
-            const int64_t rs0 = __ldg(a.indptr + row);
+            int64_t rstart_abs = __ldg(a.indptr + row);
             int64_t rend_abs = __shfl_sync(0xffffffffu, my_rend, 0);
-            int64_t rstart_abs = rs0;
-            int oend = (int)imin64(rend_abs - e0, n);  // end offset of the current row (clipped)
+            int oend = (int)imin64(rend_abs - e0, n);
             double acc[VEC];
-            T acc_s[VEC];
-            int since = 0;
+            T accs[VEC];
 #pragma unroll
             for (int v = 0; v < VEC; v++) {
                 acc[v] = 0.0;
-                acc_s[v] = (T)0;
+                accs[v] = (T)0;
             }
-            for (int co = 0; co < n; co += EPI) {
-                cp_async_wait<S / EPI - 1>();
-                __syncwarp();
+            for (int base = 0; base < n; base += S) {
+                if (((base + S) & 31) == 0) {  // next issues start a new 32-edge window
+                    wb = base + S;
+                    wcol = wcol_nx;
+                    wval = wval_nx;
+                    wcol_nx = wb + 32 + lane < n ? __ldg(cols + wb + 32 + lane) : 0;
+                    wval_nx = wb + 32 + lane < n ? __ldg(vals + wb + 32 + lane) : (T)0;
+                }
 #pragma unroll
-                for (int t = 0; t < EPI; t++) {
-                    const int o = co + t;
+                for (int t = 0; t < S; t++) {
+                    const int o = base + t;
                     if (o < n) {
-                        const int st = o & (S - 1);
-                        T xv[VEC];
-                        VecIO<T, VEC>::ld(xlane + st * (ROW / (int)sizeof(T)), xv);
-                        const T w = rval[st];
-                        if constexpr (Acc<T>::FLUSH >= (1 << 30)) {
+                        if constexpr (sizeof(T) == 8) {
 #pragma unroll
-                            for (int v = 0; v < VEC; v++) acc[v] = fma((double)w, (double)xv[v], acc[v]);
+                            for (int v = 0; v < VEC; v++) acc[v] = fma((double)wsv[t], (double)xs[t][v], acc[v]);
                         } else {
 #pragma unroll
-                            for (int v = 0; v < VEC; v++) acc_s[v] = fmaf(w, xv[v], acc_s[v]);
-                            if (++since == Acc<T>::FLUSH) {
-#pragma unroll
-                                for (int v = 0; v < VEC; v++) {
-                                    acc[v] += (double)acc_s[v];
-                                    acc_s[v] = (T)0;
-                                }
-                                since = 0;
-                            }
+                            for (int v = 0; v < VEC; v++) accs[v] = fmaf(wsv[t], xs[t][v], accs[v]);
                         }
                         if (o + 1 == oend) {
-                            if constexpr (Acc<T>::FLUSH < (1 << 30)) {
+                            if constexpr (sizeof(T) == 4) {
 #pragma unroll
                                 for (int v = 0; v < VEC; v++) {
-                                    acc[v] += (double)acc_s[v];
-                                    acc_s[v] = (T)0;
+                                    acc[v] += (double)accs[v];
+                                    accs[v] = (T)0;
                                 }
-                                since = 0;
                             }
                             const bool cut = rstart_abs < e0 || rend_abs > wk.e1;
                             if (!cut) {
@@ -588,12 +582,29 @@ __global__ void __launch_bounds__(PULL_THREADS, 2) k_pull(PullArgs<T> a) {
                             oend = (int)imin64(rend_abs - e0, n);
                         }
                     }
+                    // refill slot t with edge o + S
+                    const int oi = o + S;
+                    const int c = __shfl_sync(0xffffffffu, wcol, (oi - wb) & 31);
+                    wsv[t] = __shfl_sync(0xffffffffu, wval, (oi - wb) & 31);
+                    if (oi < n) ldg_vec<T, VEC>(X + (int64_t)c * B, xs[t]);
                 }
-                __syncwarp();
-                issue(co + S);
+                if constexpr (sizeof(T) == 4) {  // bound the fp32 partial to S terms
+#pragma unroll
+                    for (int v = 0; v < VEC; v++) {
+                        acc[v] += (double)accs[v];
+                        accs[v] = (T)0;
+                    }
+                }
             }
-            cp_async_wait<0>();
         }
+    }
+    if (a.dbg && lane == 0 && gw < a.n_warps) {
+        a.dbg[gw * 4 + 0] = t_start;
+        a.dbg[gw * 4 + 1] = gtimer();
+        a.dbg[gw * 4 + 2] = (uint64_t)(a.work[gw].e1 - a.work[gw].e0);
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+        a.dbg[gw * 4 + 3] = smid;
     }
     if constexpr (SIDE == SIDE_V) {
         if (gw < a.n_warps)
