@@ -471,27 +471,94 @@ __device__ __forceinline__ void ldg_vec(const T *p, T (&v)[VEC]) {
 template <int B, typename T>
 struct RegPipe {
     static constexpr int VEC = B / 32;
-    static constexpr int S = (VEC * (int)sizeof(T) <= 8) ? 16 : 8;
+    static constexpr int LANE_BYTES = VEC * (int)sizeof(T);
+    static constexpr int S = (sizeof(T) == 4 && LANE_BYTES <= 8) ? 16 : (LANE_BYTES <= 16 ? 8 : 4);
 };
 
+// Rare path of the pull: a row cut by a warp-range boundary.  Publishes this
+// warp's fp64 partial; the last warp to arrive adds the partials in warp order
+// and writes the row.  Returns the row's n_p contribution (V pull) per slot.
+template <typename T>
+struct CutCtx {
+    double *scratch;
+    int32_t *cut_count;
+    const CutRow *cuts;
+    T *Y;
+    const int64_t *indptr;
+    double scale;  // (1 - alpha) on the V side, 1 on the U side
+};
+
+template <int B, typename T, int VEC>
+__device__ __noinline__ IVec<VEC> pull_cut(CutCtx<T> cx, int ci, int pi, int slot0, uint32_t cmask, DVec<VEC> acc) {
+    const int lane = threadIdx.x & 31;
+    IVec<VEC> inc;
+#pragma unroll
+    for (int v = 0; v < VEC; v++) inc.v[v] = 0;
+#pragma unroll
+    for (int v = 0; v < VEC; v++) cx.scratch[(int64_t)pi * B + slot0 + v] = acc.v[v];
+    __threadfence();
+    __syncwarp();
+    const CutRow cr = cx.cuts[ci];
+    int last = 0;
+    if (lane == 0) last = atomicAdd(cx.cut_count + ci, 1) == cr.n_parts - 1;
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (!last) return inc;
+    __threadfence();
+    double tot[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; v++) tot[v] = 0.0;
+    int p = 0;
+    for (; p + 4 <= cr.n_parts; p += 4) {  // 4 partials in flight
+        double q[4][VEC];
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+#pragma unroll
+            for (int v = 0; v < VEC; v++) q[k][v] = __ldcg(cx.scratch + (int64_t)(cr.first_part + p + k) * B + slot0 + v);
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+#pragma unroll
+            for (int v = 0; v < VEC; v++) tot[v] += q[k][v];
+    }
+    for (; p < cr.n_parts; p++)
+#pragma unroll
+        for (int v = 0; v < VEC; v++) tot[v] += __ldcg(cx.scratch + (int64_t)(cr.first_part + p) * B + slot0 + v);
+    const int64_t deg = __ldg(cx.indptr + cr.row + 1) - __ldg(cx.indptr + cr.row);
+    T out[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; v++) {
+        out[v] = (T)(cx.scale * tot[v]);
+        if (((cmask >> v) & 1u) && (double)out[v] > 0.0) inc.v[v] = deg;
+    }
+    VecIO<T, VEC>::st(cx.Y + (int64_t)cr.row * B + slot0, out);
+    if (lane == 0) cx.cut_count[ci] = 0;
+    return inc;
+}
+
 // B >= 32: lanes own slots; each warp streams its edge range with S operand
-// rows in flight in registers (fully unrolled blocks of S edges).
+// rows in flight in registers (fully unrolled 32-edge chunks).
 template <int B, typename T, int SIDE>
 __global__ void __launch_bounds__(PULL_THREADS, 2) k_pull(PullArgs<T> a) {
     if (*a.active == 0) return;
     constexpr int VEC = RegPipe<B, T>::VEC, S = RegPipe<B, T>::S;
-    __shared__ int32_t s_op[MAX_B];
-    for (int s = threadIdx.x; s < B; s += blockDim.x) s_op[s] = a.slots[s].op;
-    __syncthreads();
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int gw = blockIdx.x * PULL_WARPS + warp;
     const int slot0 = lane * VEC;
-    int64_t np[VEC];
+    // V side: n_p counts deg(v) for r_v > 0 of slots in a push round
+    uint32_t cmask = 0;
+    if constexpr (SIDE == SIDE_V) {
+#pragma unroll
+        for (int v = 0; v < VEC; v++) cmask |= (op_is_push(a.slots[slot0 + v].op) ? 1u : 0u) << v;
+    }
+    const double scale = SIDE == SIDE_V ? a.one_minus_alpha : 1.0;
+    int32_t np[VEC];
 #pragma unroll
     for (int v = 0; v < VEC; v++) np[v] = 0;
-
+    int64_t np_cut[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; v++) np_cut[v] = 0;
     const uint64_t t_start = a.dbg ? gtimer() : 0;
+
     if (gw < a.n_warps) {
         const WarpWork wk = a.work[gw];
         const int64_t e0 = wk.e0;
@@ -500,12 +567,16 @@ __global__ void __launch_bounds__(PULL_THREADS, 2) k_pull(PullArgs<T> a) {
             const int32_t *cols = a.indices + e0;
             const T *vals = a.vals + e0;
             const T *X = a.X + slot0;
+            T *Yl = a.Y + slot0;
+            // rows cut by this warp's range (-1: none)
+            const int64_t cutA = wk.cut0 >= 0 ? (int64_t)wk.r0 : -1;
+            const int64_t cutB = wk.cut1 >= 0 ? (int64_t)a.cuts[wk.cut1].row : -1;
             // issue windows: lane l holds (col, val) of edge wb + l
             int wcol = lane < n ? __ldg(cols + lane) : 0;
             T wval = lane < n ? __ldg(vals + lane) : (T)0;
             int wcol_nx = 32 + lane < n ? __ldg(cols + 32 + lane) : 0;
             T wval_nx = 32 + lane < n ? __ldg(vals + 32 + lane) : (T)0;
-            int wb = 0;  // first edge of the current issue window
+            int wb = 0;
             T xs[S][VEC];
             T wsv[S];
 #pragma unroll
@@ -514,14 +585,13 @@ __global__ void __launch_bounds__(PULL_THREADS, 2) k_pull(PullArgs<T> a) {
                 wsv[t] = __shfl_sync(0xffffffffu, wval, t);
                 if (t < n) ldg_vec<T, VEC>(X + (int64_t)c * B, xs[t]);
             }
-            // rows
+            // rows: ends of 32 rows per window
             int64_t row = wk.r0;
             int64_t rwin = row;
-            auto rend_of = [&](int64_t r) { return __ldg(a.indptr + (r <= a.n_rows ? r : a.n_rows)); };
-            int64_t my_rend = rend_of(rwin + lane + 1);
-            int64_t rstart_abs = __ldg(a.indptr + row);
-            int64_t rend_abs = __shfl_sync(0xffffffffu, my_rend, 0);
-            int oend = (int)imin64(rend_abs - e0, n);
+            int64_t my_rend = __ldg(a.indptr + imin64(rwin + lane + 1, a.n_rows));
+            int64_t rstart = __ldg(a.indptr + row);
+            int64_t rend = __shfl_sync(0xffffffffu, my_rend, 0);
+            int oend = (int)imin64(rend - e0, n);
             double acc[VEC];
             T accs[VEC];
 #pragma unroll
@@ -529,8 +599,89 @@ __global__ void __launch_bounds__(PULL_THREADS, 2) k_pull(PullArgs<T> a) {
                 acc[v] = 0.0;
                 accs[v] = (T)0;
             }
-            for (int base = 0; base < n; base += S) {
-                if (((base + S) & 31) == 0) {  // next issues start a new 32-edge window
+            auto emit = [&]() {  // current row complete (or this warp's part of it)
+                if constexpr (sizeof(T) == 4) {
+#pragma unroll
+                    for (int v = 0; v < VEC; v++) acc[v] += (double)accs[v];
+                }
+                if (row == cutA || row == cutB) {
+                    DVec<VEC> av;
+#pragma unroll
+                    for (int v = 0; v < VEC; v++) av.v[v] = acc[v];
+                    const CutCtx<T> cx{a.scratch, a.cut_count, a.cuts, a.Y, a.indptr, scale};
+                    const IVec<VEC> inc = pull_cut<B, T, VEC>(cx, row == cutA ? wk.cut0 : wk.cut1,
+                                                             row == cutA ? wk.part0 : wk.part1, slot0, cmask, av);
+#pragma unroll
+                    for (int v = 0; v < VEC; v++) np_cut[v] += inc.v[v];
+                } else {
+                    T out[VEC];
+                    const int32_t deg = (int32_t)(rend - rstart);
+#pragma unroll
+                    for (int v = 0; v < VEC; v++) {
+                        out[v] = (T)(scale * acc[v]);
+                        if constexpr (SIDE == SIDE_V) np[v] += (((cmask >> v) & 1u) && out[v] > (T)0) ? deg : 0;
+                    }
+                    VecIO<T, VEC>::st(Yl + row * B, out);
+                }
+#pragma unroll
+                for (int v = 0; v < VEC; v++) {
+                    acc[v] = 0.0;
+                    accs[v] = (T)0;
+                }
+                row++;
+                rstart = rend;
+                if (row - rwin >= 32) {
+                    rwin = row;
+                    my_rend = __ldg(a.indptr + imin64(rwin + lane + 1, a.n_rows));
+                }
+                rend = __shfl_sync(0xffffffffu, my_rend, (int)(row - rwin) & 31);
+                oend = (int)imin64(rend - e0, n);
+            };
+            auto consume = [&](int t) {
+                if constexpr (sizeof(T) == 8) {
+#pragma unroll
+                    for (int v = 0; v < VEC; v++) acc[v] = fma((double)wsv[t], (double)xs[t][v], acc[v]);
+                } else {
+#pragma unroll
+                    for (int v = 0; v < VEC; v++) accs[v] = fmaf(wsv[t], xs[t][v], accs[v]);
+                }
+            };
+            auto flush_s = [&]() {  // bound the fp32 partial to S terms
+                if constexpr (sizeof(T) == 4) {
+#pragma unroll
+                    for (int v = 0; v < VEC; v++) {
+                        acc[v] += (double)accs[v];
+                        accs[v] = (T)0;
+                    }
+                }
+            };
+            // ---- fast path: 32-edge chunks, every consume and issue in range
+            int c0 = 0;
+            for (; c0 + 32 + S <= n; c0 += 32) {
+                int d = oend - c0 - 1;  // chunk offset of the current row's last edge
+#pragma unroll
+                for (int t = 0; t < 32; t++) {
+                    const int sl = t & (S - 1);
+                    consume(sl);
+                    if (d == t) {
+                        emit();
+                        d = oend - c0 - 1;
+                    }
+                    const int src = (t + S) & 31;
+                    const int c = __shfl_sync(0xffffffffu, (t + S < 32) ? wcol : wcol_nx, src);
+                    wsv[sl] = __shfl_sync(0xffffffffu, (t + S < 32) ? wval : wval_nx, src);
+                    ldg_vec<T, VEC>(X + (int64_t)c * B, xs[sl]);
+                    if (sl == S - 1) flush_s();
+                }
+                wb = c0 + 32;
+                wcol = wcol_nx;
+                wval = wval_nx;
+                wcol_nx = wb + 32 + lane < n ? __ldg(cols + wb + 32 + lane) : 0;
+                wval_nx = wb + 32 + lane < n ? __ldg(vals + wb + 32 + lane) : (T)0;
+            }
+            // ---- tail: blocks of S edges with range checks
+            for (int base = c0; base < n; base += S) {
+                if (((base + S) & 31) == 0) {
                     wb = base + S;
                     wcol = wcol_nx;
                     wval = wval_nx;
@@ -541,60 +692,15 @@ __global__ void __launch_bounds__(PULL_THREADS, 2) k_pull(PullArgs<T> a) {
                 for (int t = 0; t < S; t++) {
                     const int o = base + t;
                     if (o < n) {
-                        if constexpr (sizeof(T) == 8) {
-#pragma unroll
-                            for (int v = 0; v < VEC; v++) acc[v] = fma((double)wsv[t], (double)xs[t][v], acc[v]);
-                        } else {
-#pragma unroll
-                            for (int v = 0; v < VEC; v++) accs[v] = fmaf(wsv[t], xs[t][v], accs[v]);
-                        }
-                        if (o + 1 == oend) {
-                            if constexpr (sizeof(T) == 4) {
-#pragma unroll
-                                for (int v = 0; v < VEC; v++) {
-                                    acc[v] += (double)accs[v];
-                                    accs[v] = (T)0;
-                                }
-                            }
-                            const bool cut = rstart_abs < e0 || rend_abs > wk.e1;
-                            if (!cut) {
-                                pull_row_final<B, T, SIDE, VEC>(a, s_op, row, (int32_t)(rend_abs - rstart_abs), slot0,
-                                                                acc, np);
-                            } else {
-                                const bool first = row == wk.r0;
-                                DVec<VEC> av;
-#pragma unroll
-                                for (int v = 0; v < VEC; v++) av.v[v] = acc[v];
-                                const IVec<VEC> inc = pull_cut_row<B, T, SIDE, VEC>(
-                                    a, s_op, first ? wk.cut0 : wk.cut1, first ? wk.part0 : wk.part1, slot0, av);
-#pragma unroll
-                                for (int v = 0; v < VEC; v++) np[v] += inc.v[v];
-                            }
-#pragma unroll
-                            for (int v = 0; v < VEC; v++) acc[v] = 0.0;
-                            row++;
-                            rstart_abs = rend_abs;
-                            if (row - rwin >= 32) {
-                                rwin = row;
-                                my_rend = rend_of(rwin + lane + 1);
-                            }
-                            rend_abs = __shfl_sync(0xffffffffu, my_rend, (int)(row - rwin) & 31);
-                            oend = (int)imin64(rend_abs - e0, n);
-                        }
+                        consume(t);
+                        if (o + 1 == oend) emit();
                     }
-                    // refill slot t with edge o + S
                     const int oi = o + S;
                     const int c = __shfl_sync(0xffffffffu, wcol, (oi - wb) & 31);
                     wsv[t] = __shfl_sync(0xffffffffu, wval, (oi - wb) & 31);
                     if (oi < n) ldg_vec<T, VEC>(X + (int64_t)c * B, xs[t]);
                 }
-                if constexpr (sizeof(T) == 4) {  // bound the fp32 partial to S terms
-#pragma unroll
-                    for (int v = 0; v < VEC; v++) {
-                        acc[v] += (double)accs[v];
-                        accs[v] = (T)0;
-                    }
-                }
+                flush_s();
             }
         }
     }
@@ -603,13 +709,13 @@ __global__ void __launch_bounds__(PULL_THREADS, 2) k_pull(PullArgs<T> a) {
         a.dbg[gw * 4 + 1] = gtimer();
         a.dbg[gw * 4 + 2] = (uint64_t)(a.work[gw].e1 - a.work[gw].e0);
         uint32_t smid;
-        asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         a.dbg[gw * 4 + 3] = smid;
     }
     if constexpr (SIDE == SIDE_V) {
         if (gw < a.n_warps)
 #pragma unroll
-            for (int v = 0; v < VEC; v++) a.np_v[(int64_t)(slot0 + v) * a.n_warps + gw] = np[v];
+            for (int v = 0; v < VEC; v++) a.np_v[(int64_t)(slot0 + v) * a.n_warps + gw] = (int64_t)np[v] + np_cut[v];
     }
 }
 
