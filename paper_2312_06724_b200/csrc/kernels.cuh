@@ -535,7 +535,11 @@ __device__ __noinline__ IVec<VEC> pull_cut(CutCtx<T> cx, int ci, int pi, int slo
 }
 
 // B >= 32: lanes own slots; each warp streams its edge range with S operand
-// rows in flight in registers (fully unrolled 32-edge chunks).
+// rows in flight in registers.  One loop of S-edge blocks, fully unrolled, no
+// range checks: the (col, val) windows are zero-padded past the range, so the
+// trailing issues gather row 0 with weight 0.  Row ends are 32-bit offsets;
+// rows cut by the range boundary keep their partial in registers and are
+// published after the loop.
 template <int B, typename T, int SIDE>
 __global__ void __launch_bounds__(PULL_THREADS, 2) k_pull(PullArgs<T> a) {
     if (*a.active == 0) return;
@@ -544,8 +548,7 @@ __global__ void __launch_bounds__(PULL_THREADS, 2) k_pull(PullArgs<T> a) {
     const int warp = threadIdx.x >> 5;
     const int gw = blockIdx.x * PULL_WARPS + warp;
     const int slot0 = lane * VEC;
-    // V side: n_p counts deg(v) for r_v > 0 of slots in a push round
-    uint32_t cmask = 0;
+    uint32_t cmask = 0;  // V side: slots in a push round count n_p
     if constexpr (SIDE == SIDE_V) {
 #pragma unroll
         for (int v = 0; v < VEC; v++) cmask |= (op_is_push(a.slots[slot0 + v].op) ? 1u : 0u) << v;
@@ -567,140 +570,126 @@ __global__ void __launch_bounds__(PULL_THREADS, 2) k_pull(PullArgs<T> a) {
             const int32_t *cols = a.indices + e0;
             const T *vals = a.vals + e0;
             const T *X = a.X + slot0;
-            T *Yl = a.Y + slot0;
-            // rows cut by this warp's range (-1: none)
-            const int64_t cutA = wk.cut0 >= 0 ? (int64_t)wk.r0 : -1;
-            const int64_t cutB = wk.cut1 >= 0 ? (int64_t)a.cuts[wk.cut1].row : -1;
-            // issue windows: lane l holds (col, val) of edge wb + l
-            int wcol = lane < n ? __ldg(cols + lane) : 0;
-            T wval = lane < n ? __ldg(vals + lane) : (T)0;
-            int wcol_nx = 32 + lane < n ? __ldg(cols + 32 + lane) : 0;
-            T wval_nx = 32 + lane < n ? __ldg(vals + 32 + lane) : (T)0;
-            int wb = 0;
+            T *Y0 = a.Y + (int64_t)wk.r0 * B + slot0;
+            const int64_t *rp = a.indptr + wk.r0;  // row r0 + i ends at rp[i + 1]
+            const int64_t nrow_left = a.n_rows - wk.r0;
+            // local row index of the cut rows (-1: none)
+            const int cutA = wk.cut0 >= 0 ? 0 : -1;
+            const int cutB = wk.cut1 >= 0 ? (int)(a.cuts[wk.cut1].row - wk.r0) : -1;
+            auto col_at = [&](int o) { return o < n ? __ldg(cols + o) : 0; };
+            auto val_at = [&](int o) { return o < n ? __ldg(vals + o) : (T)0; };
+            auto rend_at = [&](int i) {  // clipped end offset of local row i
+                const int64_t r = i + 1 <= nrow_left ? __ldg(rp + i + 1) : __ldg(rp + nrow_left);
+                return (int)imin64(imin64(r - e0, n), (int64_t)n);
+            };
             T xs[S][VEC];
             T wsv[S];
+            {
+                const int c = col_at(lane);
+                const T w = val_at(lane);
 #pragma unroll
-            for (int t = 0; t < S; t++) {
-                const int c = __shfl_sync(0xffffffffu, wcol, t);
-                wsv[t] = __shfl_sync(0xffffffffu, wval, t);
-                if (t < n) ldg_vec<T, VEC>(X + (int64_t)c * B, xs[t]);
+                for (int t = 0; t < S; t++) {
+                    const int ct = __shfl_sync(0xffffffffu, c, t);
+                    wsv[t] = __shfl_sync(0xffffffffu, w, t);
+                    ldg_vec<T, VEC>(X + (int64_t)ct * B, xs[t]);
+                }
             }
-            // rows: ends of 32 rows per window
-            int64_t row = wk.r0;
-            int64_t rwin = row;
-            int64_t my_rend = __ldg(a.indptr + imin64(rwin + lane + 1, a.n_rows));
-            int64_t rstart = __ldg(a.indptr + row);
-            int64_t rend = __shfl_sync(0xffffffffu, my_rend, 0);
-            int oend = (int)imin64(rend - e0, n);
-            double acc[VEC];
+            // windows of the next blocks' issues: lane t < S holds edge base + S + t
+            int cw = col_at(S + lane), cw1 = col_at(2 * S + lane);
+            T vw = val_at(S + lane), vw1 = val_at(2 * S + lane);
+            // row ends, 32 rows per window (current and next)
+            int rw = 0;
+            int re0 = rend_at(lane), re1 = rend_at(32 + lane);
+            int lr = 0;                                    // local row index
+            int rstart = (int)(__ldg(rp) - e0);            // may be < 0 for a cut first row
+            int rend = __shfl_sync(0xffffffffu, re0, 0);
+            double acc[VEC], accA[VEC], accB[VEC];
             T accs[VEC];
 #pragma unroll
             for (int v = 0; v < VEC; v++) {
-                acc[v] = 0.0;
+                acc[v] = accA[v] = accB[v] = 0.0;
                 accs[v] = (T)0;
             }
-            auto emit = [&]() {  // current row complete (or this warp's part of it)
-                if constexpr (sizeof(T) == 4) {
+            for (int base = 0; base < n; base += S) {
+                int d = rend - base - 1;  // block offset of the current row's last edge
 #pragma unroll
-                    for (int v = 0; v < VEC; v++) acc[v] += (double)accs[v];
-                }
-                if (row == cutA || row == cutB) {
-                    DVec<VEC> av;
+                for (int t = 0; t < S; t++) {
+                    if constexpr (sizeof(T) == 8) {
 #pragma unroll
-                    for (int v = 0; v < VEC; v++) av.v[v] = acc[v];
-                    const CutCtx<T> cx{a.scratch, a.cut_count, a.cuts, a.Y, a.indptr, scale};
-                    const IVec<VEC> inc = pull_cut<B, T, VEC>(cx, row == cutA ? wk.cut0 : wk.cut1,
-                                                             row == cutA ? wk.part0 : wk.part1, slot0, cmask, av);
+                        for (int v = 0; v < VEC; v++) acc[v] = fma((double)wsv[t], (double)xs[t][v], acc[v]);
+                    } else {
 #pragma unroll
-                    for (int v = 0; v < VEC; v++) np_cut[v] += inc.v[v];
-                } else {
-                    T out[VEC];
-                    const int32_t deg = (int32_t)(rend - rstart);
-#pragma unroll
-                    for (int v = 0; v < VEC; v++) {
-                        out[v] = (T)(scale * acc[v]);
-                        if constexpr (SIDE == SIDE_V) np[v] += (((cmask >> v) & 1u) && out[v] > (T)0) ? deg : 0;
+                        for (int v = 0; v < VEC; v++) accs[v] = fmaf(wsv[t], xs[t][v], accs[v]);
                     }
-                    VecIO<T, VEC>::st(Yl + row * B, out);
-                }
+                    if (d == t) {  // ---- row emit
+                        if constexpr (sizeof(T) == 4) {
 #pragma unroll
-                for (int v = 0; v < VEC; v++) {
-                    acc[v] = 0.0;
-                    accs[v] = (T)0;
-                }
-                row++;
-                rstart = rend;
-                if (row - rwin >= 32) {
-                    rwin = row;
-                    my_rend = __ldg(a.indptr + imin64(rwin + lane + 1, a.n_rows));
-                }
-                rend = __shfl_sync(0xffffffffu, my_rend, (int)(row - rwin) & 31);
-                oend = (int)imin64(rend - e0, n);
-            };
-            auto consume = [&](int t) {
-                if constexpr (sizeof(T) == 8) {
+                            for (int v = 0; v < VEC; v++) {
+                                acc[v] += (double)accs[v];
+                                accs[v] = (T)0;
+                            }
+                        }
+                        if (lr == cutA) {
 #pragma unroll
-                    for (int v = 0; v < VEC; v++) acc[v] = fma((double)wsv[t], (double)xs[t][v], acc[v]);
-                } else {
+                            for (int v = 0; v < VEC; v++) accA[v] = acc[v];
+                        } else if (lr == cutB) {
 #pragma unroll
-                    for (int v = 0; v < VEC; v++) accs[v] = fmaf(wsv[t], xs[t][v], accs[v]);
+                            for (int v = 0; v < VEC; v++) accB[v] = acc[v];
+                        } else {
+                            T out[VEC];
+#pragma unroll
+                            for (int v = 0; v < VEC; v++) {
+                                out[v] = (T)(scale * acc[v]);
+                                if constexpr (SIDE == SIDE_V)
+                                    np[v] += (((cmask >> v) & 1u) && out[v] > (T)0) ? rend - rstart : 0;
+                            }
+                            VecIO<T, VEC>::st(Y0 + (int64_t)lr * B, out);
+                        }
+#pragma unroll
+                        for (int v = 0; v < VEC; v++) acc[v] = 0.0;
+                        lr++;
+                        rstart = rend;
+                        if (lr - rw >= 32) {
+                            rw += 32;
+                            re0 = re1;
+                            re1 = rend_at(rw + 32 + lane);
+                        }
+                        rend = __shfl_sync(0xffffffffu, re0, lr - rw);
+                        d = rend - base - 1;
+                    }
+                    const int ct = __shfl_sync(0xffffffffu, cw, t);
+                    wsv[t] = __shfl_sync(0xffffffffu, vw, t);
+                    ldg_vec<T, VEC>(X + (int64_t)ct * B, xs[t]);
                 }
-            };
-            auto flush_s = [&]() {  // bound the fp32 partial to S terms
-                if constexpr (sizeof(T) == 4) {
+                if constexpr (sizeof(T) == 4) {  // bound the fp32 partial to S terms
 #pragma unroll
                     for (int v = 0; v < VEC; v++) {
                         acc[v] += (double)accs[v];
                         accs[v] = (T)0;
                     }
                 }
-            };
-            // ---- fast path: 32-edge chunks, every consume and issue in range
-            int c0 = 0;
-            for (; c0 + 32 + S <= n; c0 += 32) {
-                int d = oend - c0 - 1;  // chunk offset of the current row's last edge
-#pragma unroll
-                for (int t = 0; t < 32; t++) {
-                    const int sl = t & (S - 1);
-                    consume(sl);
-                    if (d == t) {
-                        emit();
-                        d = oend - c0 - 1;
-                    }
-                    const int src = (t + S) & 31;
-                    const int c = __shfl_sync(0xffffffffu, (t + S < 32) ? wcol : wcol_nx, src);
-                    wsv[sl] = __shfl_sync(0xffffffffu, (t + S < 32) ? wval : wval_nx, src);
-                    ldg_vec<T, VEC>(X + (int64_t)c * B, xs[sl]);
-                    if (sl == S - 1) flush_s();
-                }
-                wb = c0 + 32;
-                wcol = wcol_nx;
-                wval = wval_nx;
-                wcol_nx = wb + 32 + lane < n ? __ldg(cols + wb + 32 + lane) : 0;
-                wval_nx = wb + 32 + lane < n ? __ldg(vals + wb + 32 + lane) : (T)0;
+                cw = cw1;
+                vw = vw1;
+                cw1 = col_at(base + 3 * S + lane);
+                vw1 = val_at(base + 3 * S + lane);
             }
-            // ---- tail: blocks of S edges with range checks
-            for (int base = c0; base < n; base += S) {
-                if (((base + S) & 31) == 0) {
-                    wb = base + S;
-                    wcol = wcol_nx;
-                    wval = wval_nx;
-                    wcol_nx = wb + 32 + lane < n ? __ldg(cols + wb + 32 + lane) : 0;
-                    wval_nx = wb + 32 + lane < n ? __ldg(vals + wb + 32 + lane) : (T)0;
-                }
+            // publish cut rows (rare path, out of line)
+            const CutCtx<T> cx{a.scratch, a.cut_count, a.cuts, a.Y, a.indptr, scale};
+            if (cutA >= 0) {
+                DVec<VEC> av;
 #pragma unroll
-                for (int t = 0; t < S; t++) {
-                    const int o = base + t;
-                    if (o < n) {
-                        consume(t);
-                        if (o + 1 == oend) emit();
-                    }
-                    const int oi = o + S;
-                    const int c = __shfl_sync(0xffffffffu, wcol, (oi - wb) & 31);
-                    wsv[t] = __shfl_sync(0xffffffffu, wval, (oi - wb) & 31);
-                    if (oi < n) ldg_vec<T, VEC>(X + (int64_t)c * B, xs[t]);
-                }
-                flush_s();
+                for (int v = 0; v < VEC; v++) av.v[v] = accA[v];
+                const IVec<VEC> inc = pull_cut<B, T, VEC>(cx, wk.cut0, wk.part0, slot0, cmask, av);
+#pragma unroll
+                for (int v = 0; v < VEC; v++) np_cut[v] += inc.v[v];
+            }
+            if (cutB >= 0) {
+                DVec<VEC> av;
+#pragma unroll
+                for (int v = 0; v < VEC; v++) av.v[v] = accB[v];
+                const IVec<VEC> inc = pull_cut<B, T, VEC>(cx, wk.cut1, wk.part1, slot0, cmask, av);
+#pragma unroll
+                for (int v = 0; v < VEC; v++) np_cut[v] += inc.v[v];
             }
         }
     }
