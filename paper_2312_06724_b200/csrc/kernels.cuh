@@ -621,7 +621,7 @@ __global__ void __launch_bounds__(PULL_THREADS, 2) k_pull(PullArgs<T> a) {
 #pragma unroll
                         for (int v = 0; v < VEC; v++) accs[v] = fmaf(wsv[t], xs[t][v], accs[v]);
                     }
-                    if (d == t) {  // ---- row emit
+                    if (d == t) {  // ---- row emit (d is warp-uniform)
                         if constexpr (sizeof(T) == 4) {
 #pragma unroll
                             for (int v = 0; v < VEC; v++) {
