@@ -35,10 +35,11 @@ template <typename X>
 static X *dalloc(size_t count) {
     void *p = nullptr;
     cudaError_t e = cudaMalloc(&p, std::max<size_t>(1, count * sizeof(X)));
-    if (e != cudaSuccess) {
+    if (e == cudaErrorMemoryAllocation) {
         (void)cudaGetLastError();
         throw std::bad_alloc();
     }
+    if (e != cudaSuccess) throw CudaError(std::string("cudaMalloc: ") + cudaGetErrorString(e));
     return (X *)p;
 }
 

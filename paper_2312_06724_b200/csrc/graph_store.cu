@@ -55,7 +55,11 @@ X *dmalloc(size_t count, int64_t &acc) {
     void *p = nullptr;
     size_t bytes = std::max<size_t>(1, count * sizeof(X));
     cudaError_t e = cudaMalloc(&p, bytes);
-    if (e != cudaSuccess) throw std::bad_alloc();
+    if (e == cudaErrorMemoryAllocation) {
+        (void)cudaGetLastError();
+        throw std::bad_alloc();
+    }
+    if (e != cudaSuccess) throw CudaError(std::string("cudaMalloc: ") + cudaGetErrorString(e));
     acc += (int64_t)bytes;
     return (X *)p;
 }
