@@ -12,7 +12,7 @@ for r in rows[hdr + 1:]:
     if len(r) <= vi:
         continue
     v = float(r[vi].replace(",", ""))
-    v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(r[ui], 1.0)
+    v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0)
     name = r[ki].split("(")[0]
     agg[name][0] += 1
     agg[name][1] += v
