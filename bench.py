@@ -120,6 +120,21 @@ class Clocks:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def ncu_round_traffic():
+    """DRAM bytes (read + write) of one round's kernels from the committed ncu
+    capture (profiles/r01_ncu_round_kernels.json), or None."""
+    p = REPO / "profiles" / "r01_ncu_round_kernels.json"
+    if not p.exists():
+        return None
+    try:
+        ks = json.loads(p.read_text())["kernels"]
+        tot = sum(v.get("dram_read_MB", 0) + v.get("dram_write_MB", 0)
+                  for k, v in ks.items() if k.startswith(("k_push", "k_pull", "k_combine")))
+        return tot * 1e6
+    except Exception:
+        return None
+
+
 def peak_hbm():
     p = REPO / "MEASURED_PEAKS.json"
     if p.exists():
@@ -347,8 +362,17 @@ def run_ours(args):
             "config": config_json(cfg, n, world, prof.get("slots", 0), k),
             "roofline": {
                 "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak if achieved else None, "traffic": None,
-                "kernel": "push/PI round = K1 prep + K2 V-pull(+finisher) + K3 U-pull(+finisher)",
+                "frac": achieved / peak if achieved else None, "traffic": ncu_round_traffic(),
+                "traffic_note": "DRAM read+write bytes of one round's K1+K2+K3+K1a from one ncu --set full "
+                                "capture (profiles/r01_ncu_round_kernels.json, cold cache), per round",
+                "algorithmic_bytes_per_round": alg / max(1, prof["rounds"]),
+                "kernel": "push/PI round = K1 push + K2 V-pull + K3 U-pull + K1a combine (SURVEY 8(d) unit)",
+                "gather": {"bytes_per_round": 2 * g.edge_count * prof.get("slots", 0) * s_bytes,
+                           "achieved_tbs": (2 * g.edge_count * prof.get("slots", 0) * s_bytes * prof["rounds"]
+                                            / ((prof["ms_vpull"] + prof["ms_upull"]) / 1e3) / 1e12)
+                           if prof["ms_vpull"] + prof["ms_upull"] > 0 else None,
+                           "note": "operand-row gathers of the two pulls (E x B x s each), L2-served; "
+                                   "tools/gather_bench.cu ceiling 13-17 TB/s"},
                 "algorithmic_bytes_per_step": alg / args.steps, "kernel_ms_per_step": kern_ms / args.steps,
                 "rounds_per_step": prof["rounds"] / args.steps,
                 "share_of_step": kern_ms / pms if pms else None,
