@@ -31,6 +31,14 @@ struct InvalidArg : std::runtime_error {
 
 void count_launch(int n = 1);
 
+// Programmatic dependent launch: every round kernel lets its successor launch
+// early (the successor's blocks occupy SMs freed by this kernel's tail) and
+// waits for its predecessor's memory before touching round state.
+__device__ __forceinline__ void pdl_begin() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // ---------------------------------------------------------------------------
 // Static per-warp work of one pull side (rows = this side's nodes): a
 // contiguous edge range [e0, e1) chosen by a merge-path split of rows + edges.

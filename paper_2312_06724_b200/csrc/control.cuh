@@ -100,6 +100,7 @@ constexpr int CONTROL_THREADS = 256;
 // slot's state transition, then the last block to arrive refills free slots
 // from the query queue in slot order and publishes the round's flags.
 __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
+    pdl_begin();
     __shared__ int64_t r_cnt[CONTROL_THREADS];
     __shared__ int64_t r_np[CONTROL_THREADS];
     __shared__ double r_sum[CONTROL_THREADS];

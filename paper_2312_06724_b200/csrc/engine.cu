@@ -56,6 +56,22 @@ __global__ void k_col_set(T *X, int B, int s, int64_t n, const double *in) {
         X[u * B + s] = (T)in[u];
 }
 
+// Launch a round kernel with programmatic stream serialization (PDL).
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    BH_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+
 static int grid1d(int64_t n, int threads = 256, int cap = 148 * 16) {
     return (int)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, cap));
 }
@@ -180,6 +196,7 @@ struct Engine final : EngineBase {
     uint64_t *cand_key = nullptr;
     int64_t *cand_idx = nullptr;
     double *hook_r = nullptr, *hook_est = nullptr;
+    int32_t *chunk_done = nullptr;
     std::vector<cudaEvent_t> evpool;
     SidePlan plan_v, plan_u;
     uint64_t *dbg_v = nullptr, *dbg_u = nullptr;  // BH_DEBUG_WARP_TIMING
@@ -250,6 +267,8 @@ struct Engine final : EngineBase {
         scratch = dalloc<double>((size_t)parts * B);
         hook_r = dalloc<double>(nu);
         hook_est = dalloc<double>(nu);
+        chunk_done = dalloc<int32_t>(MAX_B);
+        BH_CUDA(cudaMemset(chunk_done, 0, MAX_B * sizeof(int32_t)));
         if (getenv("BH_DEBUG_WARP_TIMING")) {
             dbg_v = dalloc<uint64_t>((size_t)plan_v.n_warps * 4);
             dbg_u = dalloc<uint64_t>((size_t)plan_u.n_warps * 4);
@@ -282,7 +301,7 @@ struct Engine final : EngineBase {
         cudaFree(part.cnt); cudaFree(part.np_u); cudaFree(part.np_v);
         cudaFree(part.any); cudaFree(part.sum); cudaFree(part.wsum);
         cudaFree(scratch); cudaFree(cand_key); cudaFree(cand_idx);
-        cudaFree(hook_r); cudaFree(hook_est);
+        cudaFree(hook_r); cudaFree(hook_est); cudaFree(chunk_done);
         plan_u.free_all();
         plan_v.free_all();
         for (auto e : evpool) cudaEventDestroy(e);
@@ -332,11 +351,11 @@ struct Engine final : EngineBase {
     void launch_pull(int side, const PullArgs<T> &a, cudaStream_t st) {
         const int grid = side == SIDE_V ? plan_v.grid : plan_u.grid;
         if constexpr (WIDE) {
-            if (side == SIDE_V) k_pull<B, T, SIDE_V><<<grid, PULL_THREADS, pull_smem, st>>>(a);
-            else k_pull<B, T, SIDE_U><<<grid, PULL_THREADS, pull_smem, st>>>(a);
+            if (side == SIDE_V) launch_pdl(k_pull<B, T, SIDE_V>, grid, PULL_THREADS, pull_smem, st, a);
+            else launch_pdl(k_pull<B, T, SIDE_U>, grid, PULL_THREADS, pull_smem, st, a);
         } else {
-            if (side == SIDE_V) k_pull_small<B, T, SIDE_V><<<grid, PULL_THREADS, 0, st>>>(a);
-            else k_pull_small<B, T, SIDE_U><<<grid, PULL_THREADS, 0, st>>>(a);
+            if (side == SIDE_V) launch_pdl(k_pull_small<B, T, SIDE_V>, grid, PULL_THREADS, 0, st, a);
+            else launch_pdl(k_pull_small<B, T, SIDE_U>, grid, PULL_THREADS, 0, st, a);
         }
     }
 
@@ -358,19 +377,18 @@ struct Engine final : EngineBase {
         ea.part = part;
         ea.alpha = rs.alpha;
         if (prof) BH_CUDA(cudaEventRecord(ev(e0), st));
-        k_push<B, T><<<grid_elem, ELEM_THREADS, 0, st>>>(ea);
+        launch_pdl(k_push<B, T>, grid_elem, ELEM_THREADS, 0, st, ea);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 1), st));
         launch_pull(SIDE_V, pull_args(SIDE_V, 1.0 - rs.alpha), st);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 2), st));
         launch_pull(SIDE_U, pull_args(SIDE_U, 1.0 - rs.alpha), st);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 3), st));
-        k_combine<B, T><<<grid_elem, ELEM_THREADS, 0, st>>>(ea);
+        launch_pdl(k_combine<B, T>, grid_elem, ELEM_THREADS, 0, st, ea);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 4), st));
-        k_control<<<B, CONTROL_THREADS, 0, st>>>(ca);
-        k_finalize<T><<<grid_k5, TOPK_THREADS, 0, st>>>(fa);
-        k_topk_merge<T><<<B, TOPK_THREADS, 0, st>>>(fa);
+        launch_pdl(k_control, B, CONTROL_THREADS, 0, st, ca);
+        launch_pdl(k_finalize<T>, grid_k5, TOPK_THREADS, 0, st, fa);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 5), st));
-        const int launches = 7;
+        const int launches = 6;
         count_launch(launches);
         stats.launches += launches;
         BH_CUDA(cudaGetLastError());
@@ -453,6 +471,7 @@ struct Engine final : EngineBase {
         fa.topk_idx = rs.topk_idx;
         fa.topk_score = rs.topk_score;
         fa.trace = rs.trace;
+        fa.chunk_done = chunk_done;
 
         const int poll = rs.hook ? 1 : 8;
         const bool prof = g_profiling.load() != 0;

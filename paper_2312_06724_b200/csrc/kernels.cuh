@@ -166,6 +166,7 @@ struct ElemArgs {
 // K1: push (and ledger init / power-iteration entry) for the coming round.
 template <int B, typename T>
 __global__ void __launch_bounds__(ELEM_THREADS) k_push(ElemArgs<T> a) {
+    pdl_begin();
     if (*a.active == 0) return;
     using EG = ElemGeo<B>;
     constexpr int EV = EG::EV, TPN = EG::TPN;
@@ -261,6 +262,7 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_push(ElemArgs<T> a) {
 // the exit-test reductions of the round that just ran.
 template <int B, typename T>
 __global__ void __launch_bounds__(ELEM_THREADS) k_combine(ElemArgs<T> a) {
+    pdl_begin();
     if (*a.active == 0) return;
     using EG = ElemGeo<B>;
     constexpr int EV = EG::EV, TPN = EG::TPN;
@@ -542,6 +544,7 @@ __device__ __noinline__ IVec<VEC> pull_cut(CutCtx<T> cx, int ci, int pi, int slo
 // published after the loop.
 template <int B, typename T, int SIDE>
 __global__ void __launch_bounds__(PULL_THREADS, 2) k_pull(PullArgs<T> a) {
+    pdl_begin();
     if (*a.active == 0) return;
     constexpr int VEC = RegPipe<B, T>::VEC, S = RegPipe<B, T>::S;
     const int lane = threadIdx.x & 31;
@@ -712,6 +715,7 @@ __global__ void __launch_bounds__(PULL_THREADS, 2) k_pull(PullArgs<T> a) {
 // split each row; plain loads.  Same partition, cut rows and epilogue.
 template <int B, typename T, int SIDE>
 __global__ void __launch_bounds__(PULL_THREADS) k_pull_small(PullArgs<T> a) {
+    pdl_begin();
     if (*a.active == 0) return;
     constexpr int G = B, EPW = 32 / B;
     __shared__ int32_t s_op[MAX_B];

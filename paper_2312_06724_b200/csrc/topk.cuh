@@ -181,6 +181,7 @@ struct FinalArgs {
     int32_t *topk_idx;   // [n_q][k]
     double *topk_score;  // [n_q][k]
     bh_trace *trace;     // [n_q]
+    int32_t *chunk_done; // [B] chunks finished per finishing slot (zero between rounds)
 };
 
 template <typename T>
@@ -188,66 +189,17 @@ __device__ __forceinline__ double *score_row(const FinalArgs<T> &a, int s, const
     return a.want_scores ? a.out_scores + (int64_t)f.qidx * a.n_u : a.outs + (int64_t)s * a.n_u;
 }
 
+// Merge the chunk candidates of finished slot s, sort, write top-k + trace.
 template <typename T>
-__global__ void __launch_bounds__(TOPK_THREADS) k_finalize(FinalArgs<T> a) {
-    const int n_fin = a.ctl->n_fin;
-    if (n_fin == 0) return;
-    __shared__ SelectSmem sm;
-    const int B = a.B;
-    for (int64_t p = blockIdx.x; p < (int64_t)n_fin * a.n_chunks; p += gridDim.x) {
-        const int fi = (int)(p / a.n_chunks);
-        const int c = (int)(p % a.n_chunks);
-        const int s = a.ctl->fin_slots[fi];
-        const Finish f = a.fin[s];
-        if (f.job == BH_JOB_SS_PUSH || f.job == BH_JOB_SELECTIVE) continue;
-        double *dst = score_row(a, s, f);
-        const int64_t u0 = (int64_t)c * a.chunk;
-        const int64_t u1 = imin64(a.n_u, u0 + a.chunk);
-        for (int64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
-            const double est = a.EST[u * B + s];
-            const double ws = a.ws_u[u];
-            double v;
-            if (f.job == BH_JOB_POWER) {
-                v = a.alpha * (ws * (double)a.P[u * B + s]);
-            } else {
-                v = (ws * f.inv_ws_q) * est;                                  // w_ratio * est
-                if (f.has_pi) v = v + a.alpha * (ws * (double)a.P[u * B + s]);  // + alpha acc_t
-                if (f.job == BH_JOB_BHPP) v = v + est;                         // + backward est
-            }
-            dst[u] = v;
-        }
-        if (a.k <= 0) continue;
-        __syncthreads();
-        const int64_t excl = (a.exclude && f.job == BH_JOB_BHPP) ? f.src : -1;
-        auto acc = [&](int64_t i, uint64_t &kk, int64_t &ii) -> bool {
-            ii = u0 + i;
-            kk = order_key(dst[ii]);
-            return ii != excl;
-        };
-        uint64_t *ck = a.cand_key + ((int64_t)s * a.n_chunks + c) * a.k;
-        int64_t *ci = a.cand_idx + ((int64_t)s * a.n_chunks + c) * a.k;
-        const int64_t m = block_select(u1 - u0, a.k, acc, sm, ck, ci);
-        for (int64_t i = m + threadIdx.x; i < a.k; i += blockDim.x) ci[i] = -1;
-        __syncthreads();
-    }
-}
-
-template <typename T>
-__global__ void __launch_bounds__(TOPK_THREADS) k_topk_merge(FinalArgs<T> a) {
-    const int n_fin = a.ctl->n_fin;
-    if ((int)blockIdx.x >= n_fin) return;
-    __shared__ SelectSmem sm;
-    __shared__ uint64_t skey[TOPK_MAX];
-    __shared__ int64_t sidx[TOPK_MAX];
-    const int s = a.ctl->fin_slots[blockIdx.x];
-    const Finish f = a.fin[s];
+__device__ void merge_slot(const FinalArgs<T> &a, int s, const Finish &f, SelectSmem &sm, uint64_t *skey,
+                           int64_t *sidx) {
     if (threadIdx.x == 0) a.trace[f.qidx] = f.trace;
     if (a.k <= 0 || f.job == BH_JOB_SS_PUSH || f.job == BH_JOB_SELECTIVE || !a.topk_idx) return;
     const uint64_t *ck = a.cand_key + (int64_t)s * a.n_chunks * a.k;
     const int64_t *ci = a.cand_idx + (int64_t)s * a.n_chunks * a.k;
     auto acc = [&](int64_t i, uint64_t &kk, int64_t &ii) -> bool {
-        ii = ci[i];
-        kk = ck[i];
+        ii = __ldcg(ci + i);
+        kk = __ldcg(ck + i);
         return ii >= 0;
     };
     int P = 1;
@@ -263,6 +215,68 @@ __global__ void __launch_bounds__(TOPK_THREADS) k_topk_merge(FinalArgs<T> a) {
         const bool ok = i < m;
         a.topk_idx[(int64_t)f.qidx * a.k + i] = ok ? (int32_t)sidx[i] : -1;
         if (a.topk_score) a.topk_score[(int64_t)f.qidx * a.k + i] = ok ? key_value(skey[i]) : 0.0;
+    }
+}
+
+// K5: scores + chunk top-k candidates per (finished slot, chunk); the last
+// chunk block of a slot merges (K6 folded in: no extra launch per round).
+template <typename T>
+__global__ void __launch_bounds__(TOPK_THREADS) k_finalize(FinalArgs<T> a) {
+    pdl_begin();
+    const int n_fin = a.ctl->n_fin;
+    if (n_fin == 0) return;
+    __shared__ SelectSmem sm;
+    __shared__ uint64_t skey[TOPK_MAX];
+    __shared__ int64_t sidx[TOPK_MAX];
+    __shared__ int s_last;
+    const int B = a.B;
+    for (int64_t p = blockIdx.x; p < (int64_t)n_fin * a.n_chunks; p += gridDim.x) {
+        const int fi = (int)(p / a.n_chunks);
+        const int c = (int)(p % a.n_chunks);
+        const int s = a.ctl->fin_slots[fi];
+        const Finish f = a.fin[s];
+        const bool scores = !(f.job == BH_JOB_SS_PUSH || f.job == BH_JOB_SELECTIVE);
+        if (scores) {
+            double *dst = score_row(a, s, f);
+            const int64_t u0 = (int64_t)c * a.chunk;
+            const int64_t u1 = imin64(a.n_u, u0 + a.chunk);
+            for (int64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
+                const double est = a.EST[u * B + s];
+                const double ws = a.ws_u[u];
+                double v;
+                if (f.job == BH_JOB_POWER) {
+                    v = a.alpha * (ws * (double)a.P[u * B + s]);
+                } else {
+                    v = (ws * f.inv_ws_q) * est;                                  // w_ratio * est
+                    if (f.has_pi) v = v + a.alpha * (ws * (double)a.P[u * B + s]);  // + alpha acc_t
+                    if (f.job == BH_JOB_BHPP) v = v + est;                         // + backward est
+                }
+                dst[u] = v;
+            }
+            if (a.k > 0) {
+                __syncthreads();
+                const int64_t excl = (a.exclude && f.job == BH_JOB_BHPP) ? f.src : -1;
+                auto acc = [&](int64_t i, uint64_t &kk, int64_t &ii) -> bool {
+                    ii = u0 + i;
+                    kk = order_key(dst[ii]);
+                    return ii != excl;
+                };
+                uint64_t *ck = a.cand_key + ((int64_t)s * a.n_chunks + c) * a.k;
+                int64_t *ci = a.cand_idx + ((int64_t)s * a.n_chunks + c) * a.k;
+                const int64_t m = block_select(u1 - u0, a.k, acc, sm, ck, ci);
+                for (int64_t i = m + threadIdx.x; i < a.k; i += blockDim.x) ci[i] = -1;
+            }
+        }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) s_last = atomicAdd(a.chunk_done + s, 1) == a.n_chunks - 1;
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            merge_slot(a, s, f, sm, skey, sidx);
+            if (threadIdx.x == 0) a.chunk_done[s] = 0;
+        }
+        __syncthreads();
     }
 }
 
