@@ -204,9 +204,20 @@ struct Engine final : EngineBase {
     int fin_chunk = 4096, n_chunks = 1;
     int grid_elem = 1, grid_k5 = 1;
 
-    static void pull_kernel(int side, void **fn) {
-        if constexpr (WIDE) *fn = side == SIDE_V ? (void *)k_pull<B, T, SIDE_V> : (void *)k_pull<B, T, SIDE_U>;
-        else *fn = side == SIDE_V ? (void *)k_pull_small<B, T, SIDE_V> : (void *)k_pull_small<B, T, SIDE_U>;
+    // Pull mapping per side: half-warp workers (two operand rows per warp
+    // instruction) when rows are long enough that the per-row emit is
+    // amortised, full-warp workers (cheapest emit) for short rows.
+    bool half_v = false, half_u = false;
+    static constexpr int64_t HALF_MIN_AVG_DEG = 16;
+
+    void pull_kernel(int side, void **fn) const {
+        if constexpr (WIDE) {
+            const bool half = side == SIDE_V ? half_v : half_u;
+            if (side == SIDE_V) *fn = half ? (void *)k_pull_half<B, T, SIDE_V> : (void *)k_pull<B, T, SIDE_V>;
+            else *fn = half ? (void *)k_pull_half<B, T, SIDE_U> : (void *)k_pull<B, T, SIDE_U>;
+        } else {
+            *fn = side == SIDE_V ? (void *)k_pull_small<B, T, SIDE_V> : (void *)k_pull_small<B, T, SIDE_U>;
+        }
     }
 
     explicit Engine(bh_graph *graph) : g(graph) {
@@ -231,6 +242,8 @@ struct Engine final : EngineBase {
         int sms = 148;
         BH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
         pull_smem = 0;
+        half_v = WIDE && g->n_e >= HALF_MIN_AVG_DEG * g->n_v;
+        half_u = WIDE && g->n_e >= HALF_MIN_AVG_DEG * g->n_u;
         for (int side = 0; side < 2; side++) {
             void *fn;
             pull_kernel(side, &fn);
@@ -246,13 +259,14 @@ struct Engine final : EngineBase {
             const int64_t want = (g->n_e + 2 * sd.n_rows) / 64 / PULL_WARPS + 1;
             grid = std::max<int64_t>(1, std::min(grid, want));
             pl.grid = (int)grid;
-            build_plan(sd, g->n_e, (int)grid * PULL_WARPS, pl);
+            const bool half = side == SIDE_V ? half_v : half_u;
+            build_plan(sd, g->n_e, (int)grid * PULL_WARPS * (half ? 2 : 1), pl);
         }
         grid_elem = grid1d(nu * (B / ElemGeo<B>::EV), ELEM_THREADS, 4 * sms);
         n_chunks = (int)((nu + fin_chunk - 1) / fin_chunk);
         grid_k5 = (int)std::min<int64_t>((int64_t)n_chunks * std::min(B, 8), 8 * sms);
         part.rows_k1 = grid_elem;
-        part.rows_k2 = plan_v.n_warps;
+        part.rows_k2 = half_v ? (plan_v.n_warps + 1) / 2 : plan_v.n_warps;
         part.rows_k3 = grid_elem;
         part.cnt = dalloc<int64_t>((size_t)grid_elem * B);
         part.np_u = dalloc<int64_t>((size_t)grid_elem * B);
@@ -351,8 +365,14 @@ struct Engine final : EngineBase {
     void launch_pull(int side, const PullArgs<T> &a, cudaStream_t st) {
         const int grid = side == SIDE_V ? plan_v.grid : plan_u.grid;
         if constexpr (WIDE) {
-            if (side == SIDE_V) launch_pdl(k_pull<B, T, SIDE_V>, grid, PULL_THREADS, pull_smem, st, a);
-            else launch_pdl(k_pull<B, T, SIDE_U>, grid, PULL_THREADS, pull_smem, st, a);
+            const bool half = side == SIDE_V ? half_v : half_u;
+            if (side == SIDE_V) {
+                if (half) launch_pdl(k_pull_half<B, T, SIDE_V>, grid, PULL_THREADS, pull_smem, st, a);
+                else launch_pdl(k_pull<B, T, SIDE_V>, grid, PULL_THREADS, pull_smem, st, a);
+            } else {
+                if (half) launch_pdl(k_pull_half<B, T, SIDE_U>, grid, PULL_THREADS, pull_smem, st, a);
+                else launch_pdl(k_pull<B, T, SIDE_U>, grid, PULL_THREADS, pull_smem, st, a);
+            }
         } else {
             if (side == SIDE_V) launch_pdl(k_pull_small<B, T, SIDE_V>, grid, PULL_THREADS, 0, st, a);
             else launch_pdl(k_pull_small<B, T, SIDE_U>, grid, PULL_THREADS, 0, st, a);

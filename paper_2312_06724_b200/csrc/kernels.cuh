@@ -64,6 +64,18 @@ struct VecIO<float, 4> {
     }
 };
 template <>
+struct VecIO<float, 8> {
+    static __device__ __forceinline__ void ld(const float *p, float (&v)[8]) {
+        const float4 a = *reinterpret_cast<const float4 *>(p);
+        const float4 b = *(reinterpret_cast<const float4 *>(p) + 1);
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    }
+    static __device__ __forceinline__ void st(float *p, const float (&v)[8]) {
+        reinterpret_cast<float4 *>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+        reinterpret_cast<float4 *>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+    }
+};
+template <>
 struct VecIO<double, 1> {
     static __device__ __forceinline__ void ld(const double *p, double (&v)[1]) { v[0] = *p; }
     static __device__ __forceinline__ void st(double *p, const double (&v)[1]) { *p = v[0]; }
@@ -88,6 +100,22 @@ struct VecIO<double, 4> {
     static __device__ __forceinline__ void st(double *p, const double (&v)[4]) {
         reinterpret_cast<double2 *>(p)[0] = make_double2(v[0], v[1]);
         reinterpret_cast<double2 *>(p)[1] = make_double2(v[2], v[3]);
+    }
+};
+
+template <>
+struct VecIO<double, 8> {
+    static __device__ __forceinline__ void ld(const double *p, double (&v)[8]) {
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const double2 t = *(reinterpret_cast<const double2 *>(p) + k);
+            v[2 * k] = t.x;
+            v[2 * k + 1] = t.y;
+        }
+    }
+    static __device__ __forceinline__ void st(double *p, const double (&v)[8]) {
+#pragma unroll
+        for (int k = 0; k < 4; k++) reinterpret_cast<double2 *>(p)[k] = make_double2(v[2 * k], v[2 * k + 1]);
     }
 };
 
@@ -708,6 +736,249 @@ __global__ void __launch_bounds__(PULL_THREADS, 2) k_pull(PullArgs<T> a) {
         if (gw < a.n_warps)
 #pragma unroll
             for (int v = 0; v < VEC; v++) a.np_v[(int64_t)(slot0 + v) * a.n_warps + gw] = (int64_t)np[v] + np_cut[v];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Half-warp workers (B >= 32): each 16-lane half of a warp is an independent
+// worker with its own cost-balanced edge range; a lane owns VEC = B/16 slots
+// (16 B of fp32 at B = 64), so one warp instruction gathers two operand rows.
+// Same pipeline as k_pull: S rows in flight per worker in registers, zero-
+// padded (col, val) windows, width-16 shuffles with immediate lanes, compact
+// per-row emit, cut rows published after the loop.
+template <int B, typename T>
+struct HalfPipe {
+    static constexpr int VEC = B / 16;
+    static constexpr int LANE_BYTES = VEC * (int)sizeof(T);
+    static constexpr int S = LANE_BYTES <= 8 ? 16 : (LANE_BYTES <= 16 ? 8 : (LANE_BYTES <= 32 ? 4 : 2));
+};
+
+template <int B, typename T, int VEC>
+__device__ __noinline__ IVec<VEC> pull_cut_half(CutCtx<T> cx, int ci, int pi, int slot0, uint32_t cmask,
+                                                DVec<VEC> acc, uint32_t hmask) {
+    const int q = threadIdx.x & 15;
+    IVec<VEC> inc;
+#pragma unroll
+    for (int v = 0; v < VEC; v++) inc.v[v] = 0;
+#pragma unroll
+    for (int v = 0; v < VEC; v++) cx.scratch[(int64_t)pi * B + slot0 + v] = acc.v[v];
+    __threadfence();
+    __syncwarp(hmask);
+    const CutRow cr = cx.cuts[ci];
+    int last = 0;
+    if (q == 0) last = atomicAdd(cx.cut_count + ci, 1) == cr.n_parts - 1;
+    last = __shfl_sync(hmask, last, 0, 16);
+    if (!last) return inc;
+    __threadfence();
+    double tot[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; v++) tot[v] = 0.0;
+    int p = 0;
+    for (; p + 4 <= cr.n_parts; p += 4) {
+        double qv[4][VEC];
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+#pragma unroll
+            for (int v = 0; v < VEC; v++) qv[k][v] = __ldcg(cx.scratch + (int64_t)(cr.first_part + p + k) * B + slot0 + v);
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+#pragma unroll
+            for (int v = 0; v < VEC; v++) tot[v] += qv[k][v];
+    }
+    for (; p < cr.n_parts; p++)
+#pragma unroll
+        for (int v = 0; v < VEC; v++) tot[v] += __ldcg(cx.scratch + (int64_t)(cr.first_part + p) * B + slot0 + v);
+    const int64_t deg = __ldg(cx.indptr + cr.row + 1) - __ldg(cx.indptr + cr.row);
+    T out[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; v++) {
+        out[v] = (T)(cx.scale * tot[v]);
+        if (((cmask >> v) & 1u) && (double)out[v] > 0.0) inc.v[v] = deg;
+    }
+    VecIO<T, VEC>::st(cx.Y + (int64_t)cr.row * B + slot0, out);
+    if (q == 0) cx.cut_count[ci] = 0;
+    return inc;
+}
+
+template <int B, typename T, int SIDE>
+__global__ void __launch_bounds__(PULL_THREADS, 2) k_pull_half(PullArgs<T> a) {
+    pdl_begin();
+    if (*a.active == 0) return;
+    constexpr int VEC = HalfPipe<B, T>::VEC, S = HalfPipe<B, T>::S;
+    const int lane = threadIdx.x & 31;
+    const int h = lane >> 4, q = lane & 15;
+    const uint32_t hmask = h ? 0xffff0000u : 0x0000ffffu;
+    const int warp = threadIdx.x >> 5;
+    const int gw = blockIdx.x * PULL_WARPS + warp;
+    const int wid = gw * 2 + h;  // worker
+    const int slot0 = q * VEC;
+    uint32_t cmask = 0;
+    if constexpr (SIDE == SIDE_V) {
+#pragma unroll
+        for (int v = 0; v < VEC; v++) cmask |= (op_is_push(a.slots[slot0 + v].op) ? 1u : 0u) << v;
+    }
+    const double scale = SIDE == SIDE_V ? a.one_minus_alpha : 1.0;
+    int32_t np[VEC];
+    int64_t np_cut[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; v++) {
+        np[v] = 0;
+        np_cut[v] = 0;
+    }
+    const uint64_t t_start = a.dbg ? gtimer() : 0;
+    const int n_workers = a.n_warps;  // work entries (two per warp)
+    WarpWork wk;
+    wk.e0 = wk.e1 = 0;
+    wk.r0 = 0;
+    wk.cut0 = wk.cut1 = wk.part0 = wk.part1 = -1;
+    if (wid < n_workers) wk = a.work[wid];
+    const int64_t e0 = wk.e0;
+    const int n = (int)(wk.e1 - e0);
+    const int n_max = max(n, __shfl_xor_sync(0xffffffffu, n, 16));
+    if (n_max > 0) {
+        const int32_t *cols = a.indices + e0;
+        const T *vals = a.vals + e0;
+        const T *X = a.X + slot0;
+        T *Y0 = a.Y + (int64_t)wk.r0 * B + slot0;
+        const int64_t *rp = a.indptr + wk.r0;
+        const int64_t nrow_left = a.n_rows - wk.r0;
+        const int cutA = wk.cut0 >= 0 ? 0 : -1;
+        const int cutB = wk.cut1 >= 0 ? (int)(a.cuts[wk.cut1].row - wk.r0) : -1;
+        auto col_at = [&](int o) { return o < n ? __ldg(cols + o) : 0; };
+        auto val_at = [&](int o) { return o < n ? __ldg(vals + o) : (T)0; };
+        auto rend_at = [&](int i) {
+            if (n <= 0) return 0;
+            const int64_t r = i + 1 <= nrow_left ? __ldg(rp + i + 1) : __ldg(rp + nrow_left);
+            return (int)imin64(r - e0, (int64_t)n);
+        };
+        T xs[S][VEC];
+        T wsv[S];
+        {
+            const int c = col_at(q);
+            const T w = val_at(q);
+#pragma unroll
+            for (int t = 0; t < S; t++) {
+                const int ct = __shfl_sync(0xffffffffu, c, t, 16);
+                wsv[t] = __shfl_sync(0xffffffffu, w, t, 16);
+                ldg_vec<T, VEC>(X + (int64_t)ct * B, xs[t]);
+            }
+        }
+        int cw = col_at(S + q), cw1 = col_at(2 * S + q);
+        T vw = val_at(S + q), vw1 = val_at(2 * S + q);
+        int rw = 0;
+        int re0 = rend_at(q), re1 = rend_at(16 + q);
+        int lr = 0;
+        int rstart = n > 0 ? (int)(__ldg(rp) - e0) : 0;
+        int rend = __shfl_sync(0xffffffffu, re0, 0, 16);
+        if (n <= 0) rend = 1 << 30;  // idle worker: never emits
+        double acc[VEC], accA[VEC], accB[VEC];
+        T accs[VEC];
+#pragma unroll
+        for (int v = 0; v < VEC; v++) {
+            acc[v] = accA[v] = accB[v] = 0.0;
+            accs[v] = (T)0;
+        }
+        for (int base = 0; base < n_max; base += S) {
+            int d = rend - base - 1;
+#pragma unroll
+            for (int t = 0; t < S; t++) {
+                if constexpr (sizeof(T) == 8) {
+#pragma unroll
+                    for (int v = 0; v < VEC; v++) acc[v] = fma((double)wsv[t], (double)xs[t][v], acc[v]);
+                } else {
+#pragma unroll
+                    for (int v = 0; v < VEC; v++) accs[v] = fmaf(wsv[t], xs[t][v], accs[v]);
+                }
+                if (d == t) {  // ---- row emit (uniform within the half-warp)
+                    if constexpr (sizeof(T) == 4) {
+#pragma unroll
+                        for (int v = 0; v < VEC; v++) {
+                            acc[v] += (double)accs[v];
+                            accs[v] = (T)0;
+                        }
+                    }
+                    if (lr == cutA) {
+#pragma unroll
+                        for (int v = 0; v < VEC; v++) accA[v] = acc[v];
+                    } else if (lr == cutB) {
+#pragma unroll
+                        for (int v = 0; v < VEC; v++) accB[v] = acc[v];
+                    } else {
+                        T out[VEC];
+#pragma unroll
+                        for (int v = 0; v < VEC; v++) {
+                            out[v] = (T)(scale * acc[v]);
+                            if constexpr (SIDE == SIDE_V)
+                                np[v] += (((cmask >> v) & 1u) && out[v] > (T)0) ? rend - rstart : 0;
+                        }
+                        VecIO<T, VEC>::st(Y0 + (int64_t)lr * B, out);
+                    }
+#pragma unroll
+                    for (int v = 0; v < VEC; v++) acc[v] = 0.0;
+                    lr++;
+                    rstart = rend;
+                    if (lr - rw >= 16) {
+                        rw += 16;
+                        re0 = re1;
+                        re1 = rend_at(rw + 16 + q);
+                    }
+                    rend = __shfl_sync(hmask, re0, lr - rw, 16);
+                    d = rend - base - 1;
+                }
+                const int ct = __shfl_sync(0xffffffffu, cw, t, 16);
+                wsv[t] = __shfl_sync(0xffffffffu, vw, t, 16);
+                ldg_vec<T, VEC>(X + (int64_t)ct * B, xs[t]);
+            }
+            if constexpr (sizeof(T) == 4) {
+#pragma unroll
+                for (int v = 0; v < VEC; v++) {
+                    acc[v] += (double)accs[v];
+                    accs[v] = (T)0;
+                }
+            }
+            cw = cw1;
+            vw = vw1;
+            cw1 = col_at(base + 3 * S + q);
+            vw1 = val_at(base + 3 * S + q);
+        }
+        const CutCtx<T> cx{a.scratch, a.cut_count, a.cuts, a.Y, a.indptr, scale};
+        for (int hh = 0; hh < 2; hh++) {
+            if (h == hh) {
+                if (cutA >= 0) {
+                    DVec<VEC> av;
+#pragma unroll
+                    for (int v = 0; v < VEC; v++) av.v[v] = accA[v];
+                    const IVec<VEC> inc = pull_cut_half<B, T, VEC>(cx, wk.cut0, wk.part0, slot0, cmask, av, hmask);
+#pragma unroll
+                    for (int v = 0; v < VEC; v++) np_cut[v] += inc.v[v];
+                }
+                if (cutB >= 0) {
+                    DVec<VEC> av;
+#pragma unroll
+                    for (int v = 0; v < VEC; v++) av.v[v] = accB[v];
+                    const IVec<VEC> inc = pull_cut_half<B, T, VEC>(cx, wk.cut1, wk.part1, slot0, cmask, av, hmask);
+#pragma unroll
+                    for (int v = 0; v < VEC; v++) np_cut[v] += inc.v[v];
+                }
+            }
+            __syncwarp();
+        }
+    }
+    if (a.dbg && lane == 0 && gw * 2 < n_workers) {
+        a.dbg[gw * 4 + 0] = t_start;
+        a.dbg[gw * 4 + 1] = gtimer();
+        a.dbg[gw * 4 + 2] = (uint64_t)n;
+        a.dbg[gw * 4 + 3] = 0;
+    }
+    if constexpr (SIDE == SIDE_V) {
+        // both halves cover the same slots: combine, half 0 writes the warp's row
+        const int n_rows_out = (n_workers + 1) / 2;
+#pragma unroll
+        for (int v = 0; v < VEC; v++) {
+            int64_t t = (int64_t)np[v] + np_cut[v];
+            t += __shfl_xor_sync(0xffffffffu, t, 16);
+            if (h == 0 && gw < n_rows_out) a.np_v[(int64_t)(slot0 + v) * n_rows_out + gw] = t;
+        }
     }
 }
 
