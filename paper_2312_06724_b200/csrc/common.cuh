@@ -111,7 +111,7 @@ struct Slot {
     int32_t src;       // source / target U index
     int32_t phase;     // Phase
     int32_t term_b, term_f;
-    int32_t all_full;  // every forward round so far pushed all of U
+    int32_t pad0;
     int32_t tie_checks, tie_skip, tie_broke;
     int32_t pi_t, pi_done;
     int32_t last_phase;   // BH_PHASE_* of the last executed push round (-1 none)
@@ -121,6 +121,8 @@ struct Slot {
     int64_t sel_b, seq_b, sel_f;
     int64_t last_rounds;  // counter reported to round_hook
     double gamma;
+    double mass_prev;       // weighted residue mass at the start of the current forward round
+    double defsum;          // sum_j log1p(alpha f_j / (1 - alpha)), f_j = left-behind mass fraction
     double ws_q, inv_ws_q;  // ws(source), 1 / ws(source)
     double ysc;             // y0 = residue * ysc in power iteration
     double theta_c;         // eps_f / lam
@@ -138,6 +140,7 @@ struct Finish {
 struct Partials {
     int64_t *cnt;    // [rows_k1][B] |A| (K1 push)
     int64_t *np_u;   // [rows_k1][B] sum deg(A) (K1 push)
+    double *lmass;   // [rows_k1][B] weighted residue left below threshold (K1, forward)
     int64_t *np_v;   // [rows_k2][B] sum deg over r_v > 0 (K2, one row per warp)
     int32_t *any;    // [rows_k3][B] any(r > threshold) (K1a combine)
     double *sum;     // [rows_k3][B] sum r (K1a)

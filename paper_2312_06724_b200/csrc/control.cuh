@@ -53,7 +53,6 @@ __device__ void slot_start(Slot &sl, const ControlArgs &a, int32_t q) {
         case BH_JOB_PI_PUSH:
             sl.n_p = a.init_np;
             sl.n_p_entry = a.init_np;
-            sl.all_full = 1;
             sl.phase = PH_FWD;
             sl.op = OP_MEASURE;  // gamma of the seed ledger first, then forward rounds
             break;
@@ -106,6 +105,7 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
     __shared__ double r_sum[CONTROL_THREADS];
     __shared__ double r_wsum[CONTROL_THREADS];
     __shared__ int32_t r_any[CONTROL_THREADS];
+    __shared__ double r_left[CONTROL_THREADS];
     __shared__ int32_t s_last;
     const int tid = threadIdx.x;
     const int s = blockIdx.x;
@@ -119,13 +119,16 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
         int64_t cnt = 0, np = 0;
         double sum = 0.0, wsum = 0.0;
         int32_t any = 0;
+        double left = 0.0;
         if (!a.first) {
             // partial rows are stored slot-major: [slot][row]
             const int64_t *pc = a.part.cnt + (int64_t)s * a.part.rows_k1;
             const int64_t *pn = a.part.np_u + (int64_t)s * a.part.rows_k1;
+            const double *pl = a.part.lmass + (int64_t)s * a.part.rows_k1;
             for (int r = tid; r < a.part.rows_k1; r += CONTROL_THREADS) {
                 cnt += pc[r];
                 np += pn[r];
+                left += pl[r];
             }
             const int64_t *pv = a.part.np_v + (int64_t)s * a.part.rows_k2;
             for (int r = tid; r < a.part.rows_k2; r += CONTROL_THREADS) np += pv[r];
@@ -143,6 +146,7 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
         r_sum[tid] = sum;
         r_wsum[tid] = wsum;
         r_any[tid] = any;
+        r_left[tid] = left;
     }
     __syncthreads();
     for (int off = CONTROL_THREADS / 2; off > 0; off >>= 1) {  // fixed-shape tree
@@ -152,6 +156,7 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
             r_sum[tid] += r_sum[tid + off];
             r_wsum[tid] += r_wsum[tid + off];
             r_any[tid] |= r_any[tid + off];
+            r_left[tid] += r_left[tid + off];
         }
         __syncthreads();
     }
@@ -164,6 +169,8 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
         const double sum = r_sum[0], wsum = r_wsum[0];
         if (op == OP_MEASURE) {  // pi_push entry: gamma of the uploaded ledger (push_engine.py:222)
             sl.gamma = wsum;
+            sl.mass_prev = wsum;
+            sl.defsum = 0.0;
             sl.op = OP_FENTRY;
         } else if (op_is_push(op)) {
             sl.push_seq++;
@@ -207,7 +214,16 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
                 sl.sel_f += worked;
                 sl.last_phase = BH_PHASE_FORWARD;
                 sl.last_rounds = sl.sel_f;
-                if (cnt != a.n_u) sl.all_full = 0;
+                // Eq. 12 in exact (telescoped) form.  By detailed balance a forward
+                // round maps the weighted residue mass m = P + L (P pushed, L left
+                // below threshold) to (1-alpha) P + L, so
+                //   ln(gamma / wmass_k) = sum_j [ln(1/(1-alpha)) - log1p(alpha f_j / (1-alpha))],
+                // f_j = L_j / m_{j-1}.  The budget test n_p - n_0 >= 2|E| ln(gamma/wmass)/ln(1/(1-alpha))
+                // becomes (2|E| k - used) <= 2|E| sum_j log1p(...) / ln(1/(1-alpha)): a comparison of
+                // two small quantities that fp32 residues resolve as well as fp64 ones.
+                const double fj = sl.mass_prev > 0.0 ? r_left[0] / sl.mass_prev : 0.0;
+                if (fj > 0.0) sl.defsum += log1p(a.alpha * fj / (1.0 - a.alpha));
+                sl.mass_prev = wsum;
                 if (!any) {
                     sl.term_f = BH_TERM_THRESHOLD;
                     sl.pi_t = 0;
@@ -220,16 +236,22 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
                     slot_finish(sl, a.fin[s], false);
                 } else {
                     bool brk;
-                    if (sl.all_full) {
-                        // Exact tie: n_p - n_p_entry == 2|E| k == budget in exact
-                        // arithmetic.  Break, unless the
-                        // caller asked to replay a reference run that continued.
-                        sl.tie_checks++;
-                        brk = sl.tie_checks > sl.tie_skip;
-                        if (brk) sl.tie_broke = 1;
+                    const int64_t used = sl.n_p - sl.n_p_entry;
+                    const int64_t limit = (int64_t)a.budget_scale * sl.sel_f;  // 2|E| k
+                    if (sl.defsum == 0.0) {
+                        // Every positive residue was pushed in every forward round: the
+                        // budget is exactly 2|E| k.  Equality (A = U in every round) is the
+                        // exact tie of SURVEY.md sec. 0 fact 11, which the reference resolves
+                        // by rounding: break, unless replaying a reference run (tie_skip).
+                        if (used >= limit) {
+                            sl.tie_checks++;
+                            brk = sl.tie_checks > sl.tie_skip;
+                            if (brk) sl.tie_broke = 1;
+                        } else {
+                            brk = false;
+                        }
                     } else {
-                        const double budget = a.budget_scale * (log(sl.gamma / wsum) / a.log_decay);
-                        brk = (double)(sl.n_p - sl.n_p_entry) >= budget;
+                        brk = (double)(limit - used) <= a.budget_scale * sl.defsum / a.log_decay;
                     }
                     if (brk) {
                         sl.term_f = BH_TERM_BUDGET;
@@ -251,9 +273,10 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
                     sl.phase = PH_FWD;
                     sl.op = OP_FENTRY;
                     sl.gamma = wsum;  // gamma at PI-Push entry (push_engine.py:222)
+                    sl.mass_prev = wsum;
+                    sl.defsum = 0.0;
                     sl.n_p_entry = sl.n_p;
-                    sl.all_full = 1;
-                    sl.tie_checks = 0;
+                            sl.tie_checks = 0;
                 }
             }
         } else if (op == OP_PIENTRY0) {

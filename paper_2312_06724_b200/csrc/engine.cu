@@ -270,6 +270,8 @@ struct Engine final : EngineBase {
         part.rows_k3 = grid_elem;
         part.cnt = dalloc<int64_t>((size_t)grid_elem * B);
         part.np_u = dalloc<int64_t>((size_t)grid_elem * B);
+        part.lmass = dalloc<double>((size_t)grid_elem * B);
+        BH_CUDA(cudaMemset(part.lmass, 0, (size_t)grid_elem * B * sizeof(double)));
         part.np_v = dalloc<int64_t>((size_t)plan_v.n_warps * B);
         part.any = dalloc<int32_t>((size_t)grid_elem * B);
         part.sum = dalloc<double>((size_t)grid_elem * B);
@@ -312,7 +314,7 @@ struct Engine final : EngineBase {
     ~Engine() override {
         cudaFree(R); cudaFree(P); cudaFree(Y); cudaFree(XV); cudaFree(EST); cudaFree(OUTS);
         cudaFree(slots); cudaFree(fins); cudaFree(ctl); cudaFreeHost(h_ctl);
-        cudaFree(part.cnt); cudaFree(part.np_u); cudaFree(part.np_v);
+        cudaFree(part.cnt); cudaFree(part.np_u); cudaFree(part.np_v); cudaFree(part.lmass);
         cudaFree(part.any); cudaFree(part.sum); cudaFree(part.wsum);
         cudaFree(scratch); cudaFree(cand_key); cudaFree(cand_idx);
         cudaFree(hook_r); cudaFree(hook_est); cudaFree(chunk_done);

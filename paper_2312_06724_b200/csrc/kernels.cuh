@@ -201,6 +201,7 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_push(ElemArgs<T> a) {
     __shared__ SlotSmem sm;
     __shared__ int64_t red_cnt[ELEM_THREADS * EV];
     __shared__ int64_t red_np[ELEM_THREADS * EV];
+    __shared__ double red_left[ELEM_THREADS * EV];
     load_slot_smem<B>(sm, a.slots);
     __syncthreads();
     const int j0 = (threadIdx.x % TPN) * EV;  // first slot of this thread (fixed: blockDim % TPN == 0)
@@ -212,8 +213,12 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_push(ElemArgs<T> a) {
         any_work |= op_is_push(op[v]) || op[v] == OP_PIENTRY || op[v] == OP_PIENTRY0;
     }
     int64_t cnt[EV], npu[EV];
+    double left[EV];
 #pragma unroll
-    for (int v = 0; v < EV; v++) cnt[v] = npu[v] = 0;
+    for (int v = 0; v < EV; v++) {
+        cnt[v] = npu[v] = 0;
+        left[v] = 0.0;
+    }
     if (any_work) {
         const int64_t total = a.n_u * TPN;
         for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
@@ -259,6 +264,8 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_push(ElemArgs<T> a) {
                         rv[v] = (T)r;
                         a.EST[i + v] = 0.0;
                         wrote_r = true;
+                    } else if (op_is_fwd(o)) {
+                        left[v] += (a.ws_u[u] * sm.iwsq[s]) * r;  // w_ratio r left behind this round
                     }
                 } else {
                     pv[v] = a.P[i + v];  // keep (power-iteration iterate / idle)
@@ -272,17 +279,21 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_push(ElemArgs<T> a) {
     for (int v = 0; v < EV; v++) {
         red_cnt[threadIdx.x * EV + v] = cnt[v];
         red_np[threadIdx.x * EV + v] = npu[v];
+        red_left[threadIdx.x * EV + v] = left[v];
     }
     __syncthreads();
     // slot s is owned by the threads t with t % TPN == s / EV
     for (int s = threadIdx.x; s < B; s += blockDim.x) {
         int64_t c = 0, n = 0;
+        double l = 0.0;
         for (int t = s / EV; t < ELEM_THREADS; t += TPN) {
             c += red_cnt[t * EV + s % EV];
             n += red_np[t * EV + s % EV];
+            l += red_left[t * EV + s % EV];
         }
         a.part.cnt[(int64_t)s * gridDim.x + blockIdx.x] = c;
         a.part.np_u[(int64_t)s * gridDim.x + blockIdx.x] = n;
+        a.part.lmass[(int64_t)s * gridDim.x + blockIdx.x] = l;
     }
 }
 
