@@ -27,6 +27,9 @@ struct ControlArgs {
     int64_t init_np;      // BH_JOB_PI_PUSH seed ledger n_p
     int32_t first;        // 1: no round ran yet, only assign queries
     int32_t B;
+    int32_t use_cond;     // running inside a CUDA-graph WHILE node: set its condition
+    int32_t max_rounds;   // safety stop
+    cudaGraphConditionalHandle cond;
 };
 
 __device__ __forceinline__ int32_t required_iterations_dev(double alpha, double eps_f, double mass) {
@@ -112,7 +115,10 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
     const int B = a.B;
     Control *ctl = a.ctl;
     if (ctl->active == 0 && !a.first) {
-        if (s == 0 && tid == 0) ctl->n_fin = 0;
+        if (s == 0 && tid == 0) {
+            ctl->n_fin = 0;
+            if (a.use_cond) cudaGraphSetConditional(a.cond, 0);
+        }
         return;
     }
     {
@@ -344,9 +350,14 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
         for (int i = 0; i < B; i++) nfree += f_free[i];
         ctl->next_q = min(n_q, next0 + nfree);
         ctl->n_fin = s_last;
+        if (!a.first) ctl->rounds_active++;
+        if (ctl->rounds_active > a.max_rounds) {  // runaway guard (never expected)
+            busy = 0;
+            ctl->error = 1;
+        }
         ctl->active = busy;
         ctl->arrive = 0;
-        if (!a.first) ctl->rounds_active++;
+        if (a.use_cond) cudaGraphSetConditional(a.cond, busy ? 1u : 0u);
         __threadfence();
     }
 }

@@ -200,6 +200,11 @@ struct Engine final : EngineBase {
     std::vector<cudaEvent_t> evpool;
     SidePlan plan_v, plan_u;
     uint64_t *dbg_v = nullptr, *dbg_u = nullptr;  // BH_DEBUG_WARP_TIMING
+    // one batch = one CUDA graph: a WHILE node around one round, condition set by K4
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t graph_exec = nullptr;
+    cudaStream_t cap_stream = nullptr;
+    std::vector<unsigned char> graph_key;
     size_t pull_smem = 0;
     int fin_chunk = 4096, n_chunks = 1;
     int grid_elem = 1, grid_k5 = 1;
@@ -321,6 +326,9 @@ struct Engine final : EngineBase {
         plan_u.free_all();
         plan_v.free_all();
         for (auto e : evpool) cudaEventDestroy(e);
+        if (graph_exec) cudaGraphExecDestroy(graph_exec);
+        if (graph) cudaGraphDestroy(graph);
+        if (cap_stream) cudaStreamDestroy(cap_stream);
     }
 
     cudaEvent_t ev(size_t i) {
@@ -432,6 +440,46 @@ struct Engine final : EngineBase {
         stats.profiled = 1;
     }
 
+    // (Re)build the batch graph when the round's kernel arguments change.
+    void ensure_graph(const RunSpec &rs, ControlArgs ca, const FinalArgs<T> &fa) {
+        std::vector<unsigned char> key(sizeof(RunSpec) + sizeof(ControlArgs) + sizeof(FinalArgs<T>));
+        RunSpec rk = rs;
+        rk.hook = nullptr;
+        rk.hook_user = nullptr;
+        std::memcpy(key.data(), &rk, sizeof(RunSpec));
+        ca.cond = 0;
+        std::memcpy(key.data() + sizeof(RunSpec), &ca, sizeof(ControlArgs));
+        std::memcpy(key.data() + sizeof(RunSpec) + sizeof(ControlArgs), &fa, sizeof(FinalArgs<T>));
+        if (graph_exec && key == graph_key) return;
+        if (graph_exec) cudaGraphExecDestroy(graph_exec);
+        if (graph) cudaGraphDestroy(graph);
+        graph_exec = nullptr;
+        graph = nullptr;
+        if (!cap_stream) BH_CUDA(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
+        BH_CUDA(cudaGraphCreate(&graph, 0));
+        cudaGraphConditionalHandle h;
+        BH_CUDA(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault));
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t node;
+        BH_CUDA(cudaGraphAddNode(&node, graph, nullptr, 0, &cp));
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        ca.use_cond = 1;
+        ca.cond = h;
+        BH_CUDA(cudaStreamBeginCaptureToGraph(cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        const int64_t launches0 = stats.launches;
+        launch_round(rs, ca, fa, cap_stream, 0, false);
+        stats.launches = launches0;
+        count_launch(-6);  // captured, not launched
+        cudaGraph_t captured;
+        BH_CUDA(cudaStreamEndCapture(cap_stream, &captured));
+        BH_CUDA(cudaGraphInstantiate(&graph_exec, graph, 0));
+        graph_key = key;
+    }
+
     void run(const RunSpec &rs, cudaStream_t st) override {
         if (rs.k > TOPK_MAX) throw InvalidArg("k exceeds the device top-k limit (1024) of bh_query_batch");
         if (rs.k > 0) ensure_cand(rs.k);
@@ -500,6 +548,18 @@ struct Engine final : EngineBase {
         stats = bh_run_stats{};
         stats.slots = B;
         stats.launches = 1;
+        ca.max_rounds = 100000000;
+        if (!rs.hook && !prof && !dbg_v && !getenv("BH_NO_GRAPH")) {
+            ensure_graph(rs, ca, fa);
+            BH_CUDA(cudaGraphLaunch(graph_exec, st));
+            BH_CUDA(cudaMemcpyAsync(h_ctl, ctl, sizeof(Control), cudaMemcpyDeviceToHost, st));
+            BH_CUDA(cudaStreamSynchronize(st));
+            if (h_ctl->error) throw CudaError("query batch did not terminate");
+            stats.rounds = h_ctl->rounds_active;
+            stats.launches += 6 * (int64_t)h_ctl->rounds_active;
+            count_launch((int)(6 * h_ctl->rounds_active));
+            return;
+        }
         int32_t last_seq = 0;
         std::vector<double> hr, he;
         const int64_t max_rounds = 100000000;

@@ -891,6 +891,13 @@ __global__ void __launch_bounds__(PULL_THREADS, 2) k_pull_half(PullArgs<T> a) {
         }
         for (int base = 0; base < n_max; base += S) {
             int d = rend - base - 1;
+            int cvec[S];
+            T wvec[S];
+#pragma unroll
+            for (int t = 0; t < S; t++) {
+                cvec[t] = __shfl_sync(0xffffffffu, cw, t, 16);
+                wvec[t] = __shfl_sync(0xffffffffu, vw, t, 16);
+            }
 #pragma unroll
             for (int t = 0; t < S; t++) {
                 if constexpr (sizeof(T) == 8) {
@@ -936,9 +943,8 @@ __global__ void __launch_bounds__(PULL_THREADS, 2) k_pull_half(PullArgs<T> a) {
                     rend = __shfl_sync(hmask, re0, lr - rw, 16);
                     d = rend - base - 1;
                 }
-                const int ct = __shfl_sync(0xffffffffu, cw, t, 16);
-                wsv[t] = __shfl_sync(0xffffffffu, vw, t, 16);
-                ldg_vec<T, VEC>(X + (int64_t)ct * B, xs[t]);
+                wsv[t] = wvec[t];
+                ldg_vec<T, VEC>(X + (int64_t)cvec[t] * B, xs[t]);
             }
             if constexpr (sizeof(T) == 4) {
 #pragma unroll
