@@ -442,14 +442,18 @@ struct Engine final : EngineBase {
 
     // (Re)build the batch graph when the round's kernel arguments change.
     void ensure_graph(const RunSpec &rs, ControlArgs ca, const FinalArgs<T> &fa) {
-        std::vector<unsigned char> key(sizeof(RunSpec) + sizeof(ControlArgs) + sizeof(FinalArgs<T>));
-        RunSpec rk = rs;
-        rk.hook = nullptr;
-        rk.hook_user = nullptr;
-        std::memcpy(key.data(), &rk, sizeof(RunSpec));
-        ca.cond = 0;
-        std::memcpy(key.data() + sizeof(RunSpec), &ca, sizeof(ControlArgs));
-        std::memcpy(key.data() + sizeof(RunSpec) + sizeof(ControlArgs), &fa, sizeof(FinalArgs<T>));
+        // explicit field-wise key (struct padding is not part of it)
+        std::vector<unsigned char> key;
+        auto put = [&key](const auto &v) {
+            const unsigned char *p = reinterpret_cast<const unsigned char *>(&v);
+            key.insert(key.end(), p, p + sizeof(v));
+        };
+        put(rs.job); put(rs.n_q); put(rs.sources); put(rs.tie); put(rs.alpha); put(rs.lam); put(rs.eps_b);
+        put(rs.eps_f); put(rs.power_t); put(rs.init_np); put(rs.x0); put(rs.ledger_r); put(rs.ledger_est);
+        put(rs.k); put(rs.exclude); put(rs.want_scores); put(rs.topk_idx); put(rs.topk_score); put(rs.trace);
+        put(rs.scores);
+        put(ca.budget_scale); put(ca.log_decay); put(ca.max_rounds); put(ca.sources); put(ca.tie_skip);
+        put(fa.cand_key); put(fa.cand_idx); put(fa.out_scores); put(fa.chunk_done);
         if (graph_exec && key == graph_key) return;
         if (graph_exec) cudaGraphExecDestroy(graph_exec);
         if (graph) cudaGraphDestroy(graph);
@@ -790,7 +794,7 @@ int bh_query_batch(bh_graph *g, const bh_query_params *p, const int32_t *sources
         const int B = p->slots > 0 ? p->slots : auto_slots(g, n_q);
         EngineBase &e = engine_for(g, B);
         c.last = &e;
-        RunSpec rs;
+        RunSpec rs{};
         rs.job = BH_JOB_BHPP;
         rs.n_q = n_q;
         rs.alpha = p->alpha;
@@ -874,7 +878,7 @@ int bh_push_run(bh_graph *g, int32_t job, int32_t source, double alpha, double l
         }
         grow(c.d_scores, c.cap_sc, nu);
         BH_CUDA(cudaMemcpyAsync(c.d_src, &source, sizeof(int32_t), cudaMemcpyHostToDevice, st));
-        RunSpec rs;
+        RunSpec rs{};
         rs.job = job;
         rs.n_q = 1;
         rs.sources = c.d_src;
@@ -933,7 +937,7 @@ int bh_power_iteration(bh_graph *g, const double *start, int64_t n_vec, double a
         double *d_out = dalloc<double>((size_t)n_vec * nu);
         try {
             BH_CUDA(cudaMemcpyAsync(d_x0, start, n_vec * nu * sizeof(double), cudaMemcpyHostToDevice, st));
-            RunSpec rs;
+            RunSpec rs{};
             rs.job = BH_JOB_POWER;
             rs.n_q = n_vec;
             rs.sources = c.d_src;
