@@ -267,6 +267,7 @@ def run_ours(args):
         def run_steps(nsteps, profiled):
             _capi.set_profiling(profiled)
             ms = 0.0
+            per_step = []
             prof = {"ms_prep": 0.0, "ms_vpull": 0.0, "ms_upull": 0.0, "ms_control": 0.0, "rounds": 0, "slots": 0}
             traces = []
             for _ in range(nsteps):
@@ -279,12 +280,14 @@ def run_ours(args):
                 e1.record(stream)
                 e1.synchronize()
                 ms += e0.elapsed_time(e1)
+                per_step.append(e0.elapsed_time(e1))
                 st = dg.last_run_stats()
                 for key in ("ms_prep", "ms_vpull", "ms_upull", "ms_control", "rounds"):
                     prof[key] += st[key]
                 prof["slots"] = st["slots"]
                 traces.append(tr.cpu().numpy().copy().view(_capi.TRACE_DTYPE).reshape(-1))
             _capi.set_profiling(False)
+            prof["step_ms"] = per_step
             return ms, prof, traces
 
         run_steps(warmup, False)
@@ -293,7 +296,7 @@ def run_ours(args):
             dist.barrier()
         clocks = Clocks(local)
         launches0 = _capi.kernel_launches()
-        ms, _, traces_all = run_steps(steps, False)
+        ms, tprof, traces_all = run_steps(steps, False)
         launches = _capi.kernel_launches() - launches0
         clk = clocks.stop()
         torch.cuda.synchronize(dev)
@@ -303,6 +306,7 @@ def run_ours(args):
             ms = float(t.item())
             dist.barrier()
         pms, prof, ptraces = run_steps(steps, True)
+        prof["timed_step_ms"] = tprof["step_ms"]
         return ms, launches, prof, clk, ptraces, pms
 
     # headline: fp32 storage / fp64 accumulation
@@ -380,6 +384,8 @@ def run_ours(args):
                           "(the headline value is timed without per-kernel events)",
                 "breakdown_ms_per_step": {k2: prof[k2] / args.steps for k2 in ("ms_prep", "ms_vpull", "ms_upull", "ms_control")},
                 "peak_source": peak_src,
+                "timed_step_ms": [round(x, 3) for x in prof.get("timed_step_ms", [])],
+                "profiled_step_ms": [round(x, 3) for x in prof.get("step_ms", [])],
             },
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(n * 4),

@@ -103,14 +103,13 @@ constexpr int CONTROL_THREADS = 256;
 // from the query queue in slot order and publishes the round's flags.
 __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
     pdl_begin();
-    __shared__ int64_t r_cnt[CONTROL_THREADS];
-    __shared__ int64_t r_np[CONTROL_THREADS];
-    __shared__ double r_sum[CONTROL_THREADS];
-    __shared__ double r_wsum[CONTROL_THREADS];
-    __shared__ int32_t r_any[CONTROL_THREADS];
-    __shared__ double r_left[CONTROL_THREADS];
+    constexpr int NW = CONTROL_THREADS / 32;
+    __shared__ int64_t w_cnt[NW], w_np[NW];
+    __shared__ double w_sum[NW], w_wsum[NW], w_left[NW];
+    __shared__ int32_t w_any[NW];
     __shared__ int32_t s_last;
     const int tid = threadIdx.x;
+    const int lane = tid & 31, wid = tid >> 5;
     const int s = blockIdx.x;
     const int B = a.B;
     Control *ctl = a.ctl;
@@ -121,58 +120,104 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
         }
         return;
     }
-    {
-        int64_t cnt = 0, np = 0;
-        double sum = 0.0, wsum = 0.0;
-        int32_t any = 0;
-        double left = 0.0;
-        if (!a.first) {
-            // partial rows are stored slot-major: [slot][row]
-            const int64_t *pc = a.part.cnt + (int64_t)s * a.part.rows_k1;
-            const int64_t *pn = a.part.np_u + (int64_t)s * a.part.rows_k1;
-            const double *pl = a.part.lmass + (int64_t)s * a.part.rows_k1;
-            for (int r = tid; r < a.part.rows_k1; r += CONTROL_THREADS) {
-                cnt += pc[r];
-                np += pn[r];
-                left += pl[r];
+    // Deterministic reduction of the slot's partial rows: each thread adds a
+    // fixed strided subset (4 independent loads in flight), then a fixed-shape
+    // shuffle tree per warp and across the warps.
+    int64_t cnt = 0, np = 0;
+    double sum = 0.0, wsum = 0.0, left = 0.0;
+    int32_t any = 0;
+    if (!a.first) {
+        constexpr int U4 = 4, STEP = CONTROL_THREADS * U4;
+        // partial rows are stored slot-major: [slot][row]
+        const int64_t *pc = a.part.cnt + (int64_t)s * a.part.rows_k1;
+        const int64_t *pn = a.part.np_u + (int64_t)s * a.part.rows_k1;
+        const double *pl = a.part.lmass + (int64_t)s * a.part.rows_k1;
+        const int64_t *pv = a.part.np_v + (int64_t)s * a.part.rows_k2;
+        const int32_t *pa = a.part.any + (int64_t)s * a.part.rows_k3;
+        const double *ps = a.part.sum + (int64_t)s * a.part.rows_k3;
+        const double *pw = a.part.wsum + (int64_t)s * a.part.rows_k3;
+        for (int r0 = 0; r0 < a.part.rows_k1; r0 += STEP) {
+            int64_t c4[U4], n4[U4];
+            double l4[U4];
+#pragma unroll
+            for (int j = 0; j < U4; j++) {
+                const int r = r0 + j * CONTROL_THREADS + tid;
+                const bool ok = r < a.part.rows_k1;
+                c4[j] = ok ? __ldcg(pc + r) : 0;
+                n4[j] = ok ? __ldcg(pn + r) : 0;
+                l4[j] = ok ? __ldcg(pl + r) : 0.0;
             }
-            const int64_t *pv = a.part.np_v + (int64_t)s * a.part.rows_k2;
-            for (int r = tid; r < a.part.rows_k2; r += CONTROL_THREADS) np += pv[r];
-            const int32_t *pa = a.part.any + (int64_t)s * a.part.rows_k3;
-            const double *ps = a.part.sum + (int64_t)s * a.part.rows_k3;
-            const double *pw = a.part.wsum + (int64_t)s * a.part.rows_k3;
-            for (int r = tid; r < a.part.rows_k3; r += CONTROL_THREADS) {
-                any |= pa[r];
-                sum += ps[r];
-                wsum += pw[r];
+#pragma unroll
+            for (int j = 0; j < U4; j++) {
+                cnt += c4[j];
+                np += n4[j];
+                left += l4[j];
             }
         }
-        r_cnt[tid] = cnt;
-        r_np[tid] = np;
-        r_sum[tid] = sum;
-        r_wsum[tid] = wsum;
-        r_any[tid] = any;
-        r_left[tid] = left;
+        for (int r0 = 0; r0 < a.part.rows_k2; r0 += STEP) {
+            int64_t n4[U4];
+#pragma unroll
+            for (int j = 0; j < U4; j++) {
+                const int r = r0 + j * CONTROL_THREADS + tid;
+                n4[j] = r < a.part.rows_k2 ? __ldcg(pv + r) : 0;
+            }
+#pragma unroll
+            for (int j = 0; j < U4; j++) np += n4[j];
+        }
+        for (int r0 = 0; r0 < a.part.rows_k3; r0 += STEP) {
+            int32_t a4[U4];
+            double s4[U4], w4[U4];
+#pragma unroll
+            for (int j = 0; j < U4; j++) {
+                const int r = r0 + j * CONTROL_THREADS + tid;
+                const bool ok = r < a.part.rows_k3;
+                a4[j] = ok ? __ldcg(pa + r) : 0;
+                s4[j] = ok ? __ldcg(ps + r) : 0.0;
+                w4[j] = ok ? __ldcg(pw + r) : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < U4; j++) {
+                any |= a4[j];
+                sum += s4[j];
+                wsum += w4[j];
+            }
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        cnt += __shfl_down_sync(0xffffffffu, cnt, off);
+        np += __shfl_down_sync(0xffffffffu, np, off);
+        sum += __shfl_down_sync(0xffffffffu, sum, off);
+        wsum += __shfl_down_sync(0xffffffffu, wsum, off);
+        left += __shfl_down_sync(0xffffffffu, left, off);
+        any |= __shfl_down_sync(0xffffffffu, any, off);
+    }
+    if (lane == 0) {
+        w_cnt[wid] = cnt;
+        w_np[wid] = np;
+        w_sum[wid] = sum;
+        w_wsum[wid] = wsum;
+        w_left[wid] = left;
+        w_any[wid] = any;
     }
     __syncthreads();
-    for (int off = CONTROL_THREADS / 2; off > 0; off >>= 1) {  // fixed-shape tree
-        if (tid < off) {
-            r_cnt[tid] += r_cnt[tid + off];
-            r_np[tid] += r_np[tid + off];
-            r_sum[tid] += r_sum[tid + off];
-            r_wsum[tid] += r_wsum[tid + off];
-            r_any[tid] |= r_any[tid + off];
-            r_left[tid] += r_left[tid + off];
+    if (tid == 0) {
+        for (int w = 1; w < NW; w++) {
+            w_cnt[0] += w_cnt[w];
+            w_np[0] += w_np[w];
+            w_sum[0] += w_sum[w];
+            w_wsum[0] += w_wsum[w];
+            w_left[0] += w_left[w];
+            w_any[0] |= w_any[w];
         }
-        __syncthreads();
     }
     if (tid == 0) {
         Slot sl = a.slots[s];
         bool fin = false;
         const int op = a.first ? OP_IDLE : sl.op;
-        const int64_t cnt = r_cnt[0];
-        const int32_t any = r_any[0];
-        const double sum = r_sum[0], wsum = r_wsum[0];
+        const int64_t cnt = w_cnt[0];
+        const int32_t any = w_any[0];
+        const double sum = w_sum[0], wsum = w_wsum[0];
         if (op == OP_MEASURE) {  // pi_push entry: gamma of the uploaded ledger (push_engine.py:222)
             sl.gamma = wsum;
             sl.mass_prev = wsum;
@@ -181,7 +226,7 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
         } else if (op_is_push(op)) {
             sl.push_seq++;
             const int64_t worked = cnt > 0;
-            sl.n_p += r_np[0];
+            sl.n_p += w_np[0];
             bool end_backward = false;
             if (op == OP_BSEL_INIT || op == OP_BSEL) {
                 sl.sel_b += worked;
@@ -227,7 +272,7 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
                 // f_j = L_j / m_{j-1}.  The budget test n_p - n_0 >= 2|E| ln(gamma/wmass)/ln(1/(1-alpha))
                 // becomes (2|E| k - used) <= 2|E| sum_j log1p(...) / ln(1/(1-alpha)): a comparison of
                 // two small quantities that fp32 residues resolve as well as fp64 ones.
-                const double fj = sl.mass_prev > 0.0 ? r_left[0] / sl.mass_prev : 0.0;
+                const double fj = sl.mass_prev > 0.0 ? w_left[0] / sl.mass_prev : 0.0;
                 if (fj > 0.0) sl.defsum += log1p(a.alpha * fj / (1.0 - a.alpha));
                 sl.mass_prev = wsum;
                 if (!any) {
@@ -282,7 +327,7 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
                     sl.mass_prev = wsum;
                     sl.defsum = 0.0;
                     sl.n_p_entry = sl.n_p;
-                            sl.tie_checks = 0;
+                    sl.tie_checks = 0;
                 }
             }
         } else if (op == OP_PIENTRY0) {
@@ -310,46 +355,52 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
     if (!s_last) return;
     // last block: refill free slots in slot order (prefix count), publish flags
     __threadfence();
-    __shared__ int32_t f_free[MAX_B], f_fin[MAX_B], pre_free[MAX_B], pre_fin[MAX_B];
+    // slot-order prefix counts of the free / finishing slots (ballots per warp)
+    __shared__ int32_t w_free[MAX_B / 32], w_fin[MAX_B / 32];
     volatile Control *vc = ctl;
+    int32_t my_free = 0, my_fin = 0, pre_free = 0, pre_fin = 0;
     if (tid < B) {
         const int32_t f = vc->free_slot[tid];
-        f_free[tid] = f & 1;
-        f_fin[tid] = (f >> 1) & 1;
+        my_free = f & 1;
+        my_fin = (f >> 1) & 1;
+    }
+    const uint32_t b_free = __ballot_sync(0xffffffffu, my_free), b_fin = __ballot_sync(0xffffffffu, my_fin);
+    if (lane == 0 && wid < MAX_B / 32) {
+        w_free[wid] = __popc(b_free);
+        w_fin[wid] = __popc(b_fin);
     }
     __syncthreads();
-    if (tid == 0) {
-        int32_t a1 = 0, a2 = 0;
-        for (int i = 0; i < B; i++) {
-            pre_free[i] = a1;
-            pre_fin[i] = a2;
-            a1 += f_free[i];
-            a2 += f_fin[i];
+    const uint32_t below = (1u << lane) - 1u;
+    pre_free = __popc(b_free & below);
+    pre_fin = __popc(b_fin & below);
+    int32_t nfree = 0, nfin = 0;
+    for (int w = 0; w < (B + 31) / 32; w++) {
+        if (w < wid) {
+            pre_free += w_free[w];
+            pre_fin += w_fin[w];
         }
-        s_last = a2;  // reuse: number finishing
+        nfree += w_free[w];
+        nfin += w_fin[w];
     }
-    __syncthreads();
     const int32_t next0 = vc->next_q, n_q = vc->n_q;
     int32_t busy = 0;
     if (tid < B) {
-        if (f_fin[tid]) ctl->fin_slots[pre_fin[tid]] = tid;
-        const int32_t q = next0 + pre_free[tid];
-        if (f_free[tid] && q < n_q) {
+        if (my_fin) ctl->fin_slots[pre_fin] = tid;
+        const int32_t q = next0 + pre_free;
+        if (my_free && q < n_q) {
             Slot ns;
             slot_start(ns, a, q);
             a.slots[tid] = ns;
             busy = ns.op != OP_IDLE;
         } else {
-            if (f_free[tid]) a.slots[tid].qidx = -1;
+            if (my_free) a.slots[tid].qidx = -1;
             busy = *(volatile int32_t *)&a.slots[tid].op != OP_IDLE;
         }
     }
     busy = __syncthreads_or(busy);
     if (tid == 0) {
-        int32_t nfree = 0;
-        for (int i = 0; i < B; i++) nfree += f_free[i];
         ctl->next_q = min(n_q, next0 + nfree);
-        ctl->n_fin = s_last;
+        ctl->n_fin = nfin;
         if (!a.first) ctl->rounds_active++;
         if (ctl->rounds_active > a.max_rounds) {  // runaway guard (never expected)
             busy = 0;

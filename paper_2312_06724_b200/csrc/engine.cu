@@ -215,11 +215,26 @@ struct Engine final : EngineBase {
     bool half_v = false, half_u = false;
     static constexpr int64_t HALF_MIN_AVG_DEG = 16;
 
+    // Full-warp workers: (col, val) windows in shared memory (k_pull_sw) or in
+    // lane registers (k_pull).  Measured at c2 on B200: fp32 is fastest with
+    // k_pull_sw on both sides; fp64 (16 B per lane, S = 8) with k_pull and
+    // half-warp workers on the long-row side.
+    bool pull_sw = sizeof(T) == 4;
+    using PullFn = void (*)(PullArgs<T>);
+    template <int SIDE>
+    PullFn sw_kernel() const {
+        return k_pull_sw<B, T, SIDE>;
+    }
+
     void pull_kernel(int side, void **fn) const {
         if constexpr (WIDE) {
             const bool half = side == SIDE_V ? half_v : half_u;
-            if (side == SIDE_V) *fn = half ? (void *)k_pull_half<B, T, SIDE_V> : (void *)k_pull<B, T, SIDE_V>;
-            else *fn = half ? (void *)k_pull_half<B, T, SIDE_U> : (void *)k_pull<B, T, SIDE_U>;
+            if (side == SIDE_V)
+                *fn = half ? (void *)k_pull_half<B, T, SIDE_V>
+                           : (pull_sw ? (void *)sw_kernel<SIDE_V>() : (void *)k_pull<B, T, SIDE_V>);
+            else
+                *fn = half ? (void *)k_pull_half<B, T, SIDE_U>
+                           : (pull_sw ? (void *)sw_kernel<SIDE_U>() : (void *)k_pull<B, T, SIDE_U>);
         } else {
             *fn = side == SIDE_V ? (void *)k_pull_small<B, T, SIDE_V> : (void *)k_pull_small<B, T, SIDE_U>;
         }
@@ -247,8 +262,14 @@ struct Engine final : EngineBase {
         int sms = 148;
         BH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
         pull_smem = 0;
-        half_v = WIDE && g->n_e >= HALF_MIN_AVG_DEG * g->n_v;
-        half_u = WIDE && g->n_e >= HALF_MIN_AVG_DEG * g->n_u;
+        half_v = WIDE && !pull_sw && g->n_e >= HALF_MIN_AVG_DEG * g->n_v;
+        half_u = WIDE && !pull_sw && g->n_e >= HALF_MIN_AVG_DEG * g->n_u;
+        if (const char *m = getenv("BH_PULL_HALF")) {  // tuning override: 0 none, 1 U side, 2 V side, 3 both
+            const int h = atoi(m);
+            half_u = WIDE && (h & 1);
+            half_v = WIDE && (h & 2);
+        }
+        if (const char *m = getenv("BH_PULL_SW")) pull_sw = atoi(m) != 0;
         for (int side = 0; side < 2; side++) {
             void *fn;
             pull_kernel(side, &fn);
@@ -378,9 +399,11 @@ struct Engine final : EngineBase {
             const bool half = side == SIDE_V ? half_v : half_u;
             if (side == SIDE_V) {
                 if (half) launch_pdl(k_pull_half<B, T, SIDE_V>, grid, PULL_THREADS, pull_smem, st, a);
+                else if (pull_sw) launch_pdl(sw_kernel<SIDE_V>(), grid, PULL_THREADS, pull_smem, st, a);
                 else launch_pdl(k_pull<B, T, SIDE_V>, grid, PULL_THREADS, pull_smem, st, a);
             } else {
                 if (half) launch_pdl(k_pull_half<B, T, SIDE_U>, grid, PULL_THREADS, pull_smem, st, a);
+                else if (pull_sw) launch_pdl(sw_kernel<SIDE_U>(), grid, PULL_THREADS, pull_smem, st, a);
                 else launch_pdl(k_pull<B, T, SIDE_U>, grid, PULL_THREADS, pull_smem, st, a);
             }
         } else {

@@ -750,6 +750,189 @@ __global__ void __launch_bounds__(PULL_THREADS, 2) k_pull(PullArgs<T> a) {
     }
 }
 
+// Same streaming pull with the per-warp (col, val) windows and row ends staged
+// in shared memory instead of lane registers: the per-edge work is one
+// broadcast LDS of the next (col, val) pair, the operand-row gather and VEC
+// FMAs, with no warp shuffle (and so no convergence barrier) on the edge path.
+// Cut-row partials go to their scratch slot at emit time.
+// Pipeline depth / residency of k_pull_sw: S = 8 rows in flight per warp at
+// three 256-thread blocks per SM measured fastest at B = 64 fp32 (c2 on B200:
+// more resident warps beat a deeper per-warp pipeline).
+template <int B, typename T>
+struct SwPipe {
+    static constexpr int LANE_BYTES = (B / 32) * (int)sizeof(T);
+    static constexpr int S = LANE_BYTES <= 16 ? 8 : 4;
+    static constexpr int MINB = LANE_BYTES <= 8 ? 3 : 2;
+};
+
+template <typename T>
+struct EdgeCV {
+    int32_t c;
+    T v;
+};
+
+template <int B, typename T, int SIDE, int S = SwPipe<B, T>::S, int MINB = SwPipe<B, T>::MINB>
+__global__ void __launch_bounds__(PULL_THREADS, MINB) k_pull_sw(PullArgs<T> a) {
+    pdl_begin();
+    if (*a.active == 0) return;
+    constexpr int VEC = RegPipe<B, T>::VEC;
+    static_assert(2 * S <= 32, "two windows must fit one warp load");
+    __shared__ EdgeCV<T> s_win[PULL_WARPS][2][S];
+    __shared__ int32_t s_re[PULL_WARPS][64];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int gw = blockIdx.x * PULL_WARPS + warp;
+    const int slot0 = lane * VEC;
+    uint32_t cmask = 0;
+    if constexpr (SIDE == SIDE_V) {
+#pragma unroll
+        for (int v = 0; v < VEC; v++) cmask |= (op_is_push(a.slots[slot0 + v].op) ? 1u : 0u) << v;
+    }
+    const double scale = SIDE == SIDE_V ? a.one_minus_alpha : 1.0;
+    int32_t np[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; v++) np[v] = 0;
+    int64_t np_cut[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; v++) np_cut[v] = 0;
+
+    if (gw < a.n_warps) {
+        const WarpWork wk = a.work[gw];
+        const int64_t e0 = wk.e0;
+        const int n = (int)(wk.e1 - e0);
+        if (n > 0) {
+            const int32_t *cols = a.indices + e0;
+            const T *vals = a.vals + e0;
+            const T *X = a.X + slot0;
+            T *Y0 = a.Y + (int64_t)wk.r0 * B + slot0;
+            const int64_t *rp = a.indptr + wk.r0;
+            const int64_t nrow_left = a.n_rows - wk.r0;
+            const int cutA = wk.cut0 >= 0 ? 0 : -1;
+            const int cutB = wk.cut1 >= 0 ? (int)(a.cuts[wk.cut1].row - wk.r0) : -1;
+            auto col_at = [&](int o) { return o < n ? __ldg(cols + o) : 0; };
+            auto val_at = [&](int o) { return o < n ? __ldg(vals + o) : (T)0; };
+            auto rend_at = [&](int i) {
+                const int64_t r = i + 1 <= nrow_left ? __ldg(rp + i + 1) : __ldg(rp + nrow_left);
+                return (int)imin64(r - e0, (int64_t)n);
+            };
+            EdgeCV<T>(*win)[S] = s_win[warp];
+            int32_t *re = s_re[warp];
+            re[lane] = rend_at(lane);
+            re[32 + lane] = rend_at(32 + lane);
+            if (lane < 2 * S) win[lane / S][lane % S] = EdgeCV<T>{col_at(lane), val_at(lane)};
+            // register prefetch of block 2's window (lanes < S)
+            int cw = col_at(2 * S + lane);
+            T vw = val_at(2 * S + lane);
+            __syncwarp();
+            T xs[S][VEC];
+            T wsv[S];
+#pragma unroll
+            for (int t = 0; t < S; t++) {
+                const EdgeCV<T> e = win[0][t];
+                wsv[t] = e.v;
+                ldg_vec<T, VEC>(X + (int64_t)e.c * B, xs[t]);
+            }
+            int rw = 0;       // row-end ring holds local rows [rw, rw + 64)
+            int lr = 0;
+            int rstart = (int)(__ldg(rp) - e0);
+            int rend = re[0];
+            double acc[VEC];
+            T accs[VEC];
+#pragma unroll
+            for (int v = 0; v < VEC; v++) {
+                acc[v] = 0.0;
+                accs[v] = (T)0;
+            }
+            int b = 0;
+            for (int base = 0; base < n; base += S, b ^= 1) {
+                const EdgeCV<T> *nxt = win[b ^ 1];
+                int d = rend - base - 1;
+#pragma unroll
+                for (int t = 0; t < S; t++) {
+                    if constexpr (sizeof(T) == 8) {
+#pragma unroll
+                        for (int v = 0; v < VEC; v++) acc[v] = fma((double)wsv[t], (double)xs[t][v], acc[v]);
+                    } else {
+#pragma unroll
+                        for (int v = 0; v < VEC; v++) accs[v] = fmaf(wsv[t], xs[t][v], accs[v]);
+                    }
+                    if (d == t) {  // row emit
+                        if constexpr (sizeof(T) == 4) {
+#pragma unroll
+                            for (int v = 0; v < VEC; v++) {
+                                acc[v] += (double)accs[v];
+                                accs[v] = (T)0;
+                            }
+                        }
+                        if (lr == cutA || lr == cutB) {
+                            double *dst = a.scratch + (int64_t)(lr == cutA ? wk.part0 : wk.part1) * B + slot0;
+#pragma unroll
+                            for (int v = 0; v < VEC; v++) dst[v] = acc[v];
+                        } else {
+                            T out[VEC];
+#pragma unroll
+                            for (int v = 0; v < VEC; v++) {
+                                out[v] = (T)(scale * acc[v]);
+                                if constexpr (SIDE == SIDE_V)
+                                    np[v] += (((cmask >> v) & 1u) && out[v] > (T)0) ? rend - rstart : 0;
+                            }
+                            VecIO<T, VEC>::st(Y0 + (int64_t)lr * B, out);
+                        }
+#pragma unroll
+                        for (int v = 0; v < VEC; v++) acc[v] = 0.0;
+                        lr++;
+                        rstart = rend;
+                        rend = re[lr & 63];
+                        d = rend - base - 1;
+                    }
+                    const EdgeCV<T> e = nxt[t];
+                    wsv[t] = e.v;
+                    ldg_vec<T, VEC>(X + (int64_t)e.c * B, xs[t]);
+                }
+                if constexpr (sizeof(T) == 4) {
+#pragma unroll
+                    for (int v = 0; v < VEC; v++) {
+                        acc[v] += (double)accs[v];
+                        accs[v] = (T)0;
+                    }
+                }
+                // stage block (base/S + 2) into the window block (base/S) read during
+                // the previous block, refill the row-end ring half that is behind lr
+                if (lane < S) win[b][lane] = EdgeCV<T>{cw, vw};
+                if (lr - rw >= 32) {
+                    re[(rw + 64 + lane) & 63] = rend_at(rw + 64 + lane);
+                    rw += 32;
+                }
+                cw = col_at(base + 3 * S + lane);
+                vw = val_at(base + 3 * S + lane);
+                __syncwarp();
+            }
+            const CutCtx<T> cx{a.scratch, a.cut_count, a.cuts, a.Y, a.indptr, scale};
+            if (cutA >= 0) {
+                DVec<VEC> av;
+#pragma unroll
+                for (int v = 0; v < VEC; v++) av.v[v] = a.scratch[(int64_t)wk.part0 * B + slot0 + v];
+                const IVec<VEC> inc = pull_cut<B, T, VEC>(cx, wk.cut0, wk.part0, slot0, cmask, av);
+#pragma unroll
+                for (int v = 0; v < VEC; v++) np_cut[v] += inc.v[v];
+            }
+            if (cutB >= 0) {
+                DVec<VEC> av;
+#pragma unroll
+                for (int v = 0; v < VEC; v++) av.v[v] = a.scratch[(int64_t)wk.part1 * B + slot0 + v];
+                const IVec<VEC> inc = pull_cut<B, T, VEC>(cx, wk.cut1, wk.part1, slot0, cmask, av);
+#pragma unroll
+                for (int v = 0; v < VEC; v++) np_cut[v] += inc.v[v];
+            }
+        }
+    }
+    if constexpr (SIDE == SIDE_V) {
+        if (gw < a.n_warps)
+#pragma unroll
+            for (int v = 0; v < VEC; v++) a.np_v[(int64_t)(slot0 + v) * a.n_warps + gw] = (int64_t)np[v] + np_cut[v];
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Half-warp workers (B >= 32): each 16-lane half of a warp is an independent
 // worker with its own cost-balanced edge range; a lane owns VEC = B/16 slots

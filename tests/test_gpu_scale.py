@@ -128,3 +128,19 @@ def test_scaled_config_refill_fp32_consistent(cfg):
     b = bh.bhpp_query_batch(g, meta, src, 1e-6, k=20, dtype="fp32", slots=16)
     for i in range(len(src)):
         np.testing.assert_allclose(b.topk_score[i], a.scores[i][a.topk_index[i]], rtol=1e-5, atol=1e-6)
+
+
+def test_pisp_query_matches_oracle_composition():
+    g = config_graph("c1")
+    og = O.OracleGraph(g)
+    for q, eps in ((0, 1e-4), (17, 1e-6)):
+        r = bh.pisp_query(g, q, 0.15, eps)
+        depth = O.required_iterations(0.15, eps / 2, 1.0)
+        start = np.zeros(g.u_count)
+        start[q] = 1.0
+        fwd = og.power_iteration(start, 0.15, depth)
+        led, tr = og.ss_push(q, 0.15, eps / 2, budget=False)
+        np.testing.assert_allclose(r.scores, fwd + led["estimate"], atol=1e-12)
+        assert r.phase_trace["forward"]["power_iterations"] == depth
+        assert r.phase_trace["backward"]["selective_rounds"] == tr["selective_rounds"]
+        assert r.method == "pisp"
