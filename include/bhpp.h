@@ -14,6 +14,7 @@
  *   ss_push / selective_push / pi_push (push_engine.py:120-258) -> bh_push_run
  *   power_iteration (push_engine.py:101-117), estimate_lambda   -> bh_power_iteration
  *   topk (bhpp_query.py:206-218) on an arbitrary score vector   -> bh_topk
+ *   BipartiteGraph.__init__ canonicalisation (bigraph.py:53-111) -> bh_csr_build
  *
  * Status codes: 0 ok; BH_EINVAL -> ValueError; BH_EUNFLUSHED -> ValueError
  * ("unflushed ledger", push_engine.py:214-217); BH_ECUDA -> RuntimeError;
@@ -34,6 +35,7 @@ extern "C" {
 #define BH_EUNFLUSHED 2
 #define BH_ECUDA 3
 #define BH_ENOMEM 4
+#define BH_EDUP 5 /* bh_csr_build: a (u, v) pair repeats (bigraph.py:84-88) */
 
 #define BH_DTYPE_F64 0 /* fp64 storage, fp64 arithmetic                       */
 #define BH_DTYPE_F32 1 /* fp32 storage, fp64 row accumulation and control     */
@@ -135,6 +137,18 @@ int bh_power_iteration(bh_graph *g, const double *start, int64_t n_vec, double a
  * *out_count.  Host pointers. */
 int bh_topk(const double *scores, int64_t n, int64_t k, int64_t exclude, int64_t *out_idx,
             double *out_score, int64_t *out_count);
+
+/* ---- graph ingestion (bigraph.py:53-111) ---------------------------------- */
+/* Canonical CSR of both sides from n_e edge triples (host pointers in and
+ * out), built on `device` with two radix sorts of the packed pair keys:
+ * U rows sorted by v, V rows sorted by u, weights carried along, ws_u / ws_v
+ * summed in CSR order (bit-identical to the reference's np.bincount).
+ * Endpoints must lie in [0, n_u) x [0, n_v) (BH_EINVAL otherwise); a repeated
+ * pair returns BH_EDUP and leaves the outputs unspecified.  Sizes < 2^31. */
+int bh_csr_build(int64_t n_u, int64_t n_v, int64_t n_e, const int64_t *edge_u, const int64_t *edge_v,
+                 const double *edge_w, int64_t *u_indptr, int32_t *u_indices, double *u_weights,
+                 int64_t *v_indptr, int32_t *v_indices, double *v_weights, double *ws_u, double *ws_v,
+                 int32_t device);
 
 /* ---- measurement ---------------------------------------------------------- */
 typedef struct bh_run_stats {

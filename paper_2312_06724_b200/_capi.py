@@ -17,7 +17,7 @@ import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libbhpp.so"
 
-BH_OK, BH_EINVAL, BH_EUNFLUSHED, BH_ECUDA, BH_ENOMEM = 0, 1, 2, 3, 4
+BH_OK, BH_EINVAL, BH_EUNFLUSHED, BH_ECUDA, BH_ENOMEM, BH_EDUP = 0, 1, 2, 3, 4, 5
 DTYPES = {"fp64": 0, "f64": 0, "float64": 0, "fp32": 1, "f32": 1, "float32": 1}
 JOB_BHPP, JOB_SS_PUSH, JOB_SELECTIVE, JOB_PI_PUSH, JOB_POWER = 0, 1, 2, 3, 4
 TERMINATIONS = ("threshold-met", "budget-switch", "mass-drained")
@@ -26,7 +26,7 @@ PHASES = ("selective", "sequential", "forward-selective")
 EXPORTS = (
     "bh_graph_create", "bh_graph_destroy", "bh_graph_get_info", "bh_query_batch", "bh_push_run",
     "bh_power_iteration", "bh_topk", "bh_last_error", "bh_version", "bh_kernel_launches",
-    "bh_set_profiling", "bh_last_run_stats",
+    "bh_set_profiling", "bh_last_run_stats", "bh_csr_build",
 )
 
 
@@ -116,6 +116,8 @@ def lib():
         L.bh_set_profiling.argtypes = [C.c_int32]
         L.bh_last_run_stats.restype = C.c_int
         L.bh_last_run_stats.argtypes = [P, C.POINTER(RunStats)]
+        L.bh_csr_build.restype = C.c_int
+        L.bh_csr_build.argtypes = [C.c_int64] * 3 + [P] * 11 + [C.c_int32]
         _lib = L
     return _lib
 
@@ -124,7 +126,7 @@ def check(rc: int) -> None:
     if rc == BH_OK:
         return
     msg = (lib().bh_last_error() or b"").decode("utf-8", "replace")
-    if rc in (BH_EINVAL, BH_EUNFLUSHED):
+    if rc in (BH_EINVAL, BH_EUNFLUSHED, BH_EDUP):
         raise ValueError(msg)
     if rc == BH_ENOMEM:
         raise MemoryError(msg)
@@ -133,6 +135,27 @@ def check(rc: int) -> None:
 
 def ptr(a):
     return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+def csr_build(n_u: int, n_v: int, eu, ev, ew, device: int = 0) -> dict | None:
+    """Both canonical CSR sides of an edge list, built on ``device``
+    (bh_csr_build).  Returns None when a (u, v) pair repeats."""
+    eu = np.ascontiguousarray(eu, dtype=np.int64)
+    ev = np.ascontiguousarray(ev, dtype=np.int64)
+    ew = np.ascontiguousarray(ew, dtype=np.float64)
+    n_e = int(eu.size)
+    out = {
+        "u_indptr": np.empty(n_u + 1, np.int64), "u_indices": np.empty(n_e, np.int32),
+        "u_weights": np.empty(n_e, np.float64), "v_indptr": np.empty(n_v + 1, np.int64),
+        "v_indices": np.empty(n_e, np.int32), "v_weights": np.empty(n_e, np.float64),
+        "ws_u": np.empty(n_u, np.float64), "ws_v": np.empty(n_v, np.float64),
+    }
+    rc = lib().bh_csr_build(n_u, n_v, n_e, ptr(eu), ptr(ev), ptr(ew), *[ptr(out[k]) for k in (
+        "u_indptr", "u_indices", "u_weights", "v_indptr", "v_indices", "v_weights", "ws_u", "ws_v")], int(device))
+    if rc == BH_EDUP:
+        return None
+    check(rc)
+    return out
 
 
 def kernel_launches() -> int:
@@ -156,15 +179,6 @@ class DeviceGraph:
             np.ascontiguousarray(g.ws_u, dtype=np.float64),
             np.ascontiguousarray(g.ws_v, dtype=np.float64),
         ]
-        import os
-        if os.environ.get("BH_PERMUTE_ROWS"):  # experiment: scatter column order within rows
-            arrs = [a.copy() for a in arrs]
-            for ip, ix, w in ((arrs[0], arrs[1], arrs[2]), (arrs[3], arrs[4], arrs[5])):
-                rowid = np.repeat(np.arange(ip.size - 1), np.diff(ip))
-                key = (ix.astype(np.int64) * 2654435761) % 1000003
-                order = np.lexsort((key, rowid))
-                ix[:] = ix[order]
-                w[:] = w[order]
         h = C.c_void_p()
         check(lib().bh_graph_create(self.n_u, self.n_v, self.n_e, *[ptr(a) for a in arrs], self.device,
                                     DTYPES[dtype], C.byref(h)))

@@ -89,7 +89,10 @@ class BipartiteGraph:
     (bigraph.py:53-111).
     """
 
-    def __init__(self, u_labels, v_labels, edge_u, edge_v, edge_w):
+    def __init__(self, u_labels, v_labels, edge_u, edge_v, edge_w, *, device: int | None = None):
+        """``device``: build the canonical CSR arrays on that CUDA device
+        (bh_csr_build: two radix sorts of the packed pair keys) instead of with
+        host sorts; the arrays and ws sums are bit-identical either way."""
         if not isinstance(u_labels, IndexLabels):
             u_labels = list(u_labels)
         if not isinstance(v_labels, IndexLabels):
@@ -123,6 +126,9 @@ class BipartiteGraph:
         self.u_labels = u_labels
         self.v_labels = v_labels
 
+        if device is not None:
+            self._build_on_device(eu, ev, ew, int(device))
+            return
         # Canonical order: rows sorted by (u, v).  A stable argsort of the
         # unique pair key is the same permutation as the reference's lexsort.
         key = eu * n_v + ev
@@ -134,12 +140,7 @@ class BipartiteGraph:
 
         self.deg_u = _frozen(np.bincount(eu, minlength=n_u))
         self.deg_v = _frozen(np.bincount(ev, minlength=n_v))
-        if (self.deg_u == 0).any():
-            i = int(np.flatnonzero(self.deg_u == 0)[0])
-            raise DataError(f"isolated node on U side: {u_labels[i]!r}")
-        if (self.deg_v == 0).any():
-            i = int(np.flatnonzero(self.deg_v == 0)[0])
-            raise DataError(f"isolated node on V side: {v_labels[i]!r}")
+        self._check_isolated()
 
         self.u_indptr = _frozen(np.concatenate(([0], np.cumsum(self.deg_u))).astype(np.int64))
         self.u_indices = _frozen(ev.astype(np.int32))
@@ -155,12 +156,33 @@ class BipartiteGraph:
         self.ws_u = _frozen(np.bincount(eu, weights=ew, minlength=n_u))
         self.ws_v = _frozen(np.bincount(ev, weights=ew, minlength=n_v))
 
+    def _check_isolated(self):
+        if (self.deg_u == 0).any():
+            i = int(np.flatnonzero(self.deg_u == 0)[0])
+            raise DataError(f"isolated node on U side: {self.u_labels[i]!r}")
+        if (self.deg_v == 0).any():
+            i = int(np.flatnonzero(self.deg_v == 0)[0])
+            raise DataError(f"isolated node on V side: {self.v_labels[i]!r}")
+
+    def _build_on_device(self, eu, ev, ew, device: int):
+        from . import _capi
+
+        out = _capi.csr_build(self.u_count, self.v_count, eu, ev, ew, device)
+        if out is None:
+            raise DataError("duplicate edge passed to constructor")
+        self.edge_count = int(eu.size)
+        self.deg_u = _frozen(np.diff(out["u_indptr"]))
+        self.deg_v = _frozen(np.diff(out["v_indptr"]))
+        self._check_isolated()
+        for k in ("u_indptr", "u_indices", "u_weights", "v_indptr", "v_indices", "v_weights", "ws_u", "ws_v"):
+            setattr(self, k, _frozen(out[k]))
+
     # -- construction helpers ------------------------------------------------
 
     @classmethod
-    def from_arrays(cls, u_count: int, v_count: int, edge_u, edge_v, edge_w):
+    def from_arrays(cls, u_count: int, v_count: int, edge_u, edge_v, edge_w, device: int | None = None):
         """Graph with labels "u{i}" / "v{j}" (the reference synth convention)."""
-        return cls(IndexLabels("u", u_count), IndexLabels("v", v_count), edge_u, edge_v, edge_w)
+        return cls(IndexLabels("u", u_count), IndexLabels("v", v_count), edge_u, edge_v, edge_w, device=device)
 
     @classmethod
     def from_edges(cls, u_labels, v_labels, triples):
@@ -217,7 +239,7 @@ class BipartiteGraph:
         return out.getvalue()
 
     @classmethod
-    def from_bytes(cls, buf: bytes) -> "BipartiteGraph":
+    def from_bytes(cls, buf: bytes, device: int | None = None) -> "BipartiteGraph":
         if len(buf) < 4 + 4 + 24 or buf[:4] != CACHE_MAGIC:
             raise DataError("not a graph cache file (bad magic)")
         (version,) = struct.unpack_from("<I", buf, 4)
@@ -249,14 +271,14 @@ class BipartiteGraph:
         if indptr[0] != 0 or indptr[-1] != edge_count or (np.diff(indptr) < 0).any():
             raise DataError("corrupt adjacency offsets in graph cache")
         eu = np.repeat(np.arange(u_count, dtype=np.int64), np.diff(indptr))
-        return cls(labels[:u_count], labels[u_count:], eu, indices.astype(np.int64), weights)
+        return cls(labels[:u_count], labels[u_count:], eu, indices.astype(np.int64), weights, device=device)
 
     def save(self, path) -> None:
         Path(path).write_bytes(self.to_bytes())
 
     @classmethod
-    def load(cls, path) -> "BipartiteGraph":
-        return cls.from_bytes(Path(path).read_bytes())
+    def load(cls, path, device: int | None = None) -> "BipartiteGraph":
+        return cls.from_bytes(Path(path).read_bytes(), device=device)
 
     @cached_property
     def fingerprint(self) -> str:

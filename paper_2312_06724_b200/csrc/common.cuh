@@ -31,6 +31,11 @@ struct InvalidArg : std::runtime_error {
 
 void count_launch(int n = 1);
 
+// csr_build.cu: device canonicalisation of an edge list (bh_csr_build); 1 = duplicate pair.
+int csr_build(int64_t n_u, int64_t n_v, int64_t n_e, const int64_t *edge_u, const int64_t *edge_v,
+              const double *edge_w, int64_t *u_indptr, int32_t *u_indices, double *u_weights, int64_t *v_indptr,
+              int32_t *v_indices, double *v_weights, double *ws_u, double *ws_v, int device);
+
 // Programmatic dependent launch: every round kernel lets its successor launch
 // early (the successor's blocks occupy SMs freed by this kernel's tail) and
 // waits for its predecessor's memory before touching round state.

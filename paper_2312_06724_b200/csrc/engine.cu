@@ -750,6 +750,25 @@ const char *bh_last_error(void) { return t_err.c_str(); }
 int bh_version(void) { return 1; }
 int64_t bh_kernel_launches(void) { return g_launches.load(); }
 
+int bh_csr_build(int64_t n_u, int64_t n_v, int64_t n_e, const int64_t *edge_u, const int64_t *edge_v,
+                 const double *edge_w, int64_t *u_indptr, int32_t *u_indices, double *u_weights,
+                 int64_t *v_indptr, int32_t *v_indices, double *v_weights, double *ws_u, double *ws_v,
+                 int32_t device) {
+    int dup = 0;
+    const int rc = guarded([&] {
+        if (!edge_u || !edge_v || !edge_w || !u_indptr || !u_indices || !u_weights || !v_indptr || !v_indices ||
+            !v_weights || !ws_u || !ws_v)
+            throw InvalidArg("null argument");
+        dup = csr_build(n_u, n_v, n_e, edge_u, edge_v, edge_w, u_indptr, u_indices, u_weights, v_indptr, v_indices,
+                        v_weights, ws_u, ws_v, device);
+    });
+    if (rc == BH_OK && dup) {
+        t_err = "duplicate edge passed to constructor";
+        return BH_EDUP;
+    }
+    return rc;
+}
+
 int bh_set_profiling(int32_t on) {
     g_profiling = on ? 1 : 0;
     return BH_OK;

@@ -111,12 +111,13 @@ def chung_lu_edges(u_count: int, v_count: int, edge_count: int, beta_u: float, b
     return eu, ev, ew
 
 
-def make_graph(cfg: GraphConfig | str, seed: int | None = None) -> BipartiteGraph:
+def make_graph(cfg: GraphConfig | str, seed: int | None = None, device: int | None = None) -> BipartiteGraph:
+    """The config's graph; ``device`` canonicalises the CSR on that GPU."""
     if isinstance(cfg, str):
         cfg = CONFIGS[cfg]
     eu, ev, ew = chung_lu_edges(cfg.u_count, cfg.v_count, cfg.edge_count, cfg.beta_u, cfg.beta_v,
                                 cfg.weights, cfg.seed if seed is None else seed, cfg.max_deg_v)
-    return BipartiteGraph.from_arrays(cfg.u_count, cfg.v_count, eu, ev, ew)
+    return BipartiteGraph.from_arrays(cfg.u_count, cfg.v_count, eu, ev, ew, device=device)
 
 
 def scaled_config(cfg: GraphConfig | str, scale: float, name: str | None = None) -> GraphConfig:
