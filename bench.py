@@ -117,7 +117,7 @@ class Clocks:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[j] for r in rows if len(r) >= 9 for j in range(4) if r[5 + j].strip() == "Active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows)}
+                "sm_min_mhz": min(sm) if sm else None, "reasons": reasons, "samples": len(rows)}
 
 
 def ncu_round_traffic():
@@ -282,6 +282,7 @@ def run_ours(args):
                 ms += e0.elapsed_time(e1)
                 per_step.append(e0.elapsed_time(e1))
                 st = dg.last_run_stats()
+                prof.setdefault("step_rounds", []).append(int(st["rounds"]))
                 for key in ("ms_prep", "ms_vpull", "ms_upull", "ms_control", "rounds"):
                     prof[key] += st[key]
                 prof["slots"] = st["slots"]
@@ -307,6 +308,7 @@ def run_ours(args):
             dist.barrier()
         pms, prof, ptraces = run_steps(steps, True)
         prof["timed_step_ms"] = tprof["step_ms"]
+        prof["timed_step_rounds"] = tprof["step_rounds"]
         return ms, launches, prof, clk, ptraces, pms
 
     # headline: fp32 storage / fp64 accumulation
@@ -386,6 +388,7 @@ def run_ours(args):
                 "peak_source": peak_src,
                 "timed_step_ms": [round(x, 3) for x in prof.get("timed_step_ms", [])],
                 "profiled_step_ms": [round(x, 3) for x in prof.get("step_ms", [])],
+                "timed_step_rounds": prof.get("timed_step_rounds"),
             },
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(n * 4),

@@ -9,6 +9,7 @@ paper_2312_06724_b200.build`` (also ``__graft_entry__.build()``).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 import weakref
 from pathlib import Path
@@ -16,6 +17,8 @@ from pathlib import Path
 import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libbhpp.so"
+if os.environ.get("BH_LIBBHPP"):  # A/B of two in-tree builds (tools/ab_pull.sh)
+    LIB_PATH = Path(os.environ["BH_LIBBHPP"]).resolve()
 
 BH_OK, BH_EINVAL, BH_EUNFLUSHED, BH_ECUDA, BH_ENOMEM, BH_EDUP = 0, 1, 2, 3, 4, 5
 DTYPES = {"fp64": 0, "f64": 0, "float64": 0, "fp32": 1, "f32": 1, "float32": 1}

@@ -288,7 +288,14 @@ struct Engine final : EngineBase {
             const bool half = side == SIDE_V ? half_v : half_u;
             build_plan(sd, g->n_e, (int)grid * PULL_WARPS * (half ? 2 : 1), pl);
         }
-        grid_elem = grid1d(nu * (B / ElemGeo<B>::EV), ELEM_THREADS, 4 * sms);
+        {  // one resident wave of the elementwise kernels
+            int occ_p = 1, occ_c = 1;
+            BH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, k_push<B, T>, ELEM_THREADS, 0));
+            BH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, k_combine<B, T>, ELEM_THREADS, 0));
+            int occ = std::max(1, std::min(occ_p, occ_c));
+            if (const char *m = getenv("BH_ELEM_BLOCKS_PER_SM")) occ = std::max(1, atoi(m));
+            grid_elem = grid1d(nu * (B / ElemGeo<B>::EV), ELEM_THREADS, occ * sms);
+        }
         n_chunks = (int)((nu + fin_chunk - 1) / fin_chunk);
         grid_k5 = (int)std::min<int64_t>((int64_t)n_chunks * std::min(B, 8), 8 * sms);
         part.rows_k1 = grid_elem;

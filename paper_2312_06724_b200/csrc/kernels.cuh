@@ -167,6 +167,7 @@ __device__ __forceinline__ void load_slot_smem(SlotSmem &sm, const Slot *__restr
 // ---------------------------------------------------------------------------
 // Elementwise kernels over [n_u x B]: one thread per (node, EV consecutive slots).
 constexpr int ELEM_THREADS = 256;
+constexpr int ELEM_UNR = 4;  // nodes in flight per thread in K1 / K1a
 
 template <int B>
 struct ElemGeo {
@@ -206,11 +207,12 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_push(ElemArgs<T> a) {
     __syncthreads();
     const int j0 = (threadIdx.x % TPN) * EV;  // first slot of this thread (fixed: blockDim % TPN == 0)
     int op[EV];
-    bool any_work = false;
+    bool any_work = false, init_any = false;
 #pragma unroll
     for (int v = 0; v < EV; v++) {
         op[v] = sm.op[j0 + v];
         any_work |= op_is_push(op[v]) || op[v] == OP_PIENTRY || op[v] == OP_PIENTRY0;
+        init_any |= op[v] == OP_BSEL_INIT;
     }
     int64_t cnt[EV], npu[EV];
     double left[EV];
@@ -220,59 +222,90 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_push(ElemArgs<T> a) {
         left[v] = 0.0;
     }
     if (any_work) {
+        // UNR nodes per thread in flight: all their loads are issued before any
+        // is consumed (the kernel is latency-bound at one node per thread).
         const int64_t total = a.n_u * TPN;
-        for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-             t += (int64_t)gridDim.x * blockDim.x) {
-            const int64_t u = t / TPN;
-            const int64_t i = u * B + j0;
-            T rv[EV];
-            VecIO<T, EV>::ld(a.R + i, rv);
-            const double iws = a.inv_ws_u[u];
-            const int32_t deg = a.deg_u[u];
-            T pv[EV];
-            bool wrote_r = false;
+        const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+        for (int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t0 < total; t0 += ELEM_UNR * stride) {
+            T rv[ELEM_UNR][EV];
+            double iwsk[ELEM_UNR];
+            int32_t degk[ELEM_UNR];
 #pragma unroll
-            for (int v = 0; v < EV; v++) {
-                const int s = j0 + v;
-                const int o = op[v];
-                pv[v] = (T)0;
-                if (o == OP_PIENTRY || o == OP_PIENTRY0) {
-                    const double *x0 = (a.x0 && sm.qidx[s] >= 0) ? a.x0 + (int64_t)sm.qidx[s] * a.n_u : nullptr;
-                    if (x0) {  // raw power iteration: y0 = start / ws  (push_engine.py:112, on a = acc / ws)
-                        const T y = (T)(x0[u] * iws);
-                        rv[v] = y;
-                        pv[v] = y;
-                        wrote_r = true;
-                    } else {   // PI-Push tail: y0 = (w_ratio r) / ws = r / ws(q)  (push_engine.py:246)
-                        pv[v] = (T)((double)rv[v] * sm.ysc[s]);
-                    }
-                } else if (op_is_push(o)) {
-                    const bool init = o == OP_BSEL_INIT;
-                    const double r = init ? (u == sm.src[s] ? 1.0 : 0.0) : (double)rv[v];
-                    double th;
-                    if (op_is_fwd(o)) th = (sm.wsq[s] * iws) * sm.thc[s];  // (ws_q / ws_i)(eps_f / lam)
-                    else th = (o == OP_SEQ) ? 0.0 : sm.eps_b[s];
-                    const bool act = r > th;
-                    if (act) {
-                        pv[v] = (T)r;
-                        rv[v] = (T)0;
-                        a.EST[i + v] = (init ? 0.0 : a.EST[i + v]) + a.alpha * r;
-                        cnt[v] += 1;
-                        npu[v] += deg;
-                        wrote_r = true;
-                    } else if (init) {
-                        rv[v] = (T)r;
-                        a.EST[i + v] = 0.0;
-                        wrote_r = true;
-                    } else if (op_is_fwd(o)) {
-                        left[v] += (a.ws_u[u] * sm.iwsq[s]) * r;  // w_ratio r left behind this round
-                    }
-                } else {
-                    pv[v] = a.P[i + v];  // keep (power-iteration iterate / idle)
+            for (int k = 0; k < ELEM_UNR; k++) {
+                const int64_t t = t0 + k * stride;
+                if (t < total) {
+                    const int64_t u = t / TPN;
+                    VecIO<T, EV>::ld(a.R + u * B + j0, rv[k]);
+                    iwsk[k] = a.inv_ws_u[u];
+                    degk[k] = a.deg_u[u];
                 }
             }
-            VecIO<T, EV>::st(a.P + i, pv);
-            if (wrote_r) VecIO<T, EV>::st(a.R + i, rv);
+#pragma unroll
+            for (int k = 0; k < ELEM_UNR; k++) {
+                const int64_t t = t0 + k * stride;
+                if (t >= total) break;
+                const int64_t u = t / TPN;
+                const int64_t i = u * B + j0;
+                const double iws = iwsk[k];
+                T pv[EV];
+                bool act[EV], any_act = false, wrote_r = false;
+                double rr[EV];
+#pragma unroll
+                for (int v = 0; v < EV; v++) {
+                    const int s = j0 + v;
+                    const int o = op[v];
+                    pv[v] = (T)0;
+                    act[v] = false;
+                    rr[v] = 0.0;
+                    if (o == OP_PIENTRY || o == OP_PIENTRY0) {
+                        const double *x0 = (a.x0 && sm.qidx[s] >= 0) ? a.x0 + (int64_t)sm.qidx[s] * a.n_u : nullptr;
+                        if (x0) {  // raw power iteration: y0 = start / ws  (push_engine.py:112, on a = acc / ws)
+                            const T y = (T)(x0[u] * iws);
+                            rv[k][v] = y;
+                            pv[v] = y;
+                            wrote_r = true;
+                        } else {   // PI-Push tail: y0 = (w_ratio r) / ws = r / ws(q)  (push_engine.py:246)
+                            pv[v] = (T)((double)rv[k][v] * sm.ysc[s]);
+                        }
+                    } else if (op_is_push(o)) {
+                        const bool init = o == OP_BSEL_INIT;
+                        const double r = init ? (u == sm.src[s] ? 1.0 : 0.0) : (double)rv[k][v];
+                        double th;
+                        if (op_is_fwd(o)) th = (sm.wsq[s] * iws) * sm.thc[s];  // (ws_q / ws_i)(eps_f / lam)
+                        else th = (o == OP_SEQ) ? 0.0 : sm.eps_b[s];
+                        rr[v] = r;
+                        if (r > th) {
+                            act[v] = true;
+                            any_act = true;
+                            pv[v] = (T)r;
+                            rv[k][v] = (T)0;
+                            cnt[v] += 1;
+                            npu[v] += degk[k];
+                            wrote_r = true;
+                        } else if (init) {
+                            rv[k][v] = (T)r;
+                            wrote_r = true;
+                        } else if (op_is_fwd(o)) {
+                            left[v] += (a.ws_u[u] * sm.iwsq[s]) * r;  // w_ratio r left behind this round
+                        }
+                    } else {
+                        pv[v] = a.P[i + v];  // keep (power-iteration iterate / idle)
+                    }
+                }
+                if (any_act || init_any) {  // est += alpha r on the pushed slots (ledger reset on init)
+                    double ev[EV];
+                    VecIO<double, EV>::ld(a.EST + i, ev);
+#pragma unroll
+                    for (int v = 0; v < EV; v++) {
+                        const bool init = op[v] == OP_BSEL_INIT;
+                        if (init) ev[v] = 0.0;
+                        if (act[v]) ev[v] += a.alpha * rr[v];
+                    }
+                    VecIO<double, EV>::st(a.EST + i, ev);
+                }
+                VecIO<T, EV>::st(a.P + i, pv);
+                if (wrote_r) VecIO<T, EV>::st(a.R + i, rv[k]);
+            }
         }
     }
 #pragma unroll
@@ -328,37 +361,52 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_combine(ElemArgs<T> a) {
     }
     if (any_work) {
         const int64_t total = a.n_u * TPN;
-        for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-             t += (int64_t)gridDim.x * blockDim.x) {
-            const int64_t u = t / TPN;
-            const int64_t i = u * B + j0;
-            T rv[EV], yv[EV];
-            VecIO<T, EV>::ld(a.R + i, rv);
-            VecIO<T, EV>::ld(a.Y + i, yv);
-            const double ws = a.ws_u[u], iws = a.inv_ws_u[u];
-            bool wrote_r = false;
+        const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+        for (int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t0 < total; t0 += ELEM_UNR * stride) {
+            T rv[ELEM_UNR][EV], yv[ELEM_UNR][EV];
+            double wsk[ELEM_UNR], iwsk[ELEM_UNR];
 #pragma unroll
-            for (int v = 0; v < EV; v++) {
-                const int s = j0 + v;
-                const int o = op[v];
-                if (op_is_push(o) || o == OP_MEASURE) {
-                    T nr = rv[v];
-                    if (o != OP_MEASURE) {
-                        nr = (T)((double)rv[v] + (double)yv[v]);
-                        rv[v] = nr;
-                        wrote_r = true;
-                    }
-                    const double r = (double)nr;
-                    sum[v] += r;
-                    wsum[v] += (ws * sm.iwsq[s]) * r;  // w_ratio * r  (push_engine.py:220,237)
-                    const double th =
-                        (op_is_fwd(o) || o == OP_MEASURE) ? (sm.wsq[s] * iws) * sm.thc[s] : sm.eps_b[s];
-                    any[v] |= r > th;
-                } else if (o == OP_PIENTRY || o == OP_PI) {
-                    a.P[i + v] = (T)((double)rv[v] * sm.ysc[s] + (double)yv[v]);
+            for (int k = 0; k < ELEM_UNR; k++) {
+                const int64_t t = t0 + k * stride;
+                if (t < total) {
+                    const int64_t u = t / TPN;
+                    VecIO<T, EV>::ld(a.R + u * B + j0, rv[k]);
+                    VecIO<T, EV>::ld(a.Y + u * B + j0, yv[k]);
+                    wsk[k] = a.ws_u[u];
+                    iwsk[k] = a.inv_ws_u[u];
                 }
             }
-            if (wrote_r) VecIO<T, EV>::st(a.R + i, rv);
+#pragma unroll
+            for (int k = 0; k < ELEM_UNR; k++) {
+                const int64_t t = t0 + k * stride;
+                if (t >= total) break;
+                const int64_t u = t / TPN;
+                const int64_t i = u * B + j0;
+                const double ws = wsk[k], iws = iwsk[k];
+                bool wrote_r = false;
+#pragma unroll
+                for (int v = 0; v < EV; v++) {
+                    const int s = j0 + v;
+                    const int o = op[v];
+                    if (op_is_push(o) || o == OP_MEASURE) {
+                        T nr = rv[k][v];
+                        if (o != OP_MEASURE) {
+                            nr = (T)((double)rv[k][v] + (double)yv[k][v]);
+                            rv[k][v] = nr;
+                            wrote_r = true;
+                        }
+                        const double r = (double)nr;
+                        sum[v] += r;
+                        wsum[v] += (ws * sm.iwsq[s]) * r;  // w_ratio * r  (push_engine.py:220,237)
+                        const double th =
+                            (op_is_fwd(o) || o == OP_MEASURE) ? (sm.wsq[s] * iws) * sm.thc[s] : sm.eps_b[s];
+                        any[v] |= r > th;
+                    } else if (o == OP_PIENTRY || o == OP_PI) {
+                        a.P[i + v] = (T)((double)rv[k][v] * sm.ysc[s] + (double)yv[k][v]);
+                    }
+                }
+                if (wrote_r) VecIO<T, EV>::st(a.R + i, rv[k]);
+            }
         }
     }
 #pragma unroll
