@@ -220,14 +220,46 @@ struct Engine final : EngineBase {
     // k_pull_sw on both sides; fp64 (16 B per lane, S = 8) with k_pull and
     // half-warp workers on the long-row side.
     bool pull_sw = sizeof(T) == 4;
+    bool pull_tma = false;             // TMA gather4 pull (k_pull_tma), BH_PULL_TMA=1
+    CUtensorMap tmap_p{}, tmap_xv{};   // operands of the V pull (P) and the U pull (XV)
     using PullFn = void (*)(PullArgs<T>);
     template <int SIDE>
     PullFn sw_kernel() const {
         return k_pull_sw<B, T, SIDE>;
     }
 
+    // X as a [rows][B] tensor for tile::gather4 (box {B, 1}).
+    static void encode_rows_map(CUtensorMap *m, const T *base, int64_t rows) {
+        using EncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                      const cuuint64_t *, const cuuint32_t *, const cuuint32_t *,
+                                      CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                      CUtensorMapFloatOOBfill);
+        static EncodeFn encode = nullptr;
+        if (!encode) {
+            void *fn = nullptr;
+            cudaDriverEntryPointQueryResult q;
+            BH_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+            if (!fn || q != cudaDriverEntryPointSuccess) throw CudaError("cuTensorMapEncodeTiled unavailable");
+            encode = (EncodeFn)fn;
+        }
+        const cuuint64_t dims[2] = {(cuuint64_t)B, (cuuint64_t)rows};
+        const cuuint64_t strides[1] = {(cuuint64_t)B * sizeof(T)};
+        const cuuint32_t box[2] = {(cuuint32_t)B, 1};
+        const cuuint32_t estr[2] = {1, 1};
+        const CUresult r = encode(m, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                  2, (void *)base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    }
+
     void pull_kernel(int side, void **fn) const {
         if constexpr (WIDE) {
+            if (pull_tma) {
+                *fn = side == SIDE_V ? (void *)k_pull_tma<B, T, SIDE_V> : (void *)k_pull_tma<B, T, SIDE_U>;
+                return;
+            }
+
             const bool half = side == SIDE_V ? half_v : half_u;
             if (side == SIDE_V)
                 *fn = half ? (void *)k_pull_half<B, T, SIDE_V>
@@ -270,6 +302,13 @@ struct Engine final : EngineBase {
             half_v = WIDE && (h & 2);
         }
         if (const char *m = getenv("BH_PULL_SW")) pull_sw = atoi(m) != 0;
+        if (const char *m = getenv("BH_PULL_TMA")) pull_tma = WIDE && atoi(m) != 0;
+        if (pull_tma) {
+            half_u = half_v = false;
+            encode_rows_map(&tmap_p, P, nu);
+            encode_rows_map(&tmap_xv, XV, nv);
+            pull_smem = TmaPipe<B, T>::BLOCK_BYTES;
+        }
         for (int side = 0; side < 2; side++) {
             void *fn;
             pull_kernel(side, &fn);
@@ -403,6 +442,15 @@ struct Engine final : EngineBase {
     void launch_pull(int side, const PullArgs<T> &a, cudaStream_t st) {
         const int grid = side == SIDE_V ? plan_v.grid : plan_u.grid;
         if constexpr (WIDE) {
+            if (pull_tma) {
+                PullTmaArgs<T> ta;
+                ta.p = a;
+                ta.tmap = side == SIDE_V ? tmap_p : tmap_xv;
+                if (side == SIDE_V) launch_pdl(k_pull_tma<B, T, SIDE_V>, grid, PULL_THREADS, pull_smem, st, ta);
+                else launch_pdl(k_pull_tma<B, T, SIDE_U>, grid, PULL_THREADS, pull_smem, st, ta);
+                return;
+            }
+
             const bool half = side == SIDE_V ? half_v : half_u;
             if (side == SIDE_V) {
                 if (half) launch_pdl(k_pull_half<B, T, SIDE_V>, grid, PULL_THREADS, pull_smem, st, a);

@@ -26,6 +26,8 @@
 // through per-block partial rows summed in a fixed order: bitwise deterministic.
 #pragma once
 
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace bh {
@@ -954,6 +956,237 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) k_pull_sw(PullArgs<T> a) {
                 cw = col_at(base + 3 * S + lane);
                 vw = val_at(base + 3 * S + lane);
                 __syncwarp();
+            }
+            const CutCtx<T> cx{a.scratch, a.cut_count, a.cuts, a.Y, a.indptr, scale};
+            if (cutA >= 0) {
+                DVec<VEC> av;
+#pragma unroll
+                for (int v = 0; v < VEC; v++) av.v[v] = a.scratch[(int64_t)wk.part0 * B + slot0 + v];
+                const IVec<VEC> inc = pull_cut<B, T, VEC>(cx, wk.cut0, wk.part0, slot0, cmask, av);
+#pragma unroll
+                for (int v = 0; v < VEC; v++) np_cut[v] += inc.v[v];
+            }
+            if (cutB >= 0) {
+                DVec<VEC> av;
+#pragma unroll
+                for (int v = 0; v < VEC; v++) av.v[v] = a.scratch[(int64_t)wk.part1 * B + slot0 + v];
+                const IVec<VEC> inc = pull_cut<B, T, VEC>(cx, wk.cut1, wk.part1, slot0, cmask, av);
+#pragma unroll
+                for (int v = 0; v < VEC; v++) np_cut[v] += inc.v[v];
+            }
+        }
+    }
+    if constexpr (SIDE == SIDE_V) {
+        if (gw < a.n_warps)
+#pragma unroll
+            for (int v = 0; v < VEC; v++) a.np_v[(int64_t)(slot0 + v) * a.n_warps + gw] = (int64_t)np[v] + np_cut[v];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// TMA-gather pull (sm_100a): the operand rows are fetched by the tensor memory
+// accelerator with cp.async.bulk.tensor.2d ... tile::gather4 (four rows of
+// B * sizeof(T) bytes per instruction, issued by one lane) into a per-warp
+// ring of NS four-row stages completed on mbarriers, so 4 * NS rows per warp
+// are in flight without holding registers; the lanes read their VEC slots of
+// each row back from shared memory.  Same edge ranges, row emit, cut rows and
+// n_p accounting as k_pull_sw.
+template <typename T>
+struct PullTmaArgs {
+    PullArgs<T> p;
+    CUtensorMap tmap;  // X as a [n_rows][B] tensor, box {B, 1}
+};
+
+template <int B, typename T>
+struct TmaPipe {
+    static constexpr int ROW = B * (int)sizeof(T);
+    static constexpr int NS = ROW <= 256 ? 8 : 4;         // stages (4 rows each) per warp
+    static constexpr int STAGE = 4 * ROW;
+    // per warp, rounded to 128 B so every warp's stages are TMA-aligned
+    static constexpr int WARP_BYTES = (NS * STAGE + 3 * 32 * (int)sizeof(EdgeCV<T>) + 64 * 4 + NS * 8 + 127) / 128 * 128;
+    static constexpr int BLOCK_BYTES = PULL_WARPS * WARP_BYTES + 128;
+};
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t ok = 0;
+    while (!ok) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *map, uint32_t bar, int r0, int r1,
+                                            int r2, int r3) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
+        "l"(map), "r"(bar), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+        : "memory");
+}
+
+template <int B, typename T, int SIDE>
+__global__ void __launch_bounds__(PULL_THREADS) k_pull_tma(const __grid_constant__ PullTmaArgs<T> ta) {
+    pdl_begin();
+    const PullArgs<T> &a = ta.p;
+    if (*a.active == 0) return;
+    using TP = TmaPipe<B, T>;
+    constexpr int VEC = B / 32, NS = TP::NS, ROW = TP::ROW, STAGE = TP::STAGE;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    unsigned char *sbase = (unsigned char *)(((uintptr_t)smem_raw + 127) & ~(uintptr_t)127);
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int gw = blockIdx.x * PULL_WARPS + warp;
+    const int slot0 = lane * VEC;
+    // per-warp carve: stages | windows (3 x 32 (col, val)) | row-end ring | barriers
+    unsigned char *wbase = sbase + warp * TP::WARP_BYTES;
+    unsigned char *stages = wbase;
+    EdgeCV<T>(*win)[32] = reinterpret_cast<EdgeCV<T>(*)[32]>(wbase + NS * STAGE);
+    int32_t *re = reinterpret_cast<int32_t *>(wbase + NS * STAGE + 3 * 32 * sizeof(EdgeCV<T>));
+    uint64_t *bars = reinterpret_cast<uint64_t *>(wbase + NS * STAGE + 3 * 32 * sizeof(EdgeCV<T>) + 64 * 4);
+    const uint32_t st0 = smem_u32(stages), bar0 = smem_u32(bars);
+
+    uint32_t cmask = 0;
+    if constexpr (SIDE == SIDE_V) {
+#pragma unroll
+        for (int v = 0; v < VEC; v++) cmask |= (op_is_push(a.slots[slot0 + v].op) ? 1u : 0u) << v;
+    }
+    const double scale = SIDE == SIDE_V ? a.one_minus_alpha : 1.0;
+    int32_t np[VEC];
+    int64_t np_cut[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; v++) {
+        np[v] = 0;
+        np_cut[v] = 0;
+    }
+    if (gw < a.n_warps) {
+        const WarpWork wk = a.work[gw];
+        const int64_t e0 = wk.e0;
+        const int n = (int)(wk.e1 - e0);
+        if (n > 0) {
+            const int32_t *cols = a.indices + e0;
+            const T *vals = a.vals + e0;
+            T *Y0 = a.Y + (int64_t)wk.r0 * B + slot0;
+            const int64_t *rp = a.indptr + wk.r0;
+            const int64_t nrow_left = a.n_rows - wk.r0;
+            const int cutA = wk.cut0 >= 0 ? 0 : -1;
+            const int cutB = wk.cut1 >= 0 ? (int)(a.cuts[wk.cut1].row - wk.r0) : -1;
+            auto col_at = [&](int o) { return o < n ? __ldg(cols + o) : 0; };
+            auto val_at = [&](int o) { return o < n ? __ldg(vals + o) : (T)0; };
+            auto rend_at = [&](int i) {
+                const int64_t r = i + 1 <= nrow_left ? __ldg(rp + i + 1) : __ldg(rp + nrow_left);
+                return (int)imin64(r - e0, (int64_t)n);
+            };
+            const int ngroups = (n + 3) >> 2;
+            // windows 0, 1 resident (slots 0, 1); window 2 in registers
+            win[0][lane] = EdgeCV<T>{col_at(lane), val_at(lane)};
+            win[1][lane] = EdgeCV<T>{col_at(32 + lane), val_at(32 + lane)};
+            int cw = col_at(64 + lane);
+            T vw = val_at(64 + lane);
+            re[lane] = rend_at(lane);
+            re[32 + lane] = rend_at(32 + lane);
+            if (lane < NS) mbar_init(bar0 + 8 * lane, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            __syncwarp();
+            auto issue = [&](int g) {  // group g = edges 4g .. 4g+3 -> stage g % NS (lane 0)
+                const EdgeCV<T> *e = &win[(g >> 3) % 3][(g & 7) * 4];
+                const uint32_t bar = bar0 + 8 * (g % NS);
+                mbar_expect_tx(bar, STAGE);
+                tma_gather4(st0 + (g % NS) * STAGE, &ta.tmap, bar, e[0].c, e[1].c, e[2].c, e[3].c);
+            };
+            if (lane == 0)
+                for (int g = 0; g < NS && g < ngroups; g++) issue(g);
+            int rw = 0, lr = 0;
+            int rstart = (int)(__ldg(rp) - e0);
+            int rend = re[0];
+            double acc[VEC];
+            T accs[VEC];
+#pragma unroll
+            for (int v = 0; v < VEC; v++) {
+                acc[v] = 0.0;
+                accs[v] = (T)0;
+            }
+            for (int g = 0; g < ngroups; g++) {
+                const int base = g << 2;
+                const EdgeCV<T> *ecur = &win[(g >> 3) % 3][(g & 7) * 4];
+                T w4[4];
+#pragma unroll
+                for (int t = 0; t < 4; t++) w4[t] = ecur[t].v;
+                mbar_wait(bar0 + 8 * (g % NS), (uint32_t)((g / NS) & 1));
+                const unsigned char *stg = stages + (g % NS) * STAGE + slot0 * sizeof(T);
+                int d = rend - base - 1;
+#pragma unroll
+                for (int t = 0; t < 4; t++) {
+                    T x[VEC];
+                    VecIO<T, VEC>::ld(reinterpret_cast<const T *>(stg + t * ROW), x);
+                    if constexpr (sizeof(T) == 8) {
+#pragma unroll
+                        for (int v = 0; v < VEC; v++) acc[v] = fma((double)w4[t], (double)x[v], acc[v]);
+                    } else {
+#pragma unroll
+                        for (int v = 0; v < VEC; v++) accs[v] = fmaf(w4[t], x[v], accs[v]);
+                    }
+                    if (d == t) {  // row emit
+                        if constexpr (sizeof(T) == 4) {
+#pragma unroll
+                            for (int v = 0; v < VEC; v++) {
+                                acc[v] += (double)accs[v];
+                                accs[v] = (T)0;
+                            }
+                        }
+                        if (lr == cutA || lr == cutB) {
+                            double *dst = a.scratch + (int64_t)(lr == cutA ? wk.part0 : wk.part1) * B + slot0;
+#pragma unroll
+                            for (int v = 0; v < VEC; v++) dst[v] = acc[v];
+                        } else {
+                            T out[VEC];
+#pragma unroll
+                            for (int v = 0; v < VEC; v++) {
+                                out[v] = (T)(scale * acc[v]);
+                                if constexpr (SIDE == SIDE_V)
+                                    np[v] += (((cmask >> v) & 1u) && out[v] > (T)0) ? rend - rstart : 0;
+                            }
+                            VecIO<T, VEC>::st(Y0 + (int64_t)lr * B, out);
+                        }
+#pragma unroll
+                        for (int v = 0; v < VEC; v++) acc[v] = 0.0;
+                        lr++;
+                        rstart = rend;
+                        rend = re[lr & 63];
+                        d = rend - base - 1;
+                    }
+                }
+                if constexpr (sizeof(T) == 4) {  // bound the fp32 partial to 16 terms
+                    if ((g & 3) == 3) {
+#pragma unroll
+                        for (int v = 0; v < VEC; v++) {
+                            acc[v] += (double)accs[v];
+                            accs[v] = (T)0;
+                        }
+                    }
+                }
+                __syncwarp();  // stage g % NS and the row ends before lr are consumed
+                if ((g & 7) == 7) {
+                    // window g/8 done: window g/8 + 2 (in registers) takes the slot of
+                    // window g/8 - 1; prefetch window g/8 + 3
+                    const int wnext = (g >> 3) + 2;
+                    win[wnext % 3][lane] = EdgeCV<T>{cw, vw};
+                    cw = col_at(32 * (wnext + 1) + lane);
+                    vw = val_at(32 * (wnext + 1) + lane);
+                }
+                if (lr - rw >= 32) {
+                    re[(rw + 64 + lane) & 63] = rend_at(rw + 64 + lane);
+                    rw += 32;
+                }
+                __syncwarp();
+                if (lane == 0 && g + NS < ngroups) issue(g + NS);
             }
             const CutCtx<T> cx{a.scratch, a.cut_count, a.cuts, a.Y, a.indptr, scale};
             if (cutA >= 0) {

@@ -252,6 +252,34 @@ def test_scaled_configs_fp32(name):
         topk_equal_up_to_ties(res.topk_index[i], res.topk_score[i], exp, ref, RTOL32, float(d["eps"]))
 
 
+@pytest.mark.parametrize("variant", [
+    {"BH_PULL_SW": "0", "BH_PULL_HALF": "0"},   # lane-register windows (k_pull)
+    {"BH_PULL_SW": "0", "BH_PULL_HALF": "3"},   # half-warp workers (k_pull_half)
+    {"BH_PULL_SW": "1", "BH_PULL_HALF": "0"},   # shared-memory windows (k_pull_sw)
+    {"BH_PULL_TMA": "1"},                        # TMA gather4 ring (k_pull_tma)
+])
+def test_every_pull_kernel_variant(variant, monkeypatch):
+    """Each pull implementation (chosen when the engine is built) reproduces
+    the golden fp64 scores / traces and the fp32 top-k on c2s."""
+    for k, v in variant.items():
+        monkeypatch.setenv(k, v)
+    d = load("c2s")
+    g = bh.BipartiteGraph.from_bytes(config_graph("c2s").to_bytes())  # fresh graph -> fresh engines
+    meta = meta_for(g, 0.15)
+    srcs = d["sources"][:6]
+    ties = np.array([tie_skip_from(t) for t in d["ties"][:6]], dtype=np.int32)
+    k = int(d["k"])
+    r64 = bh.bhpp_query_batch(g, meta, srcs, float(d["eps"]), k=k, dtype="fp64", return_scores=True, tie_skip=ties)
+    r32 = bh.bhpp_query_batch(g, meta, srcs, float(d["eps"]), k=k, dtype="fp32", tie_skip=ties)
+    for i in range(len(srcs)):
+        np.testing.assert_allclose(r64.scores[i], d["scores"][i], atol=ATOL64, rtol=0)
+        back, fwd, gamma = split_traces(d["traces"][i])
+        assert_traces(r64.trace_dicts(i), back, fwd, gamma)
+        ref, exp = d["scores"][i], d["topk"][i]
+        np.testing.assert_allclose(r32.topk_score[i], ref[exp], rtol=RTOL32, atol=float(d["eps"]))
+        topk_equal_up_to_ties(r32.topk_index[i], r32.topk_score[i], exp, ref, RTOL32, float(d["eps"]))
+
+
 # -- determinism, drop-in semantics, errors -------------------------------------
 
 def test_runs_are_bitwise_deterministic():
