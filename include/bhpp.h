@@ -84,8 +84,11 @@ typedef struct bh_query_params {
     int32_t want_scores;   /* also write the full score vector per query         */
     int32_t slots;         /* query-block width B (0 = automatic)                */
     int32_t on_device;     /* 1: all pointer arguments are device pointers       */
-    int32_t reserved;
+    int32_t flags;         /* BH_QUERY_ASYNC: with on_device, return after the  */
+                           /* batch is enqueued; bh_query_wait() completes it    */
 } bh_query_params;
+
+#define BH_QUERY_ASYNC 1
 
 typedef struct bh_graph_info {
     int64_t n_u, n_v, n_e;
@@ -132,6 +135,11 @@ int bh_push_run(bh_graph *g, int32_t job, int32_t source, double alpha, double l
 int bh_power_iteration(bh_graph *g, const double *start, int64_t n_vec, double alpha, int32_t t,
                        double *out);
 
+/* Completes a batch submitted with BH_QUERY_ASYNC on this graph: waits for
+ * its stream, checks termination, updates bh_last_run_stats.  No other call
+ * may use the graph in between. */
+int bh_query_wait(bh_graph *g);
+
 /* ---- top-k of an arbitrary score vector (bhpp_query.py:206-218) ---------- */
 /* (score desc, index asc); exclude < 0 keeps every index.  Returns count via
  * *out_count.  Host pointers. */
@@ -164,6 +172,11 @@ typedef struct bh_run_stats {
 /* on != 0: bracket every round's kernels with CUDA events on the launch stream
  * (process-wide switch; costs one event record per kernel group). */
 int bh_set_profiling(int32_t on);
+/* Measurement gate: enqueue on `stream` a one-thread kernel that spins until
+ * *flag (host-mapped pinned memory) becomes nonzero, so a batch can be fully
+ * enqueued before the device starts it and device timing excludes host
+ * submission gaps. */
+int bh_stream_gate(void *stream, const int32_t *flag);
 int bh_last_run_stats(bh_graph *g, bh_run_stats *out);
 
 /* ---- misc ----------------------------------------------------------------- */

@@ -29,8 +29,9 @@ PHASES = ("selective", "sequential", "forward-selective")
 EXPORTS = (
     "bh_graph_create", "bh_graph_destroy", "bh_graph_get_info", "bh_query_batch", "bh_push_run",
     "bh_power_iteration", "bh_topk", "bh_last_error", "bh_version", "bh_kernel_launches",
-    "bh_set_profiling", "bh_last_run_stats", "bh_csr_build",
+    "bh_set_profiling", "bh_last_run_stats", "bh_csr_build", "bh_query_wait", "bh_stream_gate",
 )
+QUERY_ASYNC = 1
 
 
 class Trace(C.Structure):
@@ -56,7 +57,7 @@ class QueryParams(C.Structure):
     _fields_ = [
         ("alpha", C.c_double), ("lam", C.c_double), ("eps_b", C.c_double), ("eps_f", C.c_double),
         ("k", C.c_int32), ("exclude_query", C.c_int32), ("want_scores", C.c_int32),
-        ("slots", C.c_int32), ("on_device", C.c_int32), ("reserved", C.c_int32),
+        ("slots", C.c_int32), ("on_device", C.c_int32), ("flags", C.c_int32),
     ]
 
 
@@ -119,6 +120,10 @@ def lib():
         L.bh_set_profiling.argtypes = [C.c_int32]
         L.bh_last_run_stats.restype = C.c_int
         L.bh_last_run_stats.argtypes = [P, C.POINTER(RunStats)]
+        L.bh_query_wait.restype = C.c_int
+        L.bh_query_wait.argtypes = [P]
+        L.bh_stream_gate.restype = C.c_int
+        L.bh_stream_gate.argtypes = [P, P]
         L.bh_csr_build.restype = C.c_int
         L.bh_csr_build.argtypes = [C.c_int64] * 3 + [P] * 11 + [C.c_int32]
         _lib = L

@@ -243,19 +243,25 @@ def bhpp_query_batch(g, meta: IndexMeta, sources, epsilon: float, k: int | None 
 def query_batch_device(dg, meta: IndexMeta, eps_b: float, eps_f: float, sources_ptr: int, n_q: int, k: int,
                        topk_idx_ptr: int, topk_score_ptr: int, trace_ptr: int, scores_ptr: int = 0,
                        exclude_query: bool = False, slots: int | None = None, tie_ptr: int = 0,
-                       stream: int | None = None) -> None:
+                       stream: int | None = None, async_: bool = False) -> None:
     """bh_query_batch with every buffer already resident on the device (raw
     device pointers, e.g. torch ``data_ptr()``); nothing crosses PCIe.  The
-    caller owns the stream ordering (``stream`` = cudaStream_t handle)."""
+    caller owns the stream ordering (``stream`` = cudaStream_t handle).
+    ``async_``: return once enqueued; ``query_wait(dg)`` completes the batch."""
     import ctypes as C
 
     prm = _capi.QueryParams(alpha=meta.alpha, lam=meta.lam, eps_b=eps_b, eps_f=eps_f, k=int(k),
                             exclude_query=int(bool(exclude_query)), want_scores=int(bool(scores_ptr)),
-                            slots=int(slots or 0), on_device=1)
+                            slots=int(slots or 0), on_device=1, flags=_capi.QUERY_ASYNC if async_ else 0)
     vp = lambda x: C.c_void_p(x) if x else None  # noqa: E731
     _capi.check(_capi.lib().bh_query_batch(dg.h, C.byref(prm), vp(sources_ptr), int(n_q), vp(tie_ptr),
                                            vp(topk_idx_ptr), vp(topk_score_ptr), vp(trace_ptr), vp(scores_ptr),
                                            vp(stream)))
+
+
+def query_wait(dg) -> None:
+    """Complete a batch submitted with ``query_batch_device(..., async_=True)``."""
+    _capi.check(_capi.lib().bh_query_wait(dg.h))
 
 
 def topk(result: QueryResult, k: int, exclude_query: bool = False) -> list[tuple[str, float]]:

@@ -95,6 +95,7 @@ struct RunSpec {
     double *scores = nullptr;
     bh_round_hook hook = nullptr;
     void *hook_user = nullptr;
+    bool async = false;  // graph path only: enqueue and return (finish() completes)
 };
 
 static std::atomic<int> g_profiling{0};
@@ -103,6 +104,7 @@ struct EngineBase {
     virtual ~EngineBase() = default;
     bh_run_stats stats{};
     virtual void run(const RunSpec &rs, cudaStream_t st) = 0;
+    virtual void finish() = 0;  // completes an async run
     virtual void read_ledger(int s, double *r_u_dev, double *est_dev, cudaStream_t st) = 0;
     virtual void slot_state(int s, Slot *out, cudaStream_t st) = 0;
     int nslots = 0;
@@ -635,11 +637,8 @@ struct Engine final : EngineBase {
             ensure_graph(rs, ca, fa);
             BH_CUDA(cudaGraphLaunch(graph_exec, st));
             BH_CUDA(cudaMemcpyAsync(h_ctl, ctl, sizeof(Control), cudaMemcpyDeviceToHost, st));
-            BH_CUDA(cudaStreamSynchronize(st));
-            if (h_ctl->error) throw CudaError("query batch did not terminate");
-            stats.rounds = h_ctl->rounds_active;
-            stats.launches += 6 * (int64_t)h_ctl->rounds_active;
-            count_launch((int)(6 * h_ctl->rounds_active));
+            pending = st;
+            if (!rs.async) finish();
             return;
         }
         int32_t last_seq = 0;
@@ -678,6 +677,19 @@ struct Engine final : EngineBase {
         throw CudaError("query batch did not terminate");
     }
 
+    cudaStream_t pending = nullptr;
+
+    void finish() override {
+        if (!pending) return;
+        cudaStream_t st = pending;
+        pending = nullptr;
+        BH_CUDA(cudaStreamSynchronize(st));
+        if (h_ctl->error) throw CudaError("query batch did not terminate");
+        stats.rounds = h_ctl->rounds_active;
+        stats.launches += 6 * (int64_t)h_ctl->rounds_active;
+        count_launch((int)(6 * h_ctl->rounds_active));
+    }
+
     void read_ledger(int s, double *r_dev, double *est_dev, cudaStream_t st) override {
         k_col_get<T><<<grid1d(g->n_u), 256, 0, st>>>(R, B, s, g->n_u, r_dev);
         k_col_get<double><<<grid1d(g->n_u), 256, 0, st>>>(EST, B, s, g->n_u, est_dev);
@@ -695,6 +707,7 @@ struct Engine final : EngineBase {
 struct EngineCache {
     std::map<int, std::unique_ptr<EngineBase>> by_b;
     EngineBase *last = nullptr;
+    EngineBase *pending = nullptr;  // engine of an un-finished BH_QUERY_ASYNC batch
     cudaStream_t stream = nullptr;
     // host-call staging buffers
     int32_t *d_src = nullptr, *d_tie = nullptr;
@@ -799,6 +812,19 @@ static int guarded(F &&f) {
     }
 }
 
+// bh_stream_gate: hold the stream until the host sets *flag (at most ~5 s, so
+// a caller that synchronises on the gated stream before releasing it stalls
+// instead of hanging).
+__global__ void k_gate(const int32_t *flag) {
+    uint64_t t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (*(volatile const int32_t *)flag == 0) {
+        __nanosleep(256);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 5000000000ull) break;
+    }
+}
+
 extern "C" {
 
 const char *bh_last_error(void) { return t_err.c_str(); }
@@ -822,6 +848,27 @@ int bh_csr_build(int64_t n_u, int64_t n_v, int64_t n_e, const int64_t *edge_u, c
         return BH_EDUP;
     }
     return rc;
+}
+
+int bh_query_wait(bh_graph *g) {
+    return guarded([&] {
+        if (!g) throw InvalidArg("null argument");
+        std::lock_guard<std::mutex> lock(g->mu);
+        BH_CUDA(cudaSetDevice(g->device));
+        EngineCache &c = cache_of(g);
+        EngineBase *e = c.pending;
+        c.pending = nullptr;
+        if (e) e->finish();
+    });
+}
+
+int bh_stream_gate(void *stream, const int32_t *flag) {
+    return guarded([&] {
+        if (!flag) throw InvalidArg("null argument");
+        k_gate<<<1, 1, 0, (cudaStream_t)stream>>>(flag);
+        count_launch();
+        BH_CUDA(cudaGetLastError());
+    });
 }
 
 int bh_set_profiling(int32_t on) {
@@ -887,6 +934,11 @@ int bh_query_batch(bh_graph *g, const bh_query_params *p, const int32_t *sources
         std::lock_guard<std::mutex> lock(g->mu);
         BH_CUDA(cudaSetDevice(g->device));
         EngineCache &c = cache_of(g);
+        if (c.pending) {  // an async batch not yet waited for: complete it first
+            EngineBase *e0 = c.pending;
+            c.pending = nullptr;
+            e0->finish();
+        }
         cudaStream_t st = stream ? (cudaStream_t)stream : c.stream;
         const int B = p->slots > 0 ? p->slots : auto_slots(g, n_q);
         EngineBase &e = engine_for(g, B);
@@ -902,6 +954,8 @@ int bh_query_batch(bh_graph *g, const bh_query_params *p, const int32_t *sources
         rs.exclude = p->exclude_query;
         rs.want_scores = p->want_scores && scores;
         if (p->on_device) {
+            rs.async = (p->flags & BH_QUERY_ASYNC) != 0;
+            c.pending = rs.async ? &e : nullptr;
             rs.sources = sources;
             rs.tie = tie_skip;
             rs.topk_idx = topk_idx;
