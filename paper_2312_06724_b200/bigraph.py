@@ -216,6 +216,59 @@ class BipartiteGraph:
         except KeyError:
             raise DataError(f"unknown U-side label: {label!r}") from None
 
+    @cached_property
+    def _v_index(self):
+        return {lab: i for i, lab in enumerate(self.v_labels)}
+
+    def v_id(self, label) -> int:
+        if isinstance(self.v_labels, IndexLabels):
+            i = self.v_labels.index_of(label)
+            if i is not None:
+                return i
+            raise DataError(f"unknown V-side label: {label!r}")
+        try:
+            return self._v_index[label]
+        except KeyError:
+            raise DataError(f"unknown V-side label: {label!r}") from None
+
+    # -- normalised operators (bigraph.py:148-188), host-side scipy views ------
+    # The device store keeps only the two prescaled value arrays (graph_store.cu);
+    # these are for host callers that use the reference's operator attributes.
+
+    @cached_property
+    def u_step(self):
+        """Row-stochastic |U| x |V| CSR: w(u, v) / ws(u)."""
+        import scipy.sparse as sp
+
+        data = self.u_weights / np.repeat(self.ws_u, self.deg_u)
+        return sp.csr_matrix((data, self.u_indices.astype(np.int64), self.u_indptr), shape=(self.u_count, self.v_count))
+
+    @cached_property
+    def v_step(self):
+        """Row-stochastic |V| x |U| CSR: w(u, v) / ws(v)."""
+        import scipy.sparse as sp
+
+        data = self.v_weights / np.repeat(self.ws_v, self.deg_v)
+        return sp.csr_matrix((data, self.v_indices.astype(np.int64), self.v_indptr), shape=(self.v_count, self.u_count))
+
+    @cached_property
+    def u_step_t(self):
+        return self.u_step.T.tocsr()
+
+    @cached_property
+    def v_step_t(self):
+        return self.v_step.T.tocsr()
+
+    @cached_property
+    def recv_uv(self) -> np.ndarray:
+        """Per U-CSR slot: w(u, v) / ws(v)."""
+        return _frozen(self.u_weights / self.ws_v[self.u_indices])
+
+    @cached_property
+    def recv_vu(self) -> np.ndarray:
+        """Per V-CSR slot: w(u, v) / ws(u)."""
+        return _frozen(self.v_weights / self.ws_u[self.v_indices])
+
     # -- serialisation (BPGR v1, bigraph.py:192-251) ---------------------------
 
     def _label_blob(self, labels) -> bytes:

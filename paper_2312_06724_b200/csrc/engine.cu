@@ -224,9 +224,16 @@ struct Engine final : EngineBase {
     bool pull_sw = sizeof(T) == 4;
     bool pull_tma = false;             // TMA gather4 pull (k_pull_tma), BH_PULL_TMA=1
     CUtensorMap tmap_p{}, tmap_xv{};   // operands of the V pull (P) and the U pull (XV)
+    // K1a fused into the U pull's row emit (k_pull_sw<..., SIDE_U, true>): no Y
+    // round trip, no combine launch; BH_FUSE_COMBINE=0 restores the separate K1a.
+    bool fuse_combine = false;
+
     using PullFn = void (*)(PullArgs<T>);
     template <int SIDE>
     PullFn sw_kernel() const {
+        if constexpr (SIDE == SIDE_U) {
+            if (fuse_combine) return k_pull_sw<B, T, SIDE_U, true>;
+        }
         return k_pull_sw<B, T, SIDE>;
     }
 
@@ -305,6 +312,8 @@ struct Engine final : EngineBase {
         }
         if (const char *m = getenv("BH_PULL_SW")) pull_sw = atoi(m) != 0;
         if (const char *m = getenv("BH_PULL_TMA")) pull_tma = WIDE && atoi(m) != 0;
+        fuse_combine = WIDE && pull_sw && !pull_tma && !half_u;
+        if (const char *m = getenv("BH_FUSE_COMBINE")) fuse_combine = fuse_combine && atoi(m) != 0;
         if (pull_tma) {
             half_u = half_v = false;
             encode_rows_map(&tmap_p, P, nu);
@@ -341,15 +350,15 @@ struct Engine final : EngineBase {
         grid_k5 = (int)std::min<int64_t>((int64_t)n_chunks * std::min(B, 8), 8 * sms);
         part.rows_k1 = grid_elem;
         part.rows_k2 = half_v ? (plan_v.n_warps + 1) / 2 : plan_v.n_warps;
-        part.rows_k3 = grid_elem;
+        part.rows_k3 = fuse_combine ? plan_u.n_warps + plan_u.n_cuts : grid_elem;
         part.cnt = dalloc<int64_t>((size_t)grid_elem * B);
         part.np_u = dalloc<int64_t>((size_t)grid_elem * B);
         part.lmass = dalloc<double>((size_t)grid_elem * B);
         BH_CUDA(cudaMemset(part.lmass, 0, (size_t)grid_elem * B * sizeof(double)));
         part.np_v = dalloc<int64_t>((size_t)plan_v.n_warps * B);
-        part.any = dalloc<int32_t>((size_t)grid_elem * B);
-        part.sum = dalloc<double>((size_t)grid_elem * B);
-        part.wsum = dalloc<double>((size_t)grid_elem * B);
+        part.any = dalloc<int32_t>((size_t)part.rows_k3 * B);
+        part.sum = dalloc<double>((size_t)part.rows_k3 * B);
+        part.wsum = dalloc<double>((size_t)part.rows_k3 * B);
         BH_CUDA(cudaMemset(part.np_v, 0, (size_t)plan_v.n_warps * B * sizeof(int64_t)));
         BH_CUDA(cudaMemset(part.cnt, 0, (size_t)grid_elem * B * sizeof(int64_t)));
         BH_CUDA(cudaMemset(part.np_u, 0, (size_t)grid_elem * B * sizeof(int64_t)));
@@ -438,6 +447,16 @@ struct Engine final : EngineBase {
         a.np_v = part.np_v;
         a.one_minus_alpha = one_minus_alpha;
         a.dbg = side == SIDE_V ? dbg_v : dbg_u;
+        if (side == SIDE_U && fuse_combine) {
+            a.R = R;
+            a.Pn = P;
+            a.ws_u = g->ws_u;
+            a.inv_ws_u = g->inv_ws_u;
+            a.p_any = part.any;
+            a.p_sum = part.sum;
+            a.p_wsum = part.wsum;
+            a.part_rows = part.rows_k3;
+        }
         return a;
     }
 
@@ -493,16 +512,18 @@ struct Engine final : EngineBase {
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 2), st));
         launch_pull(SIDE_U, pull_args(SIDE_U, 1.0 - rs.alpha), st);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 3), st));
-        launch_pdl(k_combine<B, T>, grid_elem, ELEM_THREADS, 0, st, ea);
+        if (!fuse_combine) launch_pdl(k_combine<B, T>, grid_elem, ELEM_THREADS, 0, st, ea);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 4), st));
         launch_pdl(k_control, B, CONTROL_THREADS, 0, st, ca);
         launch_pdl(k_finalize<T>, grid_k5, TOPK_THREADS, 0, st, fa);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 5), st));
-        const int launches = 6;
+        const int launches = launches_per_round();
         count_launch(launches);
         stats.launches += launches;
         BH_CUDA(cudaGetLastError());
     }
+
+    int launches_per_round() const { return fuse_combine ? 5 : 6; }
 
     void collect_profile(int64_t rounds) {
         double t[5] = {0, 0, 0, 0, 0};
@@ -557,7 +578,7 @@ struct Engine final : EngineBase {
         const int64_t launches0 = stats.launches;
         launch_round(rs, ca, fa, cap_stream, 0, false);
         stats.launches = launches0;
-        count_launch(-6);  // captured, not launched
+        count_launch(-launches_per_round());  // captured, not launched
         cudaGraph_t captured;
         BH_CUDA(cudaStreamEndCapture(cap_stream, &captured));
         BH_CUDA(cudaGraphInstantiate(&graph_exec, graph, 0));
@@ -686,8 +707,8 @@ struct Engine final : EngineBase {
         BH_CUDA(cudaStreamSynchronize(st));
         if (h_ctl->error) throw CudaError("query batch did not terminate");
         stats.rounds = h_ctl->rounds_active;
-        stats.launches += 6 * (int64_t)h_ctl->rounds_active;
-        count_launch((int)(6 * h_ctl->rounds_active));
+        stats.launches += launches_per_round() * (int64_t)h_ctl->rounds_active;
+        count_launch((int)(launches_per_round() * h_ctl->rounds_active));
     }
 
     void read_ledger(int s, double *r_dev, double *est_dev, cudaStream_t st) override {
@@ -760,12 +781,15 @@ static EngineBase *make_engine(bh_graph *g, int B) {
 }
 
 static int auto_slots(const bh_graph *g, int64_t n_q) {
-    int b = n_q <= 1 ? 1 : n_q <= 4 ? 4 : n_q <= 16 ? 16 : n_q <= 32 ? 32 : 64;
+    // 128 slots once the batch fills them: per-round cost grows sub-linearly in B
+    // (c5 on B200: 2189 q/s at 64 slots, 2625 at 128)
+    int b = n_q <= 1 ? 1 : n_q <= 4 ? 4 : n_q <= 16 ? 16 : n_q <= 32 ? 32 : n_q <= 64 ? 64 : 128;
     // keep the per-slot state within a fraction of device memory
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
         const int s = g->dtype == BH_DTYPE_F32 ? 4 : 8;
-        while (b > 1 && (double)b * (g->n_u * (2.0 * s + 16) + g->n_v * (double)s) > 0.6 * free_b) b /= 4;
+        while (b > 1 && (double)b * (g->n_u * (2.0 * s + 16) + g->n_v * (double)s) > 0.6 * free_b)
+            b = b == 128 ? 64 : b / 4;
         if (b == 2 || b == 8) b = b == 2 ? 1 : 4;
     }
     return b;

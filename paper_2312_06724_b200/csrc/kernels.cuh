@@ -17,16 +17,19 @@
 //
 // The pulls are gather-bound SpMMs: every edge reads one B-wide operand row
 // (B * sizeof(T) bytes).  Each warp owns a contiguous, cost-balanced edge range
-// (merge-path over rows + edges, built per engine) and streams the operand
-// rows through a per-warp shared-memory ring with cp.async, S edges deep, so
-// the gathers of the next S edges are in flight while the current one is
-// accumulated in fp64.  Rows cut by a range boundary are finished by the last
-// warp to arrive, which adds the fp64 partials in warp order.  Every row sum is
-// therefore a fixed-order fp64 accumulation and every per-query reduction goes
-// through per-block partial rows summed in a fixed order: bitwise deterministic.
+// (merge-path over rows + edges, built per engine) and keeps S operand rows in
+// flight in registers (k_pull_sw: (col, val) windows and row ends staged in
+// shared memory), accumulating in fp64 (fp32 mode: fp32 FMAs over at most 16
+// edges, flushed to fp64).  Rows cut by a range boundary are finished by the
+// last warp to arrive, which adds the fp64 partials in warp order.  Every row
+// sum is therefore a fixed-order accumulation and every per-query reduction
+// goes through per-block partial rows summed in a fixed order: bitwise
+// deterministic.
 #pragma once
 
 #include <cuda.h>
+
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -469,6 +472,14 @@ struct PullArgs {
     int64_t *np_v;         // [n_warps][B] (V pull)
     double one_minus_alpha;
     uint64_t *dbg;         // optional per-warp [start, end, edges, rows] globaltimer trace
+    // fused K3 + K1a (k_pull_sw<..., SIDE_U, COMBINE>): the U pull's row results
+    // go straight into the combine instead of through Y
+    T *R;                  // residues r_u [n_u][B]
+    T *Pn;                 // power-iteration iterate [n_u][B] (PI slots)
+    const double *ws_u, *inv_ws_u;
+    int32_t *p_any;        // partial rows [slot][part_rows]: one per warp, then one per cut row
+    double *p_sum, *p_wsum;
+    int32_t part_rows;
 };
 
 __device__ __forceinline__ uint64_t gtimer() {
@@ -800,6 +811,88 @@ __global__ void __launch_bounds__(PULL_THREADS, 2) k_pull(PullArgs<T> a) {
     }
 }
 
+// K1a for one U row inside the U pull: r_u += Y (push slots), a = y0 + Y (PI
+// slots), and the exit-test reductions (same arithmetic as k_combine).
+template <int B, typename T, int VEC>
+struct RowCombine {
+    double sum[VEC], wsum[VEC];
+    int32_t any[VEC];
+    __device__ __forceinline__ void init() {
+#pragma unroll
+        for (int v = 0; v < VEC; v++) {
+            sum[v] = wsum[v] = 0.0;
+            any[v] = 0;
+        }
+    }
+    __device__ __forceinline__ void row(const PullArgs<T> &a, const SlotSmem &sm, int slot0, int64_t u,
+                                        const double (&acc)[VEC], const T (&rv)[VEC], double ws, double iws) {
+        T nr[VEC];
+        bool wrote_r = false;
+#pragma unroll
+        for (int v = 0; v < VEC; v++) {
+            const int s = slot0 + v;
+            const int o = sm.op[s];
+            const T y = (T)acc[v];  // the value k_pull would have stored in Y
+            nr[v] = rv[v];
+            if (op_is_push(o) || o == OP_MEASURE) {
+                if (o != OP_MEASURE) {
+                    nr[v] = (T)((double)rv[v] + (double)y);
+                    wrote_r = true;
+                }
+                const double r = (double)nr[v];
+                sum[v] += r;
+                wsum[v] += (ws * sm.iwsq[s]) * r;  // w_ratio * r  (push_engine.py:220,237)
+                const double th = (op_is_fwd(o) || o == OP_MEASURE) ? (sm.wsq[s] * iws) * sm.thc[s] : sm.eps_b[s];
+                any[v] |= r > th;
+            } else if (o == OP_PIENTRY || o == OP_PI) {
+                a.Pn[u * B + s] = (T)((double)rv[v] * sm.ysc[s] + (double)y);
+            }
+        }
+        if (wrote_r) VecIO<T, VEC>::st(a.R + u * B + slot0, nr);
+    }
+    __device__ __forceinline__ void store(const PullArgs<T> &a, int row, int slot0) const {
+#pragma unroll
+        for (int v = 0; v < VEC; v++) {
+            const int64_t i = (int64_t)(slot0 + v) * a.part_rows + row;
+            a.p_sum[i] = sum[v];
+            a.p_wsum[i] = wsum[v];
+            a.p_any[i] = any[v];
+        }
+    }
+};
+
+// Cut row of the fused U pull: the last warp to arrive adds the partials and
+// runs the row's combine; its reductions go to partial row n_warps + cut index.
+template <int B, typename T, int VEC>
+__device__ __noinline__ void pull_cut_combine(const PullArgs<T> &a, const SlotSmem &sm, int ci, int pi, int slot0,
+                                              DVec<VEC> acc) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int v = 0; v < VEC; v++) a.scratch[(int64_t)pi * B + slot0 + v] = acc.v[v];
+    __threadfence();
+    __syncwarp();
+    const CutRow cr = a.cuts[ci];
+    int last = 0;
+    if (lane == 0) last = atomicAdd(a.cut_count + ci, 1) == cr.n_parts - 1;
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (!last) return;
+    __threadfence();
+    double tot[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; v++) tot[v] = 0.0;
+    for (int p = 0; p < cr.n_parts; p++)
+#pragma unroll
+        for (int v = 0; v < VEC; v++) tot[v] += __ldcg(a.scratch + (int64_t)(cr.first_part + p) * B + slot0 + v);
+    const int64_t u = cr.row;
+    T rv[VEC];
+    VecIO<T, VEC>::ld(a.R + u * B + slot0, rv);
+    RowCombine<B, T, VEC> rc;
+    rc.init();
+    rc.row(a, sm, slot0, u, tot, rv, a.ws_u[u], a.inv_ws_u[u]);
+    rc.store(a, a.n_warps + ci, slot0);
+    if (lane == 0) a.cut_count[ci] = 0;
+}
+
 // Same streaming pull with the per-warp (col, val) windows and row ends staged
 // in shared memory instead of lane registers: the per-edge work is one
 // broadcast LDS of the next (col, val) pair, the operand-row gather and VEC
@@ -821,11 +914,20 @@ struct EdgeCV {
     T v;
 };
 
-template <int B, typename T, int SIDE, int S = SwPipe<B, T>::S, int MINB = SwPipe<B, T>::MINB>
+template <int B, typename T, int SIDE, bool COMBINE = false, int S = SwPipe<B, T>::S,
+          int MINB = COMBINE ? 2 : SwPipe<B, T>::MINB>
 __global__ void __launch_bounds__(PULL_THREADS, MINB) k_pull_sw(PullArgs<T> a) {
+    static_assert(!COMBINE || SIDE == SIDE_U, "the combine follows the U pull");
     pdl_begin();
     if (*a.active == 0) return;
     constexpr int VEC = RegPipe<B, T>::VEC;
+    __shared__ std::conditional_t<COMBINE, SlotSmem, int> sm_c;  // slot constants, fused combine only
+    if constexpr (COMBINE) {
+        load_slot_smem<B>(sm_c, a.slots);
+        __syncthreads();
+    }
+    RowCombine<B, T, VEC> rc;
+    rc.init();
     static_assert(2 * S <= 32, "two windows must fit one warp load");
     __shared__ EdgeCV<T> s_win[PULL_WARPS][2][S];
     __shared__ int32_t s_re[PULL_WARPS][64];
@@ -882,6 +984,20 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) k_pull_sw(PullArgs<T> a) {
                 wsv[t] = e.v;
                 ldg_vec<T, VEC>(X + (int64_t)e.c * B, xs[t]);
             }
+            // fused combine: r_u row and ws of the next row to finish, one row ahead
+            T rpre[VEC];
+            double wpre = 0.0, ipre = 0.0;
+            auto prefetch_row = [&](int l) {
+                if constexpr (COMBINE) {
+                    const int64_t u = (int64_t)wk.r0 + l;
+                    if (u < a.n_rows) {
+                        VecIO<T, VEC>::ld(a.R + u * B + slot0, rpre);
+                        wpre = __ldg(a.ws_u + u);
+                        ipre = __ldg(a.inv_ws_u + u);
+                    }
+                }
+            };
+            prefetch_row(0);
             int rw = 0;       // row-end ring holds local rows [rw, rw + 64)
             int lr = 0;
             int rstart = (int)(__ldg(rp) - e0);
@@ -918,6 +1034,8 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) k_pull_sw(PullArgs<T> a) {
                             double *dst = a.scratch + (int64_t)(lr == cutA ? wk.part0 : wk.part1) * B + slot0;
 #pragma unroll
                             for (int v = 0; v < VEC; v++) dst[v] = acc[v];
+                        } else if constexpr (COMBINE) {
+                            rc.row(a, sm_c, slot0, (int64_t)wk.r0 + lr, acc, rpre, wpre, ipre);
                         } else {
                             T out[VEC];
 #pragma unroll
@@ -934,6 +1052,7 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) k_pull_sw(PullArgs<T> a) {
                         rstart = rend;
                         rend = re[lr & 63];
                         d = rend - base - 1;
+                        if constexpr (COMBINE) prefetch_row(lr);
                     }
                     const EdgeCV<T> e = nxt[t];
                     wsv[t] = e.v;
@@ -957,8 +1076,22 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) k_pull_sw(PullArgs<T> a) {
                 vw = val_at(base + 3 * S + lane);
                 __syncwarp();
             }
+            if constexpr (COMBINE) {
+                if (cutA >= 0) {
+                    DVec<VEC> av;
+#pragma unroll
+                    for (int v = 0; v < VEC; v++) av.v[v] = a.scratch[(int64_t)wk.part0 * B + slot0 + v];
+                    pull_cut_combine<B, T, VEC>(a, sm_c, wk.cut0, wk.part0, slot0, av);
+                }
+                if (cutB >= 0) {
+                    DVec<VEC> av;
+#pragma unroll
+                    for (int v = 0; v < VEC; v++) av.v[v] = a.scratch[(int64_t)wk.part1 * B + slot0 + v];
+                    pull_cut_combine<B, T, VEC>(a, sm_c, wk.cut1, wk.part1, slot0, av);
+                }
+            }
             const CutCtx<T> cx{a.scratch, a.cut_count, a.cuts, a.Y, a.indptr, scale};
-            if (cutA >= 0) {
+            if (!COMBINE && cutA >= 0) {
                 DVec<VEC> av;
 #pragma unroll
                 for (int v = 0; v < VEC; v++) av.v[v] = a.scratch[(int64_t)wk.part0 * B + slot0 + v];
@@ -966,7 +1099,7 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) k_pull_sw(PullArgs<T> a) {
 #pragma unroll
                 for (int v = 0; v < VEC; v++) np_cut[v] += inc.v[v];
             }
-            if (cutB >= 0) {
+            if (!COMBINE && cutB >= 0) {
                 DVec<VEC> av;
 #pragma unroll
                 for (int v = 0; v < VEC; v++) av.v[v] = a.scratch[(int64_t)wk.part1 * B + slot0 + v];
@@ -980,6 +1113,9 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) k_pull_sw(PullArgs<T> a) {
         if (gw < a.n_warps)
 #pragma unroll
             for (int v = 0; v < VEC; v++) a.np_v[(int64_t)(slot0 + v) * a.n_warps + gw] = (int64_t)np[v] + np_cut[v];
+    }
+    if constexpr (COMBINE) {
+        if (gw < a.n_warps) rc.store(a, gw, slot0);
     }
 }
 

@@ -184,3 +184,19 @@ def test_small_golden_graphs_load():
     for i in range(int(d["count"])):
         g = graph_from(d, f"g{i}_")
         assert g.edge_count == int(d[f"g{i}_n"][2])
+
+
+def test_operator_views_match_reference_definitions():
+    """u_step / v_step / transposes / recv_* (bigraph.py:148-188) on a golden graph."""
+    g = config_graph("c1")
+    u = g.u_step.toarray()
+    v = g.v_step.toarray()
+    np.testing.assert_allclose(u.sum(axis=1), 1.0, rtol=1e-12)
+    np.testing.assert_allclose(v.sum(axis=1), 1.0, rtol=1e-12)
+    np.testing.assert_array_equal(g.u_step_t.toarray(), u.T)
+    np.testing.assert_array_equal(g.v_step_t.toarray(), v.T)
+    eu = np.repeat(np.arange(g.u_count), np.diff(g.u_indptr))
+    np.testing.assert_array_equal(g.recv_uv, g.u_weights / g.ws_v[g.u_indices])
+    assert g.v_id(g.v_labels[7]) == 7 and g.u_id(g.u_labels[eu[3]]) == eu[3]
+    with pytest.raises(bh.DataError, match="unknown V-side label"):
+        g.v_id("nope")
