@@ -91,48 +91,93 @@ def config_json(cfg, n_local, world, slots, k):
 
 
 class Clocks:
-    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line).
+
+    The sampler is started and allowed to produce its first row before the
+    timed steps begin (``start()`` returns once it is live); only rows whose
+    timestamp falls inside [start(), stop()] are summarised."""
+
+    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        self.t0 = self.t1 = None
         try:
-            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
         except OSError:
             self.p = None
+            return
+        deadline = time.time() + 10.0
+        while time.time() < deadline and not Path(self.f.name).read_text().strip():
+            time.sleep(0.02)
+
+    def start(self):
+        import datetime
+        self.t0 = datetime.datetime.now()
 
     def stop(self) -> dict:
+        import datetime
+        self.t1 = datetime.datetime.now()
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.06)  # let the sampler flush the row covering the end of the region
         self.p.terminate()
         self.p.wait()
         self.f.flush()
-        rows = [r.split(",") for r in Path(self.f.name).read_text().strip().splitlines() if r.strip()]
+        rows = [[c.strip() for c in r.split(",")] for r in Path(self.f.name).read_text().strip().splitlines()
+                if r.strip()]
         os.unlink(self.f.name)
-        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+
+        def ts(r):
+            try:
+                return datetime.datetime.strptime(r[0], "%Y/%m/%d %H:%M:%S.%f")
+            except (ValueError, IndexError):
+                return None
+
+        inside = [r for r in rows if len(r) >= 10 and ts(r) is not None and self.t0 <= ts(r) <= self.t1]
+        num = lambda x: x.replace(".", "", 1).isdigit()  # noqa: E731
+        sm = [float(r[2]) for r in inside if num(r[2])]
+        mx = [float(r[3]) for r in rows if len(r) >= 10 and num(r[3])]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[j] for r in rows if len(r) >= 9 for j in range(4) if r[5 + j].strip() == "Active"})
+        reasons = sorted({names[j] for r in inside for j in range(4) if r[6 + j] == "Active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "sm_min_mhz": min(sm) if sm else None, "reasons": reasons, "samples": len(rows)}
+                "sm_min_mhz": min(sm) if sm else None, "reasons": reasons, "samples": len(inside),
+                "region_s": (self.t1 - self.t0).total_seconds()}
 
 
-def ncu_round_traffic():
-    """DRAM bytes (read + write) of one round's kernels from the committed ncu
-    capture (profiles/r01_ncu_round_kernels.json), or None."""
+def _ncu_kernels():
     p = REPO / "profiles" / "r01_ncu_round_kernels.json"
     if not p.exists():
         return None
     try:
-        ks = json.loads(p.read_text())["kernels"]
-        tot = sum(v.get("dram_read_MB", 0) + v.get("dram_write_MB", 0)
-                  for k, v in ks.items() if k.startswith(("k_push", "k_pull", "k_combine")))
-        return tot * 1e6
+        return json.loads(p.read_text())["kernels"]
     except Exception:
         return None
+
+
+def ncu_round_traffic():
+    """DRAM bytes (read + write) of one round's K1+K2+K3+K1a from the committed
+    ncu capture (profiles/r01_ncu_round_kernels.json), or None."""
+    ks = _ncu_kernels()
+    if not ks:
+        return None
+    return 1e6 * sum(v.get("dram_read_MB", 0) + v.get("dram_write_MB", 0)
+                     for k, v in ks.items() if k.startswith(("k_push", "k_pull", "k_combine")))
+
+
+def ncu_vpull_traffic():
+    """DRAM bytes (read + write) of one V-pull launch from the same capture."""
+    ks = _ncu_kernels()
+    if not ks:
+        return None
+    for k, v in ks.items():  # k_pull*<B, T, SIDE, ...>: SIDE 0 is the V pull
+        if k.startswith("k_pull") and k.split("<", 1)[1].split(",")[2].strip().rstrip(">") == "0":
+            return 1e6 * (v.get("dram_read_MB", 0) + v.get("dram_write_MB", 0))
+    return None
 
 
 def peak_hbm():
@@ -311,6 +356,8 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
         clocks = Clocks(local) if not os.environ.get("BH_BENCH_NO_CLOCKS") else None
+        if clocks:
+            clocks.start()
         launches0 = _capi.kernel_launches()
         ms, tprof, traces_all = run_steps(steps, False)
         launches = _capi.kernel_launches() - launches0
@@ -332,6 +379,11 @@ def run_ours(args):
     s_bytes = 4 if args.dtype == "fp32" else 8
     alg = sum(algorithmic_bytes(g, t, prof["rounds"] // args.steps, s_bytes) for t in traces_all)
     kern_ms = prof["ms_prep"] + prof["ms_vpull"] + prof["ms_upull"]
+    # dominant kernel: the V pull, SURVEY 8(d) bytes of one SpMM half per launch
+    B_slots = prof.get("slots", 0) or n
+    v_bytes = g.edge_count * (4 + s_bytes) + (g.v_count + 1) * 4 + B_slots * s_bytes * (g.u_count + g.v_count)
+    v_launch_us = prof["ms_vpull"] * 1e3 / max(1, prof["rounds"])
+    v_achieved = v_bytes / (v_launch_us / 1e6) / 1e9 if v_launch_us > 0 else None
     achieved = alg / (kern_ms / 1e3) / 1e9 if kern_ms > 0 else None
     peak, peak_src = peak_hbm()
 
@@ -382,12 +434,22 @@ def run_ours(args):
             "data": "synthetic (seeded Chung-Lu stand-in for configs[1]; reference sampler for sources)",
             "config": config_json(cfg, n, world, prof.get("slots", 0), k),
             "roofline": {
-                "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak if achieved else None, "traffic": ncu_round_traffic(),
-                "traffic_note": "DRAM read+write bytes of one round's K1+K2+K3+K1a from one ncu --set full "
-                                "capture (profiles/r01_ncu_round_kernels.json, cold cache), per round",
-                "algorithmic_bytes_per_round": alg / max(1, prof["rounds"]),
-                "kernel": "push/PI round = K1 push + K2 V-pull + K3 U-pull + K1a combine (SURVEY 8(d) unit)",
+                "bound": "hbm", "achieved": v_achieved, "peak": peak, "unit": "GB/s",
+                "frac": v_achieved / peak if v_achieved else None, "traffic": ncu_vpull_traffic(),
+                "kernel": "K2 V pull (k_pull_sw, SIDE_V), the dominant kernel",
+                "algorithmic_bytes_per_launch": v_bytes,
+                "algorithmic_model": "E(i+s) + (|V|+1) o + B s (|U| + |V|), i = o = 4 (SURVEY 8(d), one SpMM half)",
+                "launch_us": v_launch_us, "launches": int(prof["rounds"]),
+                "share_of_step": prof["ms_vpull"] / pms if pms else None,
+                "traffic_note": "DRAM read+write bytes of one V-pull launch from one ncu --set full capture "
+                                "(profiles/r01_ncu_round_kernels.json, cold cache)",
+                "round": {
+                    "unit": "push/PI round = K1 push + K2 V-pull + K3 U-pull + K1a combine (SURVEY 8(d) unit)",
+                    "achieved_gbs": achieved, "frac": achieved / peak if achieved else None,
+                    "algorithmic_bytes_per_round": alg / max(1, prof["rounds"]),
+                    "traffic_per_round": ncu_round_traffic(),
+                    "share_of_step": kern_ms / pms if pms else None,
+                },
                 "gather": {"bytes_per_round": 2 * g.edge_count * prof.get("slots", 0) * s_bytes,
                            "achieved_tbs": (2 * g.edge_count * prof.get("slots", 0) * s_bytes * prof["rounds"]
                                             / ((prof["ms_vpull"] + prof["ms_upull"]) / 1e3) / 1e12)
@@ -396,7 +458,6 @@ def run_ours(args):
                                    "tools/gather_bench.cu ceiling 13-17 TB/s"},
                 "algorithmic_bytes_per_step": alg / args.steps, "kernel_ms_per_step": kern_ms / args.steps,
                 "rounds_per_step": prof["rounds"] / args.steps,
-                "share_of_step": kern_ms / pms if pms else None,
                 "timing": "per-kernel CUDA events on the engine stream, in a replay of the timed steps "
                           "(the headline value is timed without per-kernel events; each timed step is "
                           "enqueued behind a device start gate, so e0..e1 is device time only)",
