@@ -228,6 +228,12 @@ struct Engine final : EngineBase {
     // round trip, no combine launch (BH_FUSE_COMBINE=1).
     bool fuse_combine = false;
 
+    // elementwise K1 / K1a: 2 nodes in flight per thread at 3 blocks/SM (fp32) measured
+    // fastest at c2 (prep 7.35 -> 6.68 ms per step against 4 nodes at 2 blocks/SM)
+    using ElemFn = void (*)(ElemArgs<T>);
+    ElemFn push_kernel() const { return k_push<B, T, 2, (sizeof(T) == 4 ? 3 : 2)>; }
+    ElemFn combine_kernel() const { return k_combine<B, T, 2, (sizeof(T) == 4 ? 3 : 2)>; }
+
     using PullFn = void (*)(PullArgs<T>);
     template <int SIDE>
     PullFn sw_kernel() const {
@@ -342,8 +348,8 @@ struct Engine final : EngineBase {
         }
         {  // one resident wave of the elementwise kernels
             int occ_p = 1, occ_c = 1;
-            BH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, k_push<B, T>, ELEM_THREADS, 0));
-            BH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, k_combine<B, T>, ELEM_THREADS, 0));
+            BH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, push_kernel(), ELEM_THREADS, 0));
+            BH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, combine_kernel(), ELEM_THREADS, 0));
             int occ = std::max(1, std::min(occ_p, occ_c));
             if (const char *m = getenv("BH_ELEM_BLOCKS_PER_SM")) occ = std::max(1, atoi(m));
             grid_elem = grid1d(nu * (B / ElemGeo<B>::EV), ELEM_THREADS, occ * sms);
@@ -508,13 +514,13 @@ struct Engine final : EngineBase {
         ea.part = part;
         ea.alpha = rs.alpha;
         if (prof) BH_CUDA(cudaEventRecord(ev(e0), st));
-        launch_pdl(k_push<B, T>, grid_elem, ELEM_THREADS, 0, st, ea);
+        launch_pdl(push_kernel(), grid_elem, ELEM_THREADS, 0, st, ea);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 1), st));
         launch_pull(SIDE_V, pull_args(SIDE_V, 1.0 - rs.alpha), st);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 2), st));
         launch_pull(SIDE_U, pull_args(SIDE_U, 1.0 - rs.alpha), st);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 3), st));
-        if (!fuse_combine) launch_pdl(k_combine<B, T>, grid_elem, ELEM_THREADS, 0, st, ea);
+        if (!fuse_combine) launch_pdl(combine_kernel(), grid_elem, ELEM_THREADS, 0, st, ea);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 4), st));
         launch_pdl(k_control, B, CONTROL_THREADS, 0, st, ca);
         launch_pdl(k_finalize<T>, grid_k5, TOPK_THREADS, 0, st, fa);

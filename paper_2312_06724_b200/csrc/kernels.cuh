@@ -172,7 +172,6 @@ __device__ __forceinline__ void load_slot_smem(SlotSmem &sm, const Slot *__restr
 // ---------------------------------------------------------------------------
 // Elementwise kernels over [n_u x B]: one thread per (node, EV consecutive slots).
 constexpr int ELEM_THREADS = 256;
-constexpr int ELEM_UNR = 4;  // nodes in flight per thread in K1 / K1a
 
 template <int B>
 struct ElemGeo {
@@ -198,8 +197,8 @@ struct ElemArgs {
 };
 
 // K1: push (and ledger init / power-iteration entry) for the coming round.
-template <int B, typename T>
-__global__ void __launch_bounds__(ELEM_THREADS) k_push(ElemArgs<T> a) {
+template <int B, typename T, int ELEM_UNR = 4, int MINB = 1>
+__global__ void __launch_bounds__(ELEM_THREADS, MINB) k_push(ElemArgs<T> a) {
     pdl_begin();
     if (*a.active == 0) return;
     using EG = ElemGeo<B>;
@@ -337,8 +336,8 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_push(ElemArgs<T> a) {
 
 // K1a: combine r_u += Y (push slots) / a = y0 + Y (power-iteration slots), and
 // the exit-test reductions of the round that just ran.
-template <int B, typename T>
-__global__ void __launch_bounds__(ELEM_THREADS) k_combine(ElemArgs<T> a) {
+template <int B, typename T, int ELEM_UNR = 4, int MINB = 1>
+__global__ void __launch_bounds__(ELEM_THREADS, MINB) k_combine(ElemArgs<T> a) {
     pdl_begin();
     if (*a.active == 0) return;
     using EG = ElemGeo<B>;
