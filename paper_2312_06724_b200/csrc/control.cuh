@@ -154,15 +154,16 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
                 left += l4[j];
             }
         }
-        for (int r0 = 0; r0 < a.part.rows_k2; r0 += STEP) {
-            int64_t n4[U4];
+        constexpr int U16 = 16, STEP16 = CONTROL_THREADS * U16;  // per-warp n_p rows: many, all in flight
+        for (int r0 = 0; r0 < a.part.rows_k2; r0 += STEP16) {
+            int64_t n16[U16];
 #pragma unroll
-            for (int j = 0; j < U4; j++) {
+            for (int j = 0; j < U16; j++) {
                 const int r = r0 + j * CONTROL_THREADS + tid;
-                n4[j] = r < a.part.rows_k2 ? __ldcg(pv + r) : 0;
+                n16[j] = r < a.part.rows_k2 ? __ldcg(pv + r) : 0;
             }
 #pragma unroll
-            for (int j = 0; j < U4; j++) np += n4[j];
+            for (int j = 0; j < U16; j++) np += n16[j];
         }
         for (int r0 = 0; r0 < a.part.rows_k3; r0 += STEP) {
             int32_t a4[U4];

@@ -750,8 +750,11 @@ struct EngineCache {
     int64_t cap_sc = 0;
     double *d_vec_a = nullptr, *d_vec_b = nullptr;
     int64_t cap_vec = 0;
+    unsigned char *h_stage = nullptr;  // pinned staging for the host-pointer outputs
+    size_t cap_stage = 0;
     ~EngineCache() {
         by_b.clear();
+        if (h_stage) cudaFreeHost(h_stage);
         cudaFree(d_src); cudaFree(d_tie); cudaFree(d_tk_idx); cudaFree(d_tk_sc);
         cudaFree(d_trace); cudaFree(d_scores); cudaFree(d_vec_a); cudaFree(d_vec_b);
         if (stream) cudaStreamDestroy(stream);
@@ -1020,16 +1023,33 @@ int bh_query_batch(bh_graph *g, const bh_query_params *p, const int32_t *sources
             grow(c.d_scores, c.cap_sc, n_q * g->n_u);
             rs.scores = c.d_scores;
         }
-        e.run(rs, st);
-        BH_CUDA(cudaMemcpyAsync(trace, c.d_trace, n_q * sizeof(bh_trace), cudaMemcpyDeviceToHost, st));
-        if (rs.topk_idx) {
-            BH_CUDA(cudaMemcpyAsync(topk_idx, c.d_tk_idx, n_q * p->k * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-            if (topk_score)
-                BH_CUDA(cudaMemcpyAsync(topk_score, c.d_tk_sc, n_q * p->k * sizeof(double), cudaMemcpyDeviceToHost, st));
+        // outputs go device -> pinned staging right behind the batch on the stream
+        // (one synchronisation, no host turnaround between the batch and its copies),
+        // then staging -> caller arrays on the host
+        const size_t b_tr = n_q * sizeof(bh_trace);
+        const size_t b_ti = rs.topk_idx ? n_q * p->k * sizeof(int32_t) : 0;
+        const size_t b_ts = rs.topk_idx && topk_score ? n_q * p->k * sizeof(double) : 0;
+        const size_t b_sc = rs.want_scores ? n_q * g->n_u * sizeof(double) : 0;  // large: copied directly
+        const size_t need = b_tr + b_ti + b_ts;
+        if (need > c.cap_stage) {
+            if (c.h_stage) cudaFreeHost(c.h_stage);
+            c.h_stage = nullptr;
+            c.cap_stage = 0;
+            BH_CUDA(cudaMallocHost(&c.h_stage, need));
+            c.cap_stage = need;
         }
-        if (rs.want_scores)
-            BH_CUDA(cudaMemcpyAsync(scores, c.d_scores, n_q * g->n_u * sizeof(double), cudaMemcpyDeviceToHost, st));
+        unsigned char *h_tr = c.h_stage, *h_ti = h_tr + b_tr, *h_ts = h_ti + b_ti;
+        rs.async = true;
+        e.run(rs, st);
+        BH_CUDA(cudaMemcpyAsync(h_tr, c.d_trace, b_tr, cudaMemcpyDeviceToHost, st));
+        if (b_ti) BH_CUDA(cudaMemcpyAsync(h_ti, c.d_tk_idx, b_ti, cudaMemcpyDeviceToHost, st));
+        if (b_ts) BH_CUDA(cudaMemcpyAsync(h_ts, c.d_tk_sc, b_ts, cudaMemcpyDeviceToHost, st));
+        if (b_sc) BH_CUDA(cudaMemcpyAsync(scores, c.d_scores, b_sc, cudaMemcpyDeviceToHost, st));
+        e.finish();  // synchronises the stream (graph path), checks termination
         BH_CUDA(cudaStreamSynchronize(st));
+        std::memcpy(trace, h_tr, b_tr);
+        if (b_ti) std::memcpy(topk_idx, h_ti, b_ti);
+        if (b_ts) std::memcpy(topk_score, h_ts, b_ts);
     });
 }
 
