@@ -28,43 +28,105 @@ constexpr int TOPK_MAX = 1024;
 
 struct SelectSmem {
     uint32_t hist[256];
+    uint32_t wsum[TOPK_THREADS / 32];
     unsigned long long cnt;
     uint64_t prefix;
     int64_t krem;
     int32_t out_n;
 };
 
+// Inclusive prefix sum of one value per thread over the block (blockDim == TOPK_THREADS).
+__device__ __forceinline__ uint32_t block_incl_scan(uint32_t v, SelectSmem &sm) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+    }
+    if (lane == 31) sm.wsum[w] = v;
+    __syncthreads();
+    uint32_t add = 0;
+    for (int j = 0; j < w; j++) add += sm.wsum[j];
+    __syncthreads();
+    return v + add;
+}
+
+// One radix digit of the select: given the 256-bin histogram of the candidates
+// that still match the prefix, pick the digit holding the krem-th element
+// (descending digits for keys, ascending for indices) in parallel: thread t
+// owns one bin, a block scan gives the cumulative counts, exactly one thread
+// sees the crossing.  Updates sm.prefix / sm.krem.
+__device__ __forceinline__ void pick_digit(SelectSmem &sm, uint64_t prefix, int shift, bool descending) {
+    const int t = threadIdx.x;
+    const int d = descending ? 255 - t : t;
+    const uint32_t h = sm.hist[d];
+    const int64_t krem = sm.krem;
+    const uint32_t incl = block_incl_scan(h, sm);  // elements in digits "before or at" d
+    if ((int64_t)incl >= krem && (int64_t)(incl - h) < krem) {
+        sm.prefix = prefix | ((uint64_t)d << shift);
+        sm.krem = krem - (int64_t)(incl - h);
+    }
+    __syncthreads();
+}
+
+constexpr int SEL_ITEMS = 16;  // candidates cached per thread (n <= SEL_ITEMS * TOPK_THREADS)
+
 // Select exactly min(k, #valid) elements that are largest under (key desc,
 // idx asc) among n candidates given by acc(i, &key, &idx) -> valid.  Output
-// order is arbitrary.  All threads of the block must call it.
+// order is arbitrary.  All threads of the block must call it; blockDim must be
+// TOPK_THREADS.  Up to SEL_ITEMS * TOPK_THREADS candidates are read once into
+// registers; larger inputs are re-read through acc on every pass.
 template <class Acc>
 __device__ int64_t block_select(int64_t n, int64_t k, Acc acc, SelectSmem &sm, uint64_t *out_key,
                                 int64_t *out_idx) {
     const int tid = threadIdx.x, nt = blockDim.x;
+    const bool cached = n <= (int64_t)SEL_ITEMS * nt;
+    uint64_t ck[SEL_ITEMS];
+    int64_t ci[SEL_ITEMS];
+    bool cv[SEL_ITEMS];
     if (tid == 0) {
         sm.cnt = 0;
         sm.out_n = 0;
     }
     __syncthreads();
     unsigned long long c = 0;
-    for (int64_t i = tid; i < n; i += nt) {
-        uint64_t kk;
-        int64_t ii;
-        c += acc(i, kk, ii);
+    if (cached) {
+#pragma unroll
+        for (int j = 0; j < SEL_ITEMS; j++) {
+            const int64_t i = tid + (int64_t)j * nt;
+            cv[j] = i < n && acc(i, ck[j], ci[j]);
+            c += cv[j];
+        }
+    } else {
+        for (int64_t i = tid; i < n; i += nt) {
+            uint64_t kk;
+            int64_t ii;
+            c += acc(i, kk, ii);
+        }
     }
+    // visit every valid candidate: f(key, idx)
+    auto each = [&](auto f) {
+        if (cached) {
+#pragma unroll
+            for (int j = 0; j < SEL_ITEMS; j++)
+                if (cv[j]) f(ck[j], ci[j]);
+        } else {
+            for (int64_t i = tid; i < n; i += nt) {
+                uint64_t kk;
+                int64_t ii;
+                if (acc(i, kk, ii)) f(kk, ii);
+            }
+        }
+    };
     atomicAdd(&sm.cnt, c);
     __syncthreads();
     const int64_t n_valid = (int64_t)sm.cnt;
     if (n_valid <= k) {
-        for (int64_t i = tid; i < n; i += nt) {
-            uint64_t kk;
-            int64_t ii;
-            if (acc(i, kk, ii)) {
-                int p = atomicAdd(&sm.out_n, 1);
-                out_key[p] = kk;
-                out_idx[p] = ii;
-            }
-        }
+        each([&](uint64_t kk, int64_t ii) {
+            const int p = atomicAdd(&sm.out_n, 1);
+            out_key[p] = kk;
+            out_idx[p] = ii;
+        });
         __syncthreads();
         return n_valid;
     }
@@ -72,26 +134,13 @@ __device__ int64_t block_select(int64_t n, int64_t k, Acc acc, SelectSmem &sm, u
     uint64_t prefix = 0, mask = 0;
     if (tid == 0) sm.krem = k;
     for (int shift = 56; shift >= 0; shift -= 8) {
-        for (int d = tid; d < 256; d += nt) sm.hist[d] = 0;
+        sm.hist[tid] = 0;
         __syncthreads();
-        for (int64_t i = tid; i < n; i += nt) {
-            uint64_t kk;
-            int64_t ii;
-            if (acc(i, kk, ii) && (kk & mask) == prefix) atomicAdd(&sm.hist[(kk >> shift) & 255u], 1u);
-        }
+        each([&](uint64_t kk, int64_t) {
+            if ((kk & mask) == prefix) atomicAdd(&sm.hist[(kk >> shift) & 255u], 1u);
+        });
         __syncthreads();
-        if (tid == 0) {
-            int64_t cum = 0;
-            for (int d = 255; d >= 0; d--) {
-                if (cum + sm.hist[d] >= sm.krem) {
-                    sm.krem -= cum;
-                    sm.prefix = prefix | ((uint64_t)d << shift);
-                    break;
-                }
-                cum += sm.hist[d];
-            }
-        }
-        __syncthreads();
+        pick_digit(sm, prefix, shift, true);
         prefix = sm.prefix;
         mask |= (0xffull << shift);
     }
@@ -99,40 +148,24 @@ __device__ int64_t block_select(int64_t n, int64_t k, Acc acc, SelectSmem &sm, u
     // ties at kstar: the smallest indices (4 passes over 32-bit indices)
     uint64_t ipre = 0, imask = 0;
     for (int shift = 24; shift >= 0; shift -= 8) {
-        for (int d = tid; d < 256; d += nt) sm.hist[d] = 0;
+        sm.hist[tid] = 0;
         __syncthreads();
-        for (int64_t i = tid; i < n; i += nt) {
-            uint64_t kk;
-            int64_t ii;
-            if (acc(i, kk, ii) && kk == kstar && (((uint64_t)ii) & imask) == ipre)
-                atomicAdd(&sm.hist[(((uint64_t)ii) >> shift) & 255u], 1u);
-        }
+        each([&](uint64_t kk, int64_t ii) {
+            if (kk == kstar && (((uint64_t)ii) & imask) == ipre) atomicAdd(&sm.hist[(((uint64_t)ii) >> shift) & 255u], 1u);
+        });
         __syncthreads();
-        if (tid == 0) {
-            int64_t cum = 0;
-            for (int d = 0; d < 256; d++) {
-                if (cum + sm.hist[d] >= sm.krem) {
-                    sm.krem -= cum;
-                    sm.prefix = ipre | ((uint64_t)d << shift);
-                    break;
-                }
-                cum += sm.hist[d];
-            }
-        }
-        __syncthreads();
+        pick_digit(sm, ipre, shift, false);
         ipre = sm.prefix;
         imask |= (0xffull << shift);
     }
     const uint64_t istar = ipre;
-    for (int64_t i = tid; i < n; i += nt) {
-        uint64_t kk;
-        int64_t ii;
-        if (acc(i, kk, ii) && (kk > kstar || (kk == kstar && (uint64_t)ii <= istar))) {
-            int p = atomicAdd(&sm.out_n, 1);
+    each([&](uint64_t kk, int64_t ii) {
+        if (kk > kstar || (kk == kstar && (uint64_t)ii <= istar)) {
+            const int p = atomicAdd(&sm.out_n, 1);
             out_key[p] = kk;
             out_idx[p] = ii;
         }
-    }
+    });
     __syncthreads();
     return k;
 }
