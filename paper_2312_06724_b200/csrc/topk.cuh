@@ -33,6 +33,7 @@ struct SelectSmem {
     uint64_t prefix;
     int64_t krem;
     int32_t out_n;
+    int32_t done;  // the chosen bin holds exactly the remaining count: selection complete
 };
 
 // Inclusive prefix sum of one value per thread over the block (blockDim == TOPK_THREADS).
@@ -65,6 +66,7 @@ __device__ __forceinline__ void pick_digit(SelectSmem &sm, uint64_t prefix, int 
     if ((int64_t)incl >= krem && (int64_t)(incl - h) < krem) {
         sm.prefix = prefix | ((uint64_t)d << shift);
         sm.krem = krem - (int64_t)(incl - h);
+        sm.done = (int64_t)h == krem - (int64_t)(incl - h);
     }
     __syncthreads();
 }
@@ -130,9 +132,24 @@ __device__ int64_t block_select(int64_t n, int64_t k, Acc acc, SelectSmem &sm, u
         __syncthreads();
         return n_valid;
     }
-    // 8 passes over the key bits, most significant digit first
+    // up to 8 passes over the key bits, most significant digit first; stop as soon
+    // as the bin holding the k-th element is taken whole (then the selection is
+    // exactly {key : key & mask >= prefix}, k elements)
+    auto emit_if = [&](auto pred) {
+        each([&](uint64_t kk, int64_t ii) {
+            if (pred(kk, ii)) {
+                const int p = atomicAdd(&sm.out_n, 1);
+                out_key[p] = kk;
+                out_idx[p] = ii;
+            }
+        });
+        __syncthreads();
+    };
     uint64_t prefix = 0, mask = 0;
-    if (tid == 0) sm.krem = k;
+    if (tid == 0) {
+        sm.krem = k;
+        sm.done = 0;
+    }
     for (int shift = 56; shift >= 0; shift -= 8) {
         sm.hist[tid] = 0;
         __syncthreads();
@@ -143,6 +160,10 @@ __device__ int64_t block_select(int64_t n, int64_t k, Acc acc, SelectSmem &sm, u
         pick_digit(sm, prefix, shift, true);
         prefix = sm.prefix;
         mask |= (0xffull << shift);
+        if (sm.done) {
+            emit_if([&](uint64_t kk, int64_t) { return (kk & mask) >= prefix; });
+            return k;
+        }
     }
     const uint64_t kstar = prefix;
     // ties at kstar: the smallest indices (4 passes over 32-bit indices)
@@ -157,16 +178,11 @@ __device__ int64_t block_select(int64_t n, int64_t k, Acc acc, SelectSmem &sm, u
         pick_digit(sm, ipre, shift, false);
         ipre = sm.prefix;
         imask |= (0xffull << shift);
+        if (sm.done) break;  // {index & imask <= ipre} among the key ties is exactly what is left
     }
-    const uint64_t istar = ipre;
-    each([&](uint64_t kk, int64_t ii) {
-        if (kk > kstar || (kk == kstar && (uint64_t)ii <= istar)) {
-            const int p = atomicAdd(&sm.out_n, 1);
-            out_key[p] = kk;
-            out_idx[p] = ii;
-        }
+    emit_if([&](uint64_t kk, int64_t ii) {
+        return kk > kstar || (kk == kstar && (((uint64_t)ii) & imask) <= ipre);
     });
-    __syncthreads();
     return k;
 }
 

@@ -305,6 +305,16 @@ def test_topk_semantics():
     for k in (1, 10, 1000, 1500):
         got = [int(lab) for lab, _ in bh.topk(res2, k, exclude_query=True)]
         assert got == list(O.topk_indices(x, k, 5))
+    # radix-select edge cases: all equal, k-th inside a large tie block, negative and
+    # zero values, sizes around the register-cached limit (16 x 256 per block)
+    cases = [np.full(5000, 0.125), np.r_[np.full(3000, 2.0), np.full(3000, 1.0)],
+             rng.normal(size=4096), np.r_[rng.random(4097), -rng.random(10), np.zeros(7)],
+             rng.integers(0, 3, 100000).astype(float)]
+    for x in cases:
+        r = bh.QueryResult("x", 0, x, 1e-3, 5e-4, 5e-4, {}, {}, None)
+        for k in (1, 50, 1023, 1024):
+            got = [int(lab) for lab, _ in bh.topk(r, k)]
+            assert got == list(O.topk_indices(x, k)), (x.size, k)
 
 
 def test_errors_match_reference():
