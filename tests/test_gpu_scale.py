@@ -144,3 +144,41 @@ def test_pisp_query_matches_oracle_composition():
         assert r.phase_trace["forward"]["power_iterations"] == depth
         assert r.phase_trace["backward"]["selective_rounds"] == tr["selective_rounds"]
         assert r.method == "pisp"
+
+
+def test_async_submit_and_gate_match_sync():
+    """BH_QUERY_ASYNC + bh_query_wait and the measurement gate give the sync results."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2312_06724_b200 import _capi
+    from paper_2312_06724_b200.bhpp_query import query_batch_device, query_wait
+
+    g = config_graph("c2s")
+    meta = bh.build_index_meta(g, 0.15)
+    src = load("c2s")["sources"][:8]
+    ref = bh.bhpp_query_batch(g, meta, src, 1e-7, k=20, dtype="fp32")
+    dg = _capi.device_graph(g, "fp32")
+    eb = meta.eps_split_policy(1e-7)
+    dev = torch.device("cuda:0")
+    st = torch.cuda.Stream(device=dev)
+    s_t = torch.from_numpy(np.asarray(src, dtype=np.int32)).to(dev)
+    ti = torch.empty((len(src), 20), dtype=torch.int32, device=dev)
+    ts = torch.empty((len(src), 20), dtype=torch.float64, device=dev)
+    tr = torch.empty((len(src), _capi.TRACE_DTYPE.itemsize), dtype=torch.uint8, device=dev)
+    gate = torch.zeros(1, dtype=torch.int32).pin_memory()
+    _capi.check(_capi.lib().bh_stream_gate(C.c_void_p(st.cuda_stream), C.c_void_p(gate.data_ptr())))
+    query_batch_device(dg, meta, eb, 1e-7 - eb, s_t.data_ptr(), len(src), 20, ti.data_ptr(), ts.data_ptr(),
+                       tr.data_ptr(), stream=st.cuda_stream, async_=True)
+    gate[0] = 1
+    query_wait(dg)
+    np.testing.assert_array_equal(ti.cpu().numpy(), ref.topk_index)
+    np.testing.assert_array_equal(ts.cpu().numpy(), ref.topk_score)
+    assert tr.cpu().numpy().tobytes() == ref.traces.tobytes()
+    # an async batch left unwaited is completed by the next call on the graph
+    query_batch_device(dg, meta, eb, 1e-7 - eb, s_t.data_ptr(), len(src), 20, ti.data_ptr(), ts.data_ptr(),
+                       tr.data_ptr(), stream=st.cuda_stream, async_=True)
+    again = bh.bhpp_query_batch(g, meta, src, 1e-7, k=20, dtype="fp32")
+    np.testing.assert_array_equal(again.topk_index, ref.topk_index)
+    np.testing.assert_array_equal(ti.cpu().numpy(), ref.topk_index)
