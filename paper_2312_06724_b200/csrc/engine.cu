@@ -208,7 +208,7 @@ struct Engine final : EngineBase {
     cudaStream_t cap_stream = nullptr;
     std::vector<unsigned char> graph_key;
     size_t pull_smem = 0;
-    int fin_chunk = 4096, n_chunks = 1;
+    int fin_chunk = SEL_ITEMS * TOPK_THREADS, n_chunks = 1;  // one register-cached select per chunk
     int grid_elem = 1, grid_k5 = 1;
 
     // Pull mapping per side: half-warp workers (two operand rows per warp
@@ -355,7 +355,7 @@ struct Engine final : EngineBase {
             grid_elem = grid1d(nu * (B / ElemGeo<B>::EV), ELEM_THREADS, occ * sms);
         }
         n_chunks = (int)((nu + fin_chunk - 1) / fin_chunk);
-        grid_k5 = (int)std::min<int64_t>((int64_t)n_chunks * std::min(B, 8), 8 * sms);
+        grid_k5 = (int)std::min<int64_t>((int64_t)n_chunks * std::min(B, 16), 16 * sms);
         part.rows_k1 = grid_elem;
         part.rows_k2 = half_v ? (plan_v.n_warps + 1) / 2 : plan_v.n_warps;
         part.rows_k3 = fuse_combine ? plan_u.n_warps + plan_u.n_cuts : grid_elem;
@@ -1184,7 +1184,7 @@ int bh_topk(const double *scores, int64_t n, int64_t k, int64_t exclude, int64_t
             BH_CUDA(cudaMemcpyAsync(dx, scores, n * sizeof(double), cudaMemcpyHostToDevice, st));
             const int64_t kk = std::min(k, n);
             if (kk <= TOPK_MAX) {
-                const int64_t chunk = 8192;
+                const int64_t chunk = SEL_ITEMS * TOPK_THREADS;
                 const int64_t nch = (n + chunk - 1) / chunk;
                 ck = dalloc<uint64_t>(nch * kk);
                 ci = dalloc<int64_t>(nch * kk);

@@ -71,7 +71,7 @@ __device__ __forceinline__ void pick_digit(SelectSmem &sm, uint64_t prefix, int 
     __syncthreads();
 }
 
-constexpr int SEL_ITEMS = 16;  // candidates cached per thread (n <= SEL_ITEMS * TOPK_THREADS)
+constexpr int SEL_ITEMS = 8;  // candidates cached per thread (n <= SEL_ITEMS * TOPK_THREADS)
 
 // Select exactly min(k, #valid) elements that are largest under (key desc,
 // idx asc) among n candidates given by acc(i, &key, &idx) -> valid.  Output
