@@ -15,6 +15,7 @@
  *   power_iteration (push_engine.py:101-117), estimate_lambda   -> bh_power_iteration
  *   topk (bhpp_query.py:206-218) on an arbitrary score vector   -> bh_topk
  *   BipartiteGraph.__init__ canonicalisation (bigraph.py:53-111) -> bh_csr_build
+ *   load_edge_list text parsing (bigraph.py:272-350)             -> bh_edge_list_*
  *
  * Status codes: 0 ok; BH_EINVAL -> ValueError; BH_EUNFLUSHED -> ValueError
  * ("unflushed ledger", push_engine.py:214-217); BH_ECUDA -> RuntimeError;
@@ -157,6 +158,24 @@ int bh_csr_build(int64_t n_u, int64_t n_v, int64_t n_e, const int64_t *edge_u, c
                  const double *edge_w, int64_t *u_indptr, int32_t *u_indices, double *u_weights,
                  int64_t *v_indptr, int32_t *v_indices, double *v_weights, double *ws_u, double *ws_v,
                  int32_t device);
+
+/* Text edge list (bigraph.py:272-350), host-side native parser.  buf/len: the
+ * file bytes; delim: column separator bytes or NULL for runs of whitespace;
+ * has_default/default_weight: weight of two-column lines.  Returns BH_OK with
+ * *out set, or BH_EFALLBACK when the input needs the reference's Python loop
+ * (non-ASCII bytes, weight tokens other than plain decimals, or any data error;
+ * *err_line then holds the offending line, 0 if none). */
+typedef struct bh_edge_list bh_edge_list;
+#define BH_EFALLBACK 6
+int bh_edge_list_parse(const char *buf, int64_t len, const char *delim, int64_t delim_len, int32_t has_default,
+                       double default_weight, bh_edge_list **out, int64_t *err_line);
+/* sizes: labels per side, bytes of each side's concatenated labels, merged edges */
+int bh_edge_list_sizes(const bh_edge_list *el, int64_t *n_u, int64_t *n_v, int64_t *u_bytes, int64_t *v_bytes,
+                       int64_t *n_e);
+/* labels as concatenated bytes + end offsets, merged edges in first-seen order */
+int bh_edge_list_export(const bh_edge_list *el, char *u_blob, int64_t *u_ends, char *v_blob, int64_t *v_ends,
+                        int64_t *edge_u, int64_t *edge_v, double *edge_w);
+void bh_edge_list_free(bh_edge_list *el);
 
 /* ---- measurement ---------------------------------------------------------- */
 typedef struct bh_run_stats {

@@ -20,7 +20,7 @@ LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libbhpp.so"
 if os.environ.get("BH_LIBBHPP"):  # A/B of two in-tree builds (tools/ab_pull.sh)
     LIB_PATH = Path(os.environ["BH_LIBBHPP"]).resolve()
 
-BH_OK, BH_EINVAL, BH_EUNFLUSHED, BH_ECUDA, BH_ENOMEM, BH_EDUP = 0, 1, 2, 3, 4, 5
+BH_OK, BH_EINVAL, BH_EUNFLUSHED, BH_ECUDA, BH_ENOMEM, BH_EDUP, BH_EFALLBACK = 0, 1, 2, 3, 4, 5, 6
 DTYPES = {"fp64": 0, "f64": 0, "float64": 0, "fp32": 1, "f32": 1, "float32": 1}
 JOB_BHPP, JOB_SS_PUSH, JOB_SELECTIVE, JOB_PI_PUSH, JOB_POWER = 0, 1, 2, 3, 4
 TERMINATIONS = ("threshold-met", "budget-switch", "mass-drained")
@@ -30,6 +30,7 @@ EXPORTS = (
     "bh_graph_create", "bh_graph_destroy", "bh_graph_get_info", "bh_query_batch", "bh_push_run",
     "bh_power_iteration", "bh_topk", "bh_last_error", "bh_version", "bh_kernel_launches",
     "bh_set_profiling", "bh_last_run_stats", "bh_csr_build", "bh_query_wait", "bh_stream_gate",
+    "bh_edge_list_parse", "bh_edge_list_sizes", "bh_edge_list_export", "bh_edge_list_free",
 )
 QUERY_ASYNC = 1
 
@@ -120,6 +121,15 @@ def lib():
         L.bh_set_profiling.argtypes = [C.c_int32]
         L.bh_last_run_stats.restype = C.c_int
         L.bh_last_run_stats.argtypes = [P, C.POINTER(RunStats)]
+        L.bh_edge_list_parse.restype = C.c_int
+        L.bh_edge_list_parse.argtypes = [C.c_char_p, C.c_int64, C.c_char_p, C.c_int64, C.c_int32, C.c_double,
+                                         C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]
+        L.bh_edge_list_sizes.restype = C.c_int
+        L.bh_edge_list_sizes.argtypes = [P] + [C.POINTER(C.c_int64)] * 5
+        L.bh_edge_list_export.restype = C.c_int
+        L.bh_edge_list_export.argtypes = [P, C.c_char_p, P, C.c_char_p, P, P, P, P]
+        L.bh_edge_list_free.restype = None
+        L.bh_edge_list_free.argtypes = [P]
         L.bh_query_wait.restype = C.c_int
         L.bh_query_wait.argtypes = [P]
         L.bh_stream_gate.restype = C.c_int

@@ -17,6 +17,9 @@ namespace bh {
 struct CudaError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
+struct FallbackNeeded : std::runtime_error {  // bh_edge_list_parse: use the Python loop
+    FallbackNeeded() : std::runtime_error("fallback") {}
+};
 struct InvalidArg : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
@@ -30,6 +33,18 @@ struct InvalidArg : std::runtime_error {
     } while (0)
 
 void count_launch(int n = 1);
+
+// edge_list.cpp: native text edge-list parser (host)
+enum : int { PARSE_OK = 0, PARSE_FALLBACK = 1, PARSE_ERROR = 2 };
+struct EdgeListResult {
+    std::vector<std::string> u_labels, v_labels;
+    std::vector<int64_t> eu, ev;
+    std::vector<double> ew;
+    int64_t err_line = 0;
+    int status = PARSE_OK;
+};
+EdgeListResult parse_edge_list(const char *buf, int64_t len, const char *delim, int64_t delim_len, bool has_default,
+                               double default_weight);
 
 // csr_build.cu: device canonicalisation of an edge list (bh_csr_build); 1 = duplicate pair.
 int csr_build(int64_t n_u, int64_t n_v, int64_t n_e, const int64_t *edge_u, const int64_t *edge_v,

@@ -832,6 +832,9 @@ static int guarded(F &&f) {
     try {
         f();
         return BH_OK;
+    } catch (const FallbackNeeded &) {
+        t_err = "input needs the reference-semantics parser";
+        return BH_EFALLBACK;
     } catch (const InvalidArg &e) {
         t_err = e.what();
         return BH_EINVAL;
@@ -884,6 +887,66 @@ int bh_csr_build(int64_t n_u, int64_t n_v, int64_t n_e, const int64_t *edge_u, c
     }
     return rc;
 }
+
+struct bh_edge_list {
+    bh::EdgeListResult r;
+};
+
+int bh_edge_list_parse(const char *buf, int64_t len, const char *delim, int64_t delim_len, int32_t has_default,
+                       double default_weight, bh_edge_list **out, int64_t *err_line) {
+    return guarded([&] {
+        if (!out || (!buf && len > 0) || len < 0) throw InvalidArg("null argument");
+        if (delim && delim_len <= 0) throw InvalidArg("empty delimiter");
+        *out = nullptr;
+        if (err_line) *err_line = 0;
+        auto *el = new bh_edge_list();
+        el->r = bh::parse_edge_list(buf, len, delim, delim_len, has_default != 0, default_weight);
+        if (el->r.status != bh::PARSE_OK) {
+            if (err_line) *err_line = el->r.err_line;
+            delete el;
+            throw FallbackNeeded();
+        }
+        *out = el;
+    });
+}
+
+int bh_edge_list_sizes(const bh_edge_list *el, int64_t *n_u, int64_t *n_v, int64_t *u_bytes, int64_t *v_bytes,
+                       int64_t *n_e) {
+    return guarded([&] {
+        if (!el || !n_u || !n_v || !u_bytes || !v_bytes || !n_e) throw InvalidArg("null argument");
+        *n_u = (int64_t)el->r.u_labels.size();
+        *n_v = (int64_t)el->r.v_labels.size();
+        int64_t bu = 0, bv = 0;
+        for (const auto &x : el->r.u_labels) bu += (int64_t)x.size();
+        for (const auto &x : el->r.v_labels) bv += (int64_t)x.size();
+        *u_bytes = bu;
+        *v_bytes = bv;
+        *n_e = (int64_t)el->r.ew.size();
+    });
+}
+
+int bh_edge_list_export(const bh_edge_list *el, char *u_blob, int64_t *u_ends, char *v_blob, int64_t *v_ends,
+                        int64_t *edge_u, int64_t *edge_v, double *edge_w) {
+    return guarded([&] {
+        if (!el || !u_ends || !v_ends || !edge_u || !edge_v || !edge_w) throw InvalidArg("null argument");
+        auto put = [](const std::vector<std::string> &labs, char *blob, int64_t *ends) {
+            int64_t o = 0;
+            for (size_t i = 0; i < labs.size(); i++) {
+                if (!labs[i].empty()) std::memcpy(blob + o, labs[i].data(), labs[i].size());
+                o += (int64_t)labs[i].size();
+                ends[i] = o;
+            }
+        };
+        put(el->r.u_labels, u_blob, u_ends);
+        put(el->r.v_labels, v_blob, v_ends);
+        const size_t n = el->r.ew.size();
+        std::memcpy(edge_u, el->r.eu.data(), n * sizeof(int64_t));
+        std::memcpy(edge_v, el->r.ev.data(), n * sizeof(int64_t));
+        std::memcpy(edge_w, el->r.ew.data(), n * sizeof(double));
+    });
+}
+
+void bh_edge_list_free(bh_edge_list *el) { delete el; }
 
 int bh_query_wait(bh_graph *g) {
     return guarded([&] {
