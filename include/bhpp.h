@@ -16,6 +16,7 @@
  *   topk (bhpp_query.py:206-218) on an arbitrary score vector   -> bh_topk
  *   BipartiteGraph.__init__ canonicalisation (bigraph.py:53-111) -> bh_csr_build
  *   load_edge_list text parsing (bigraph.py:272-350)             -> bh_edge_list_*
+ *   monte_carlo walks of MCSP (baselines.py:108-151)             -> bh_alias_*, bh_monte_carlo
  *
  * Status codes: 0 ok; BH_EINVAL -> ValueError; BH_EUNFLUSHED -> ValueError
  * ("unflushed ledger", push_engine.py:214-217); BH_ECUDA -> RuntimeError;
@@ -176,6 +177,19 @@ int bh_edge_list_sizes(const bh_edge_list *el, int64_t *n_u, int64_t *n_v, int64
 int bh_edge_list_export(const bh_edge_list *el, char *u_blob, int64_t *u_ends, char *v_blob, int64_t *v_ends,
                         int64_t *edge_u, int64_t *edge_v, double *edge_w);
 void bh_edge_list_free(bh_edge_list *el);
+
+/* ---- Monte-Carlo walks (MCSP forward half, baselines.py:45-151) ------------ */
+/* Alias tables of build_alias (per CSR slot, alias = local slot offset) copied
+ * to the graph's device; bh_monte_carlo adds to counts[n_u] (host) the stop
+ * counts of walks [first, first + n) from `source`: stop with probability
+ * alpha before every step, else U -> V -> U with alias draws.  Walk i uses the
+ * Philox4x32-10 stream (seed, i).  Destroy the tables before their graph. */
+typedef struct bh_alias bh_alias;
+int bh_alias_create(bh_graph *g, const double *u_prob, const int64_t *u_alias, const double *v_prob,
+                    const int64_t *v_alias, bh_alias **out);
+int bh_monte_carlo(const bh_alias *a, int64_t source, double alpha, int64_t first, int64_t n, uint64_t seed,
+                   int64_t *counts);
+void bh_alias_destroy(bh_alias *a);
 
 /* ---- measurement ---------------------------------------------------------- */
 typedef struct bh_run_stats {

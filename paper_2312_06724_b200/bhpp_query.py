@@ -285,35 +285,3 @@ def topk(result: QueryResult, k: int, exclude_query: bool = False) -> list[tuple
     return [(labels[i] if labels is not None else str(i), float(scores[i])) for i in idx[:m].tolist()]
 
 
-
-def pisp_query(g, query_u, alpha: float, epsilon: float, dtype: str = "fp64") -> QueryResult:
-    """PISP baseline (reference baselines.py:194-224) on the device kernels.
-
-    Error budget split evenly: the forward half is a fixed-depth device power
-    iteration from e_q (depth = required_iterations(alpha, eps/2, 1)), the
-    backward half a device selective push at eps/2; the returned scores are
-    their sum, with the reference's trace/timing layout and error behaviour.
-    """
-    from .push_engine import selective_push
-
-    if not epsilon > 0:
-        raise ValueError("epsilon must be positive")
-    q = int(query_u) if not isinstance(query_u, str) else g.u_id(query_u)
-    eps_half = 0.5 * epsilon
-    iters = required_iterations(alpha, eps_half, 1.0)
-    e_q = np.zeros(g.u_count)
-    e_q[q] = 1.0
-    clock = [time.perf_counter()]
-    forward = power_iteration(g, e_q, alpha, iters, dtype=dtype)
-    clock.append(time.perf_counter())
-    backward = selective_push(g, q, alpha, eps_half)
-    clock.append(time.perf_counter())
-    bt = dict(backward.phase_trace)
-    bt["terminated_by"] = backward.terminated_by
-    return QueryResult(
-        method="pisp", query_index=q, scores=forward + backward.ledger.estimate, epsilon=epsilon,
-        epsilon_b=eps_half, epsilon_f=eps_half,
-        timing={"forward": clock[1] - clock[0], "backward": clock[2] - clock[1], "total": clock[2] - clock[0]},
-        phase_trace={"forward": {"power_iterations": iters}, "backward": bt},
-        u_labels=g.u_labels, engine={"dtype": dtype},
-    )

@@ -46,6 +46,12 @@ struct EdgeListResult {
 EdgeListResult parse_edge_list(const char *buf, int64_t len, const char *delim, int64_t delim_len, bool has_default,
                                double default_weight);
 
+// walks.cu: Monte-Carlo restart walks over the device graph (MCSP forward half)
+bh_alias *alias_create(bh_graph *g, const double *u_prob, const int64_t *u_alias, const double *v_prob,
+                       const int64_t *v_alias);
+void mc_walks(const bh_alias *al, int64_t source, double alpha, int64_t first, int64_t n, uint64_t seed,
+              int64_t *counts_host);
+
 // csr_build.cu: device canonicalisation of an edge list (bh_csr_build); 1 = duplicate pair.
 int csr_build(int64_t n_u, int64_t n_v, int64_t n_e, const int64_t *edge_u, const int64_t *edge_v,
               const double *edge_w, int64_t *u_indptr, int32_t *u_indices, double *u_weights, int64_t *v_indptr,
@@ -101,6 +107,20 @@ struct bh_graph {
     int64_t device_bytes = 0;
     std::mutex mu;
     void *engines = nullptr;  // engine cache (engine.cu)
+};
+
+// Device copy of the alias tables of one graph (build_alias, baselines.py:76-80).
+struct bh_alias {
+    bh_graph *g = nullptr;  // not owned; the caller destroys the tables before the graph
+    int device = 0;
+    double *u_prob = nullptr, *v_prob = nullptr;
+    int32_t *u_alias = nullptr, *v_alias = nullptr;
+    ~bh_alias() {
+        cudaFree(u_prob);
+        cudaFree(v_prob);
+        cudaFree(u_alias);
+        cudaFree(v_alias);
+    }
 };
 
 namespace bh {

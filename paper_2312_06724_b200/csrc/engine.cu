@@ -948,6 +948,33 @@ int bh_edge_list_export(const bh_edge_list *el, char *u_blob, int64_t *u_ends, c
 
 void bh_edge_list_free(bh_edge_list *el) { delete el; }
 
+int bh_alias_create(bh_graph *g, const double *u_prob, const int64_t *u_alias, const double *v_prob,
+                    const int64_t *v_alias, bh_alias **out) {
+    return guarded([&] {
+        if (!g || !u_prob || !u_alias || !v_prob || !v_alias || !out) throw InvalidArg("null argument");
+        std::lock_guard<std::mutex> lock(g->mu);
+        *out = bh::alias_create(g, u_prob, u_alias, v_prob, v_alias);
+    });
+}
+
+int bh_monte_carlo(const bh_alias *a, int64_t source, double alpha, int64_t first, int64_t n, uint64_t seed,
+                   int64_t *counts) {
+    return guarded([&] {
+        if (!a || !counts) throw InvalidArg("null argument");
+        if (!(alpha > 0.0 && alpha < 1.0)) throw InvalidArg("alpha must lie strictly between 0 and 1");
+        if (source < 0 || source >= a->g->n_u) throw InvalidArg("node index out of range");
+        if (n < 0 || first < 0) throw InvalidArg("bad walk range");
+        std::lock_guard<std::mutex> lock(a->g->mu);
+        bh::mc_walks(a, source, alpha, first, n, seed, counts);
+    });
+}
+
+void bh_alias_destroy(bh_alias *a) {
+    if (!a) return;
+    cudaSetDevice(a->device);
+    delete a;
+}
+
 int bh_query_wait(bh_graph *g) {
     return guarded([&] {
         if (!g) throw InvalidArg("null argument");

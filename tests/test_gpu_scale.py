@@ -130,22 +130,6 @@ def test_scaled_config_refill_fp32_consistent(cfg):
         np.testing.assert_allclose(b.topk_score[i], a.scores[i][a.topk_index[i]], rtol=1e-5, atol=1e-6)
 
 
-def test_pisp_query_matches_oracle_composition():
-    g = config_graph("c1")
-    og = O.OracleGraph(g)
-    for q, eps in ((0, 1e-4), (17, 1e-6)):
-        r = bh.pisp_query(g, q, 0.15, eps)
-        depth = O.required_iterations(0.15, eps / 2, 1.0)
-        start = np.zeros(g.u_count)
-        start[q] = 1.0
-        fwd = og.power_iteration(start, 0.15, depth)
-        led, tr = og.ss_push(q, 0.15, eps / 2, budget=False)
-        np.testing.assert_allclose(r.scores, fwd + led["estimate"], atol=1e-12)
-        assert r.phase_trace["forward"]["power_iterations"] == depth
-        assert r.phase_trace["backward"]["selective_rounds"] == tr["selective_rounds"]
-        assert r.method == "pisp"
-
-
 def test_async_submit_and_gate_match_sync():
     """BH_QUERY_ASYNC + bh_query_wait and the measurement gate give the sync results."""
     import ctypes as C
