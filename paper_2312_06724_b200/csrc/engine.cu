@@ -188,7 +188,8 @@ struct Engine final : EngineBase {
     static constexpr bool WIDE = B >= 32;
     bh_graph *g;
     T *R = nullptr, *P = nullptr, *XV = nullptr, *Y = nullptr;
-    double *EST = nullptr, *OUTS = nullptr;
+    T *EST = nullptr;      // estimates, storage type (fp32 mode: fp32, SURVEY 8(d)'s s bytes)
+    double *OUTS = nullptr;
     Slot *slots = nullptr;
     Finish *fins = nullptr;
     Control *ctl = nullptr;
@@ -294,7 +295,7 @@ struct Engine final : EngineBase {
         P = dalloc<T>(nu * B);
         Y = dalloc<T>(nu * B);
         XV = dalloc<T>(nv * B);
-        EST = dalloc<double>(nu * B);
+        EST = dalloc<T>(nu * B);
         OUTS = dalloc<double>(nu * B);
         slots = dalloc<Slot>(B);
         fins = dalloc<Finish>(B);
@@ -304,7 +305,7 @@ struct Engine final : EngineBase {
         BH_CUDA(cudaMemset(P, 0, nu * B * sizeof(T)));
         BH_CUDA(cudaMemset(Y, 0, nu * B * sizeof(T)));
         BH_CUDA(cudaMemset(XV, 0, nv * B * sizeof(T)));
-        BH_CUDA(cudaMemset(EST, 0, nu * B * sizeof(double)));
+        BH_CUDA(cudaMemset(EST, 0, nu * B * sizeof(T)));
         BH_CUDA(cudaMemset(ctl, 0, sizeof(Control)));
         int sms = 148;
         BH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
@@ -629,7 +630,7 @@ struct Engine final : EngineBase {
         ca.first = 0;
         if (rs.job == BH_JOB_PI_PUSH) {  // seed ledger into slot 0 (query 0 -> slot 0)
             k_col_set<T><<<grid1d(g->n_u), 256, 0, st>>>(R, B, 0, g->n_u, rs.ledger_r);
-            k_col_set<double><<<grid1d(g->n_u), 256, 0, st>>>(EST, B, 0, g->n_u, rs.ledger_est);
+            k_col_set<T><<<grid1d(g->n_u), 256, 0, st>>>(EST, B, 0, g->n_u, rs.ledger_est);
             count_launch(2);
         }
 
@@ -721,7 +722,7 @@ struct Engine final : EngineBase {
 
     void read_ledger(int s, double *r_dev, double *est_dev, cudaStream_t st) override {
         k_col_get<T><<<grid1d(g->n_u), 256, 0, st>>>(R, B, s, g->n_u, r_dev);
-        k_col_get<double><<<grid1d(g->n_u), 256, 0, st>>>(EST, B, s, g->n_u, est_dev);
+        k_col_get<T><<<grid1d(g->n_u), 256, 0, st>>>(EST, B, s, g->n_u, est_dev);
         count_launch(2);
         BH_CUDA(cudaGetLastError());
     }

@@ -185,7 +185,7 @@ struct ElemArgs {
     T *R;
     T *P;
     T *Y;
-    double *EST;
+    T *EST;
     const int32_t *deg_u;
     const double *ws_u;
     const double *inv_ws_u;
@@ -297,15 +297,16 @@ __global__ void __launch_bounds__(ELEM_THREADS, MINB) k_push(ElemArgs<T> a) {
                     }
                 }
                 if (any_act || init_any) {  // est += alpha r on the pushed slots (ledger reset on init)
-                    double ev[EV];
-                    VecIO<double, EV>::ld(a.EST + i, ev);
+                    T ev[EV];
+                    VecIO<T, EV>::ld(a.EST + i, ev);
 #pragma unroll
                     for (int v = 0; v < EV; v++) {
                         const bool init = op[v] == OP_BSEL_INIT;
-                        if (init) ev[v] = 0.0;
-                        if (act[v]) ev[v] += a.alpha * rr[v];
+                        double e = init ? 0.0 : (double)ev[v];
+                        if (act[v]) e += a.alpha * rr[v];
+                        ev[v] = (T)e;
                     }
-                    VecIO<double, EV>::st(a.EST + i, ev);
+                    VecIO<T, EV>::st(a.EST + i, ev);
                 }
                 VecIO<T, EV>::st(a.P + i, pv);
                 if (wrote_r) VecIO<T, EV>::st(a.R + i, rv[k]);

@@ -217,7 +217,7 @@ struct FinalArgs {
     int64_t n_u;
     int32_t B, k, exclude, want_scores;
     int32_t chunk, n_chunks;
-    const double *EST;
+    const T *EST;
     const T *P;
     const double *ws_u;
     double alpha;
@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(TOPK_THREADS) k_finalize(FinalArgs<T> a) {
             const int64_t u0 = (int64_t)c * a.chunk;
             const int64_t u1 = imin64(a.n_u, u0 + a.chunk);
             for (int64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
-                const double est = a.EST[u * B + s];
+                const double est = (double)a.EST[u * B + s];
                 const double ws = a.ws_u[u];
                 double v;
                 if (f.job == BH_JOB_POWER) {
