@@ -136,7 +136,7 @@ def test_c1_unforced_ties_stay_one_sided():
         assert diff.min() >= -1e-10 and diff.max() <= eps + 1e-12
 
 
-@pytest.mark.parametrize("slots", [1, 4, 16, 32, 64])
+@pytest.mark.parametrize("slots", [1, 4, 16, 32, 64, 128])
 def test_c1_every_slot_width(slots):
     d = load("c1")
     g = config_graph("c1")
@@ -149,6 +149,11 @@ def test_c1_every_slot_width(slots):
         np.testing.assert_allclose(res.scores[i], d["scores"][i], atol=ATOL64, rtol=0)
         back, fwd, gamma = split_traces(d["traces"][i])
         assert_traces(res.trace_dicts(i), back, fwd, gamma)
+    r32 = bh.bhpp_query_batch(g, meta, srcs, float(d["eps"]), k=10, dtype="fp32", tie_skip=ties, slots=slots)
+    for i in range(len(srcs)):
+        ref = d["scores"][i]
+        exp = d["topk"][i]
+        np.testing.assert_allclose(r32.topk_score[i], ref[exp], rtol=RTOL32, atol=float(d["eps"]))
 
 
 # -- small random graphs: every kernel ------------------------------------------
