@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import sys
 import threading
 import weakref
 from pathlib import Path
@@ -232,9 +233,25 @@ _graph_cache: dict = {}
 _graph_lock = threading.Lock()
 
 
-def device_graph(g, dtype: str = "fp64", device: int = 0) -> DeviceGraph:
+def current_device() -> int:
+    """CUDA device for calls that do not name one: torch's current device when
+    torch is loaded (one process per GPU calls torch.cuda.set_device), else 0."""
+    t = sys.modules.get("torch")
+    if t is not None:
+        try:
+            if t.cuda.is_available():
+                return int(t.cuda.current_device())
+        except Exception:  # noqa: BLE001 -- no usable torch CUDA context: default device
+            pass
+    return 0
+
+
+def device_graph(g, dtype: str = "fp64", device: int | None = None) -> DeviceGraph:
     """The device store for graph object ``g`` (either package's BipartiteGraph),
-    built once per (graph, dtype, device) and freed with the graph."""
+    built once per (graph, dtype, device) and freed with the graph.  ``device``
+    defaults to the current CUDA device (see current_device)."""
+    if device is None:
+        device = current_device()
     if dtype not in DTYPES:
         raise ValueError(f"dtype must be one of {sorted(set(DTYPES))}")
     key = (id(g), DTYPES[dtype], int(device))
