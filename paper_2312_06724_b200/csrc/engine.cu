@@ -228,6 +228,9 @@ struct Engine final : EngineBase {
     // K1a fused into the U pull's row emit (k_pull_sw<..., SIDE_U, true>): no Y
     // round trip, no combine launch (BH_FUSE_COMBINE=1).
     bool fuse_combine = false;
+    // U pull at 4 blocks/SM where the V pull runs 3 (8-byte lanes): measured at c2,
+    // U 8.2 -> 7.9 ms per step (longer rows, fewer emits per edge than the V side)
+    bool u_minb4 = SwPipe<B, T>::MINB == 3;
 
     // elementwise K1 / K1a: 2 nodes in flight per thread at 3 blocks/SM (fp32) measured
     // fastest at c2 (prep 7.35 -> 6.68 ms per step against 4 nodes at 2 blocks/SM)
@@ -240,6 +243,7 @@ struct Engine final : EngineBase {
     PullFn sw_kernel() const {
         if constexpr (SIDE == SIDE_U) {
             if (fuse_combine) return k_pull_sw<B, T, SIDE_U, true>;
+            if (u_minb4) return k_pull_sw<B, T, SIDE_U, false, SwPipe<B, T>::S, 4>;
         }
         return k_pull_sw<B, T, SIDE>;
     }
@@ -319,6 +323,7 @@ struct Engine final : EngineBase {
         }
         if (const char *m = getenv("BH_PULL_SW")) pull_sw = atoi(m) != 0;
         if (const char *m = getenv("BH_PULL_TMA")) pull_tma = WIDE && atoi(m) != 0;
+        if (const char *m = getenv("BH_U_MINB4")) u_minb4 = atoi(m) != 0;
         // opt-in: measured slower at c2 (U pull 8.1 -> 19.1 ms/step, K1a 3.1 ms saved):
         // the per-row combine exposes the r_u row latency inside the gather loop
         if (const char *m = getenv("BH_FUSE_COMBINE"))
