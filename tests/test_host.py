@@ -222,3 +222,29 @@ def test_mc_walk_count():
     for bad in ((0.0, 1e-6, 10), (0.1, 0.0, 10), (0.1, 1e-6, 0)):
         with pytest.raises(ValueError):
             bh.mc_walk_count(*bad)
+
+
+def test_host_side_abi_error_paths():
+    """Entry points that need no GPU report bad arguments with status codes and
+    bh_last_error, never by crashing (status -> exception mapping of _capi.check)."""
+    import ctypes as C
+
+    lib = _capi.lib()
+    h = C.c_void_p()
+    err = C.c_int64(0)
+    assert lib.bh_edge_list_parse(None, 5, None, 0, 0, 0.0, C.byref(h), C.byref(err)) == _capi.BH_EINVAL
+    assert b"null" in lib.bh_last_error()
+    assert lib.bh_edge_list_parse(b"a x 1\n", 6, b"", 0, 0, 0.0, C.byref(h), C.byref(err)) == _capi.BH_EINVAL
+    assert lib.bh_edge_list_parse(b"a x 1\nb y\n", 10, None, 0, 0, 0.0, C.byref(h), C.byref(err)) == _capi.BH_EFALLBACK
+    assert err.value == 2  # the two-column line without a default weight
+    assert lib.bh_edge_list_parse(b"a x 1\n", 6, None, 0, 0, 0.0, C.byref(h), C.byref(err)) == _capi.BH_OK
+    n = [C.c_int64() for _ in range(5)]
+    assert lib.bh_edge_list_sizes(h, *[C.byref(x) for x in n]) == _capi.BH_OK
+    assert [x.value for x in n] == [1, 1, 1, 1, 1]
+    lib.bh_edge_list_free(h)
+    assert lib.bh_monte_carlo(None, 0, 0.15, 0, 1, 0, None) == _capi.BH_EINVAL
+    assert lib.bh_query_wait(None) == _capi.BH_EINVAL
+    with pytest.raises(ValueError):
+        _capi.check(_capi.BH_EINVAL)
+    with pytest.raises(MemoryError):
+        _capi.check(_capi.BH_ENOMEM)
