@@ -129,19 +129,6 @@ __device__ __forceinline__ bool op_is_fwd(int op) { return op == OP_FENTRY || op
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-template <int BYTES>
-__device__ __forceinline__ void cp_async(uint32_t dst, const void *src) {
-    if constexpr (BYTES == 16)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
-    else if constexpr (BYTES == 8)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src) : "memory");
-    else
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
-
 // Per-slot constants staged in shared memory by the round kernels.
 struct SlotSmem {
     int32_t op[MAX_B];
@@ -442,18 +429,6 @@ enum : int { SIDE_V = 0, SIDE_U = 1 };
 constexpr int PULL_THREADS = 256;
 constexpr int PULL_WARPS = PULL_THREADS / 32;
 
-template <int B, typename T>
-struct Pipe {
-    static constexpr int ROW = B * (int)sizeof(T);                 // operand row bytes
-    static constexpr int CHUNKS = ROW / 16;                        // 16-byte pieces per row
-    static constexpr int LPE = CHUNKS < 32 ? CHUNKS : 32;          // lanes copying one edge
-    static constexpr int CPE = CHUNKS / LPE;                       // copy instructions per edge
-    static constexpr int EPI = 32 / LPE;                           // edges per issue step
-    static constexpr int S = (4096 / ROW) < EPI ? EPI : (4096 / ROW);  // ring depth (edges)
-    static constexpr int VEC = B / 32;                             // slots per lane
-    static constexpr int WARP_SMEM = S * ROW + S * (int)sizeof(T);
-};
-
 template <typename T>
 struct PullArgs {
     const int64_t *indptr;
@@ -488,23 +463,6 @@ __device__ __forceinline__ uint64_t gtimer() {
     return t;
 }
 
-template <int B, typename T, int SIDE, int VEC>
-__device__ __forceinline__ void pull_row_final(const PullArgs<T> &a, const int32_t *s_op, int64_t row, int32_t deg,
-                                               int slot0, const double (&acc)[VEC], int64_t (&np)[VEC]) {
-    T out[VEC];
-    if constexpr (SIDE == SIDE_V) {
-#pragma unroll
-        for (int v = 0; v < VEC; v++) {
-            out[v] = (T)(a.one_minus_alpha * acc[v]);
-            if (op_is_push(s_op[slot0 + v]) && (double)out[v] > 0.0) np[v] += deg;
-        }
-    } else {
-#pragma unroll
-        for (int v = 0; v < VEC; v++) out[v] = (T)acc[v];
-    }
-    VecIO<T, VEC>::st(a.Y + row * B + slot0, out);
-}
-
 template <int VEC>
 struct DVec {
     double v[VEC];
@@ -512,54 +470,6 @@ struct DVec {
 template <int VEC>
 struct IVec {
     int64_t v[VEC];
-};
-
-// A row cut by this warp's range boundary: publish the fp64 partial; the last
-// warp to arrive adds all partials in warp order and finishes the row.  Kept
-// out of line (rare path) so the streaming loop keeps its registers; returns
-// the n_p increments of the finished row (V pull).
-template <int B, typename T, int SIDE, int VEC>
-__device__ __noinline__ IVec<VEC> pull_cut_row(const PullArgs<T> &a, const int32_t *s_op, int ci, int pi, int slot0,
-                                               DVec<VEC> acc) {
-    const int lane = threadIdx.x & 31;
-    IVec<VEC> inc;
-#pragma unroll
-    for (int v = 0; v < VEC; v++) inc.v[v] = 0;
-#pragma unroll
-    for (int v = 0; v < VEC; v++) a.scratch[(int64_t)pi * B + slot0 + v] = acc.v[v];
-    __threadfence();
-    __syncwarp();
-    const CutRow cr = a.cuts[ci];
-    int last = 0;
-    if (lane == 0) last = atomicAdd(a.cut_count + ci, 1) == cr.n_parts - 1;
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (!last) return inc;
-    __threadfence();
-    double tot[VEC];
-#pragma unroll
-    for (int v = 0; v < VEC; v++) tot[v] = 0.0;
-    for (int p = 0; p < cr.n_parts; p++)
-#pragma unroll
-        for (int v = 0; v < VEC; v++) tot[v] += __ldcg(a.scratch + (int64_t)(cr.first_part + p) * B + slot0 + v);
-    const int32_t deg = (int32_t)(__ldg(a.indptr + cr.row + 1) - __ldg(a.indptr + cr.row));
-    pull_row_final<B, T, SIDE, VEC>(a, s_op, cr.row, deg, slot0, tot, inc.v);
-    if (lane == 0) a.cut_count[ci] = 0;
-    return inc;
-}
-
-// fp64 mode accumulates each product with DFMA.  fp32 mode multiplies and adds
-// in fp32 over at most FLUSH consecutive edges of a row, then adds that short
-// partial into the fp64 row sum (SURVEY.md sec. 7 hard part 2: fp32 storage
-// with fp64 row accumulation; the chunked form avoids a conversion per edge).
-template <typename T>
-struct Acc;
-template <>
-struct Acc<double> {
-    static constexpr int FLUSH = 1 << 30;
-};
-template <>
-struct Acc<float> {
-    static constexpr int FLUSH = 16;
 };
 
 // Operand-row gather.  Plain coherent loads (ld.global, L1-cached): the
