@@ -199,7 +199,7 @@ def bhpp_query(g, meta: IndexMeta, query_u, epsilon: float, round_hook=None, dty
 
 def bhpp_query_batch(g, meta: IndexMeta, sources, epsilon: float, k: int | None = 50,
                      exclude_query: bool = False, dtype: str = "fp32", return_scores: bool = False,
-                     slots: int | None = None, tie_skip=None, stream=None) -> BatchResult:
+                     slots: int | None = None, tie_skip=None, stream=None, device: int | None = None) -> BatchResult:
     """SS-BI-PUSH for many sources at once on the device.
 
     Equivalent to ``[topk(bhpp_query(g, meta, s, epsilon), k, exclude_query)
@@ -216,7 +216,7 @@ def bhpp_query_batch(g, meta: IndexMeta, sources, epsilon: float, k: int | None 
     if kk < 0:
         raise ValueError("k must be positive")
     kk = min(kk, g.u_count)
-    dg = _capi.device_graph(g, dtype)
+    dg = _capi.device_graph(g, dtype, device)
     n_q = src.size
     prm = _capi.QueryParams(alpha=meta.alpha, lam=meta.lam, eps_b=eps_b, eps_f=eps_f, k=kk,
                             exclude_query=int(bool(exclude_query)), want_scores=int(bool(return_scores)),

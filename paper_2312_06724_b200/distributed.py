@@ -1,5 +1,10 @@
 """Query-batch sharding over the GPUs of one node.
 
+Two forms: ``bhpp_query_sharded`` for one process per GPU (torchrun, NCCL
+all-gather), and ``bhpp_query_multi`` for one process driving several GPUs
+(a host thread per device; the C ABI releases the GIL, results are merged on
+the host).
+
 Queries are independent (one ledger per query, a read-only graph), so the
 only multi-GPU structure is: replicate the device graph store on every rank,
 give rank r the interleaved shard ``sources[r::world]`` (interleaving spreads
@@ -86,3 +91,52 @@ def bhpp_query_sharded(g, meta, sources, epsilon: float, k: int = 50, exclude_qu
 
 def trace_dtype():
     return _capi.TRACE_DTYPE
+
+
+def bhpp_query_multi(g, meta, sources, epsilon: float, k: int = 50, exclude_query: bool = False,
+                     dtype: str = "fp32", slots: int | None = None, devices=None,
+                     return_scores: bool = False) -> BatchResult:
+    """bhpp_query_batch sharded over ``devices`` (default: every visible GPU)
+    from one process: device d runs the interleaved shard sources[i::n] on its
+    own replica of the graph store, concurrently; the result is in the order of
+    ``sources``, identical to a single-device call."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    if devices is None:
+        import torch
+
+        devices = list(range(max(1, torch.cuda.device_count())))
+    devices = [int(d) for d in devices]
+    src = np.asarray(sources, dtype=np.int64)
+    n = len(devices)
+    for d in set(devices):  # build each replica once, before the threads race for it
+        _capi.device_graph(g, dtype, d)
+
+    def run(i):
+        mine = shard(src, i, n)
+        if mine.size == 0:
+            return None
+        return bhpp_query_batch(g, meta, mine, epsilon, k=k, exclude_query=exclude_query, dtype=dtype,
+                                return_scores=return_scores, slots=slots, device=devices[i])
+
+    with ThreadPoolExecutor(max_workers=n) as pool:
+        parts = list(pool.map(run, range(n)))
+    first = next(p for p in parts if p is not None)
+    kk = first.k
+    idx = np.full((src.size, max(kk, 1)), -1, dtype=np.int32)[:, :kk]
+    sc = np.zeros((src.size, max(kk, 1)))[:, :kk]
+    tr = np.zeros(src.size, dtype=_capi.TRACE_DTYPE)
+    scores = np.empty((src.size, g.u_count)) if return_scores else None
+    for i, part in enumerate(parts):
+        if part is None:
+            continue
+        rows = np.arange(i, src.size, n)
+        idx[rows] = part.topk_index
+        sc[rows] = part.topk_score
+        tr[rows] = part.traces
+        if return_scores:
+            scores[rows] = part.scores
+    return BatchResult(sources=src.astype(np.int32), epsilon=epsilon, epsilon_b=first.epsilon_b,
+                       epsilon_f=first.epsilon_f, k=kk, topk_index=idx, topk_score=sc, traces=tr, scores=scores,
+                       timing={"total": max(p.timing["total"] for p in parts if p is not None)}, dtype=dtype,
+                       meta={"devices": devices})

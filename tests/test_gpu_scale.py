@@ -166,3 +166,21 @@ def test_async_submit_and_gate_match_sync():
     again = bh.bhpp_query_batch(g, meta, src, 1e-7, k=20, dtype="fp32")
     np.testing.assert_array_equal(again.topk_index, ref.topk_index)
     np.testing.assert_array_equal(ti.cpu().numpy(), ref.topk_index)
+
+
+def test_single_process_multi_device_sharding_matches_one_call():
+    """bhpp_query_multi merges interleaved shards back into source order; with
+    the devices of this box (here one GPU listed three times) it must equal one call."""
+    from paper_2312_06724_b200.distributed import bhpp_query_multi
+
+    g = config_graph("c2s")
+    meta = bh.build_index_meta(g, 0.15)
+    src = np.random.default_rng(11).choice(g.u_count, 13, replace=False)
+    # same slot width everywhere -> same engine plan -> bitwise-equal per-query results
+    one = bh.bhpp_query_batch(g, meta, src, 1e-7, k=20, dtype="fp32", return_scores=True, slots=16)
+    multi = bhpp_query_multi(g, meta, src, 1e-7, k=20, dtype="fp32", devices=[0, 0, 0], return_scores=True,
+                             slots=16)
+    np.testing.assert_array_equal(multi.topk_index, one.topk_index)
+    np.testing.assert_array_equal(multi.topk_score, one.topk_score)
+    np.testing.assert_array_equal(multi.scores, one.scores)
+    assert multi.traces.tobytes() == one.traces.tobytes()
