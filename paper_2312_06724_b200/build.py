@@ -39,14 +39,24 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not _stale():
         return LIB
     LIB_DIR.mkdir(exist_ok=True)
+    obj_dir = LIB_DIR / "obj"
+    obj_dir.mkdir(exist_ok=True)
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [
-        nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
+    flags = [
+        *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
         "-Xcompiler", "-O2", "--expt-relaxed-constexpr", "-I", str(INCLUDE),
         *(["-Xptxas", "-v"] if verbose else []),
-        "-o", str(tmp), *[str(CSRC / s) for s in SOURCES],
     ]
-    subprocess.run(cmd, check=True)
+    # one nvcc per translation unit, in parallel, then one link
+    procs, objs = [], []
+    for src in SOURCES:
+        obj = obj_dir / (src + ".o")
+        objs.append(obj)
+        procs.append((src, subprocess.Popen([nvcc(), *flags, "-c", "-o", str(obj), str(CSRC / src)])))
+    failed = [src for src, p in procs if p.wait() != 0]
+    if failed:
+        raise subprocess.CalledProcessError(1, f"nvcc {' '.join(failed)}")
+    subprocess.run([nvcc(), *ARCH, "-shared", "-o", str(tmp), *[str(o) for o in objs]], check=True)
     os.replace(tmp, LIB)
     return LIB
 

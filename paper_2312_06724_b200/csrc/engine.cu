@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <atomic>
 #include <cmath>
+#include <chrono>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -1136,13 +1137,37 @@ int bh_query_batch(bh_graph *g, const bh_query_params *p, const int32_t *sources
         }
         unsigned char *h_tr = c.h_stage, *h_ti = h_tr + b_tr, *h_ts = h_ti + b_ti;
         rs.async = true;
+        // BH_TRACE_E2E=1: host-path phase times on stderr (diagnostic)
+        static const bool trace_e2e = getenv("BH_TRACE_E2E") != nullptr;
+        cudaEvent_t tev[3] = {nullptr, nullptr, nullptr};
+        auto now_us = [] {
+            return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+        };
+        double th[4] = {now_us(), 0, 0, 0};
+        if (trace_e2e) {
+            for (auto &x : tev) BH_CUDA(cudaEventCreate(&x));
+            BH_CUDA(cudaEventRecord(tev[0], st));
+        }
         e.run(rs, st);
+        if (trace_e2e) BH_CUDA(cudaEventRecord(tev[1], st));
+        th[1] = now_us();
         BH_CUDA(cudaMemcpyAsync(h_tr, c.d_trace, b_tr, cudaMemcpyDeviceToHost, st));
         if (b_ti) BH_CUDA(cudaMemcpyAsync(h_ti, c.d_tk_idx, b_ti, cudaMemcpyDeviceToHost, st));
         if (b_ts) BH_CUDA(cudaMemcpyAsync(h_ts, c.d_tk_sc, b_ts, cudaMemcpyDeviceToHost, st));
         if (b_sc) BH_CUDA(cudaMemcpyAsync(scores, c.d_scores, b_sc, cudaMemcpyDeviceToHost, st));
+        if (trace_e2e) BH_CUDA(cudaEventRecord(tev[2], st));
+        th[2] = now_us();
         e.finish();  // synchronises the stream (graph path), checks termination
         BH_CUDA(cudaStreamSynchronize(st));
+        th[3] = now_us();
+        if (trace_e2e) {
+            float d_graph = 0.f, d_out = 0.f;
+            BH_CUDA(cudaEventElapsedTime(&d_graph, tev[0], tev[1]));
+            BH_CUDA(cudaEventElapsedTime(&d_out, tev[1], tev[2]));
+            fprintf(stderr, "[bh e2e] host: launch %.1f us, copies enqueued %.1f us, wait %.1f us; device: batch %.3f ms, "
+                    "outputs %.3f ms\n", th[1] - th[0], th[2] - th[1], th[3] - th[2], d_graph, d_out);
+            for (auto &x : tev) cudaEventDestroy(x);
+        }
         std::memcpy(trace, h_tr, b_tr);
         if (b_ti) std::memcpy(topk_idx, h_ti, b_ti);
         if (b_ts) std::memcpy(topk_score, h_ts, b_ts);

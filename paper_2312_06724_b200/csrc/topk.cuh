@@ -29,7 +29,7 @@ constexpr int TOPK_MAX = 1024;
 struct SelectSmem {
     uint32_t hist[256];
     uint32_t wsum[TOPK_THREADS / 32];
-    unsigned long long cnt;
+    uint32_t cnt;  // valid elements (32-bit: a 64-bit shared atomicAdd is a CAS loop)
     uint64_t prefix;
     int64_t krem;
     int32_t out_n;
@@ -71,30 +71,55 @@ __device__ __forceinline__ void pick_digit(SelectSmem &sm, uint64_t prefix, int 
     __syncthreads();
 }
 
-constexpr int SEL_ITEMS = 8;  // candidates cached per thread (n <= SEL_ITEMS * TOPK_THREADS)
+constexpr int SEL_ITEMS = 8;         // candidates cached per thread in a chunk select
+constexpr int SEL_ITEMS_MERGE = 16;  // ... and in the merge of the chunk candidates
 
-// Select exactly min(k, #valid) elements that are largest under (key desc,
-// idx asc) among n candidates given by acc(i, &key, &idx) -> valid.  Output
-// order is arbitrary.  All threads of the block must call it; blockDim must be
-// TOPK_THREADS.  Up to SEL_ITEMS * TOPK_THREADS candidates are read once into
-// registers; larger inputs are re-read through acc on every pass.
-template <class Acc>
+// Histogram increment aggregated per warp: lanes with the same digit are
+// counted by one shared-memory atomic (the leading digits of positive scores
+// are shared by almost every element, and per-element atomics on one bin
+// serialise).  Every lane of the warp must call it (p = whether it counts).
+__device__ __forceinline__ void hist_add_warp(uint32_t *hist, bool p, uint32_t d) {
+    const unsigned act = __ballot_sync(0xffffffffu, p);
+    if (p) {
+        const unsigned peers = __match_any_sync(act, d);
+        if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(hist + d, (uint32_t)__popc(peers));
+    }
+}
+
+// Output slot for an emitted element, one shared atomic per warp; every lane
+// calls it.  Returns -1 when p is false.
+__device__ __forceinline__ int emit_slot_warp(int32_t *counter, bool p) {
+    const unsigned act = __ballot_sync(0xffffffffu, p);
+    if (act == 0) return -1;
+    const int lane = threadIdx.x & 31;
+    const int lead = __ffs(act) - 1;
+    int base = 0;
+    if (lane == lead) base = atomicAdd(counter, __popc(act));
+    base = __shfl_sync(0xffffffffu, base, lead);
+    return p ? base + __popc(act & ((1u << lane) - 1u)) : -1;
+}
+
+// Top-k of n keyed elements by MSD radix select on the 64-bit order keys, ties
+// on the key broken by ascending index (radix select on the index bits).
+// acc(i, key, idx) -> valid.  The block size must be a multiple of 32; every
+// thread calls it.  Up to ITEMS * blockDim elements are cached in registers.
+template <int ITEMS = SEL_ITEMS, class Acc>
 __device__ int64_t block_select(int64_t n, int64_t k, Acc acc, SelectSmem &sm, uint64_t *out_key,
                                 int64_t *out_idx) {
     const int tid = threadIdx.x, nt = blockDim.x;
-    const bool cached = n <= (int64_t)SEL_ITEMS * nt;
-    uint64_t ck[SEL_ITEMS];
-    int64_t ci[SEL_ITEMS];
-    bool cv[SEL_ITEMS];
+    const bool cached = n <= (int64_t)ITEMS * nt;
+    uint64_t ck[ITEMS];
+    int64_t ci[ITEMS];
+    bool cv[ITEMS];
     if (tid == 0) {
         sm.cnt = 0;
         sm.out_n = 0;
     }
     __syncthreads();
-    unsigned long long c = 0;
+    uint32_t c = 0;
     if (cached) {
 #pragma unroll
-        for (int j = 0; j < SEL_ITEMS; j++) {
+        for (int j = 0; j < ITEMS; j++) {
             const int64_t i = tid + (int64_t)j * nt;
             cv[j] = i < n && acc(i, ck[j], ci[j]);
             c += cv[j];
@@ -106,45 +131,39 @@ __device__ int64_t block_select(int64_t n, int64_t k, Acc acc, SelectSmem &sm, u
             c += acc(i, kk, ii);
         }
     }
-    // visit every valid candidate: f(key, idx)
+    // f(valid, key, idx) on every element, all lanes of a warp in step
     auto each = [&](auto f) {
         if (cached) {
 #pragma unroll
-            for (int j = 0; j < SEL_ITEMS; j++)
-                if (cv[j]) f(ck[j], ci[j]);
+            for (int j = 0; j < ITEMS; j++) f(cv[j], ck[j], ci[j]);
         } else {
-            for (int64_t i = tid; i < n; i += nt) {
-                uint64_t kk;
-                int64_t ii;
-                if (acc(i, kk, ii)) f(kk, ii);
+            for (int64_t b = 0; b < n; b += nt) {
+                const int64_t i = b + tid;
+                uint64_t kk = 0;
+                int64_t ii = 0;
+                const bool v = i < n && acc(i, kk, ii);
+                f(v, kk, ii);
             }
         }
     };
-    atomicAdd(&sm.cnt, c);
+    c = __reduce_add_sync(0xffffffffu, c);
+    if ((tid & 31) == 0) atomicAdd(&sm.cnt, c);
     __syncthreads();
     const int64_t n_valid = (int64_t)sm.cnt;
-    if (n_valid <= k) {
-        each([&](uint64_t kk, int64_t ii) {
-            const int p = atomicAdd(&sm.out_n, 1);
-            out_key[p] = kk;
-            out_idx[p] = ii;
-        });
-        __syncthreads();
-        return n_valid;
-    }
-    // up to 8 passes over the key bits, most significant digit first; stop as soon
-    // as the bin holding the k-th element is taken whole (then the selection is
-    // exactly {key : key & mask >= prefix}, k elements)
     auto emit_if = [&](auto pred) {
-        each([&](uint64_t kk, int64_t ii) {
-            if (pred(kk, ii)) {
-                const int p = atomicAdd(&sm.out_n, 1);
+        each([&](bool v, uint64_t kk, int64_t ii) {
+            const int p = emit_slot_warp(&sm.out_n, v && pred(kk, ii));
+            if (p >= 0) {
                 out_key[p] = kk;
                 out_idx[p] = ii;
             }
         });
         __syncthreads();
     };
+    if (n_valid <= k) {
+        emit_if([](uint64_t, int64_t) { return true; });
+        return n_valid;
+    }
     uint64_t prefix = 0, mask = 0;
     if (tid == 0) {
         sm.krem = k;
@@ -153,8 +172,8 @@ __device__ int64_t block_select(int64_t n, int64_t k, Acc acc, SelectSmem &sm, u
     for (int shift = 56; shift >= 0; shift -= 8) {
         sm.hist[tid] = 0;
         __syncthreads();
-        each([&](uint64_t kk, int64_t) {
-            if ((kk & mask) == prefix) atomicAdd(&sm.hist[(kk >> shift) & 255u], 1u);
+        each([&](bool v, uint64_t kk, int64_t) {
+            hist_add_warp(sm.hist, v && (kk & mask) == prefix, (uint32_t)(kk >> shift) & 255u);
         });
         __syncthreads();
         pick_digit(sm, prefix, shift, true);
@@ -166,13 +185,13 @@ __device__ int64_t block_select(int64_t n, int64_t k, Acc acc, SelectSmem &sm, u
         }
     }
     const uint64_t kstar = prefix;
-    // ties at kstar: the smallest indices (4 passes over 32-bit indices)
     uint64_t ipre = 0, imask = 0;
     for (int shift = 24; shift >= 0; shift -= 8) {
         sm.hist[tid] = 0;
         __syncthreads();
-        each([&](uint64_t kk, int64_t ii) {
-            if (kk == kstar && (((uint64_t)ii) & imask) == ipre) atomicAdd(&sm.hist[(((uint64_t)ii) >> shift) & 255u], 1u);
+        each([&](bool v, uint64_t kk, int64_t ii) {
+            hist_add_warp(sm.hist, v && kk == kstar && (((uint64_t)ii) & imask) == ipre,
+                          (uint32_t)(((uint64_t)ii) >> shift) & 255u);
         });
         __syncthreads();
         pick_digit(sm, ipre, shift, false);
@@ -186,8 +205,6 @@ __device__ int64_t block_select(int64_t n, int64_t k, Acc acc, SelectSmem &sm, u
     return k;
 }
 
-// Bitonic sort of P (power of two) (key, idx) pairs in shared memory into
-// (key desc, idx asc) order.
 __device__ void block_sort_pairs(uint64_t *key, int64_t *idx, int P) {
     for (int size = 2; size <= P; size <<= 1) {
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
@@ -258,7 +275,7 @@ __device__ void merge_slot(const FinalArgs<T> &a, int s, const Finish &f, Select
         sidx[i] = INT64_MAX;
     }
     __syncthreads();
-    const int64_t m = block_select((int64_t)a.n_chunks * a.k, a.k, acc, sm, skey, sidx);
+    const int64_t m = block_select<SEL_ITEMS_MERGE>((int64_t)a.n_chunks * a.k, a.k, acc, sm, skey, sidx);
     block_sort_pairs(skey, sidx, P);
     for (int i = threadIdx.x; i < a.k; i += blockDim.x) {
         const bool ok = i < m;
@@ -366,7 +383,7 @@ __global__ void __launch_bounds__(TOPK_THREADS) k_vec_topk_merge(int64_t n_cand,
         sidx[i] = INT64_MAX;
     }
     __syncthreads();
-    const int64_t m = block_select(n_cand, k, acc, sm, skey, sidx);
+    const int64_t m = block_select<SEL_ITEMS_MERGE>(n_cand, k, acc, sm, skey, sidx);
     block_sort_pairs(skey, sidx, P);
     for (int i = threadIdx.x; i < m; i += blockDim.x) {
         out_idx[i] = sidx[i];
