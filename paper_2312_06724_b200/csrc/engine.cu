@@ -211,7 +211,7 @@ struct Engine final : EngineBase {
     std::vector<unsigned char> graph_key;
     size_t pull_smem = 0;
     int fin_chunk = SEL_ITEMS * TOPK_THREADS, n_chunks = 1;  // one register-cached select per chunk
-    int grid_elem = 1, grid_k5 = 1;
+    int grid_elem = 1, grid_comb = 1, grid_k5 = 1;  // K1 / K1a grids (one resident wave each)
 
     // Pull mapping per side: half-warp workers (two operand rows per warp
     // instruction) when rows are long enough that the per-row emit is
@@ -236,8 +236,40 @@ struct Engine final : EngineBase {
     // elementwise K1 / K1a: 2 nodes in flight per thread at 3 blocks/SM (fp32) measured
     // fastest at c2 (prep 7.35 -> 6.68 ms per step against 4 nodes at 2 blocks/SM)
     using ElemFn = void (*)(ElemArgs<T>);
-    ElemFn push_kernel() const { return k_push<B, T, 2, (sizeof(T) == 4 ? 3 : 2)>; }
-    ElemFn combine_kernel() const { return k_combine<B, T, 2, (sizeof(T) == 4 ? 3 : 2)>; }
+    // K1 / K1a geometry (nodes in flight per thread, blocks per SM): one node at
+    // 4 blocks/SM measured fastest for fp32 at c2 (prep 6.5 -> 5.6 ms per step
+    // against 2 nodes at 3 blocks/SM); tuning override BH_ELEM_PUSH /
+    // BH_ELEM_COMBINE = "UNR,MINB" (wide engines only).
+    int push_cfg = 0, comb_cfg = 0;
+    static constexpr const char *ELEM_CFGS[] = {"", "2,2", "4,2", "1,4", "1,3", "1,5", "1,6", "2,3", "2,4"};
+    template <template <int, typename, int, int> class K>
+    static ElemFn elem_variant(int cfg) {
+        if constexpr (B < 32) cfg = 0;  // tuning variants only for the wide engines
+        switch (cfg) {
+            case 1: return K<B, T, 2, 2>::fn;
+            case 2: return K<B, T, 4, 2>::fn;
+            case 3: return K<B, T, 1, 4>::fn;
+            case 4: return K<B, T, 1, 3>::fn;
+            case 5: return K<B, T, 1, 5>::fn;
+            case 6: return K<B, T, 1, 6>::fn;
+            case 7: return K<B, T, 2, 3>::fn;
+            case 8: return K<B, T, 2, 4>::fn;
+            default: return sizeof(T) == 4 ? K<B, T, 1, 4>::fn : K<B, T, 2, 2>::fn;
+        }
+    }
+    template <int B_, typename T_, int U_, int M_>
+    struct PushK { static constexpr ElemFn fn = k_push<B_, T_, U_, M_>; };
+    template <int B_, typename T_, int U_, int M_>
+    struct CombK { static constexpr ElemFn fn = k_combine<B_, T_, U_, M_>; };
+    static int elem_cfg_from_env(const char *name) {
+        const char *m = getenv(name);
+        if (!m) return 0;
+        for (int i = 1; i < (int)(sizeof(ELEM_CFGS) / sizeof(ELEM_CFGS[0])); i++)
+            if (std::string(m) == ELEM_CFGS[i]) return i;
+        return 0;
+    }
+    ElemFn push_kernel() const { return elem_variant<PushK>(push_cfg); }
+    ElemFn combine_kernel() const { return elem_variant<CombK>(comb_cfg); }
 
     using PullFn = void (*)(PullArgs<T>);
     template <int SIDE>
@@ -283,10 +315,10 @@ struct Engine final : EngineBase {
 
             const bool half = side == SIDE_V ? half_v : half_u;
             if (side == SIDE_V)
-                *fn = half ? (void *)k_pull_half<B, T, SIDE_V>
+                *fn = half ? (pull_sw ? (void *)k_pull_swh<B, T, SIDE_V> : (void *)k_pull_half<B, T, SIDE_V>)
                            : (pull_sw ? (void *)sw_kernel<SIDE_V>() : (void *)k_pull<B, T, SIDE_V>);
             else
-                *fn = half ? (void *)k_pull_half<B, T, SIDE_U>
+                *fn = half ? (pull_sw ? (void *)k_pull_swh<B, T, SIDE_U> : (void *)k_pull_half<B, T, SIDE_U>)
                            : (pull_sw ? (void *)sw_kernel<SIDE_U>() : (void *)k_pull<B, T, SIDE_U>);
         } else {
             *fn = side == SIDE_V ? (void *)k_pull_small<B, T, SIDE_V> : (void *)k_pull_small<B, T, SIDE_U>;
@@ -353,19 +385,21 @@ struct Engine final : EngineBase {
             const bool half = side == SIDE_V ? half_v : half_u;
             build_plan(sd, g->n_e, (int)grid * PULL_WARPS * (half ? 2 : 1), pl);
         }
+        push_cfg = elem_cfg_from_env("BH_ELEM_PUSH");
+        comb_cfg = elem_cfg_from_env("BH_ELEM_COMBINE");
         {  // one resident wave of the elementwise kernels
             int occ_p = 1, occ_c = 1;
             BH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, push_kernel(), ELEM_THREADS, 0));
             BH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, combine_kernel(), ELEM_THREADS, 0));
-            int occ = std::max(1, std::min(occ_p, occ_c));
-            if (const char *m = getenv("BH_ELEM_BLOCKS_PER_SM")) occ = std::max(1, atoi(m));
-            grid_elem = grid1d(nu * (B / ElemGeo<B>::EV), ELEM_THREADS, occ * sms);
+            if (const char *m = getenv("BH_ELEM_BLOCKS_PER_SM")) occ_p = occ_c = atoi(m);
+            grid_elem = grid1d(nu * (B / ElemGeo<B>::EV), ELEM_THREADS, std::max(1, occ_p) * sms);
+            grid_comb = grid1d(nu * (B / ElemGeo<B>::EV), ELEM_THREADS, std::max(1, occ_c) * sms);
         }
         n_chunks = (int)((nu + fin_chunk - 1) / fin_chunk);
         grid_k5 = (int)std::min<int64_t>((int64_t)n_chunks * std::min(B, 16), 16 * sms);
         part.rows_k1 = grid_elem;
         part.rows_k2 = half_v ? (plan_v.n_warps + 1) / 2 : plan_v.n_warps;
-        part.rows_k3 = fuse_combine ? plan_u.n_warps + plan_u.n_cuts : grid_elem;
+        part.rows_k3 = fuse_combine ? plan_u.n_warps + plan_u.n_cuts : grid_comb;
         part.cnt = dalloc<int64_t>((size_t)grid_elem * B);
         part.np_u = dalloc<int64_t>((size_t)grid_elem * B);
         part.lmass = dalloc<double>((size_t)grid_elem * B);
@@ -442,7 +476,8 @@ struct Engine final : EngineBase {
         k_cap = k;
     }
 
-    PullArgs<T> pull_args(int side, double one_minus_alpha) {
+    PullArgs<T> pull_args(int side, double alpha) {
+        const double one_minus_alpha = 1.0 - alpha;
         PullArgs<T> a{};
         const Side &sd = side == SIDE_V ? g->V : g->U;
         const SidePlan &pl = side == SIDE_V ? plan_v : plan_u;
@@ -465,6 +500,8 @@ struct Engine final : EngineBase {
         if (side == SIDE_U && fuse_combine) {
             a.R = R;
             a.Pn = P;
+            a.EST = EST;
+            a.alpha = alpha;
             a.ws_u = g->ws_u;
             a.inv_ws_u = g->inv_ws_u;
             a.p_any = part.any;
@@ -489,11 +526,13 @@ struct Engine final : EngineBase {
 
             const bool half = side == SIDE_V ? half_v : half_u;
             if (side == SIDE_V) {
-                if (half) launch_pdl(k_pull_half<B, T, SIDE_V>, grid, PULL_THREADS, pull_smem, st, a);
+                if (half && pull_sw) launch_pdl(k_pull_swh<B, T, SIDE_V>, grid, PULL_THREADS, pull_smem, st, a);
+                else if (half) launch_pdl(k_pull_half<B, T, SIDE_V>, grid, PULL_THREADS, pull_smem, st, a);
                 else if (pull_sw) launch_pdl(sw_kernel<SIDE_V>(), grid, PULL_THREADS, pull_smem, st, a);
                 else launch_pdl(k_pull<B, T, SIDE_V>, grid, PULL_THREADS, pull_smem, st, a);
             } else {
-                if (half) launch_pdl(k_pull_half<B, T, SIDE_U>, grid, PULL_THREADS, pull_smem, st, a);
+                if (half && pull_sw) launch_pdl(k_pull_swh<B, T, SIDE_U>, grid, PULL_THREADS, pull_smem, st, a);
+                else if (half) launch_pdl(k_pull_half<B, T, SIDE_U>, grid, PULL_THREADS, pull_smem, st, a);
                 else if (pull_sw) launch_pdl(sw_kernel<SIDE_U>(), grid, PULL_THREADS, pull_smem, st, a);
                 else launch_pdl(k_pull<B, T, SIDE_U>, grid, PULL_THREADS, pull_smem, st, a);
             }
@@ -523,11 +562,11 @@ struct Engine final : EngineBase {
         if (prof) BH_CUDA(cudaEventRecord(ev(e0), st));
         launch_pdl(push_kernel(), grid_elem, ELEM_THREADS, 0, st, ea);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 1), st));
-        launch_pull(SIDE_V, pull_args(SIDE_V, 1.0 - rs.alpha), st);
+        launch_pull(SIDE_V, pull_args(SIDE_V, rs.alpha), st);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 2), st));
-        launch_pull(SIDE_U, pull_args(SIDE_U, 1.0 - rs.alpha), st);
+        launch_pull(SIDE_U, pull_args(SIDE_U, rs.alpha), st);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 3), st));
-        if (!fuse_combine) launch_pdl(combine_kernel(), grid_elem, ELEM_THREADS, 0, st, ea);
+        if (!fuse_combine) launch_pdl(combine_kernel(), grid_comb, ELEM_THREADS, 0, st, ea);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 4), st));
         launch_pdl(k_control, B, CONTROL_THREADS, 0, st, ca);
         launch_pdl(k_finalize<T>, grid_k5, TOPK_THREADS, 0, st, fa);

@@ -141,6 +141,15 @@ struct SlotSmem {
     double ysc[MAX_B];
 };
 
+// Push threshold of a push op at node u: (ws_q / ws_u)(eps_f / lam) forward,
+// 0 sequential, eps_b selective.  K1 (which nodes feed the pulls) and K1a (which
+// residues it zeroes and moves into est) evaluate the same expression on the
+// same r, so they take the same decision.
+__device__ __forceinline__ double push_threshold(const SlotSmem &sm, int s, int o, double iws) {
+    if (op_is_fwd(o)) return (sm.wsq[s] * iws) * sm.thc[s];
+    return o == OP_SEQ ? 0.0 : sm.eps_b[s];
+}
+
 template <int B>
 __device__ __forceinline__ void load_slot_smem(SlotSmem &sm, const Slot *__restrict__ slots) {
     for (int s = threadIdx.x; s < B; s += blockDim.x) {
@@ -183,43 +192,89 @@ struct ElemArgs {
     double alpha;
 };
 
-// K1: push (and ledger init / power-iteration entry) for the coming round.
+// Per-slot constants of K1 / K1a in shared memory, element-major: the v-th slot
+// of the thread group g sits at [v * TPN + g], so the 16 slot groups of a warp
+// read 16 consecutive doubles per LDS (no bank conflicts).  The thresholds are
+// folded into one form, th = fma(thA * iws, thC, thD):
+//   forward / measure: thA = ws_q, thC = eps_f / lam, thD = 0 -> (ws_q / ws_u)(eps_f / lam)
+//   selective:         thA = thC = 0, thD = eps_b;  sequential push: thD = 0
+// (fma(x, c, 0) rounds like x * c, so the forward threshold is bit-identical to
+// (ws_q * iws) * thc).  thDp: push threshold, thDa: exit-test threshold.
+struct ElemSlotC {
+    double thA[MAX_B], thC[MAX_B], thDp[MAX_B], thDa[MAX_B], iwsq[MAX_B], ysc[MAX_B];
+    int32_t op[MAX_B], src[MAX_B], qidx[MAX_B];
+};
+
+template <int B>
+__device__ __forceinline__ void load_elem_consts(ElemSlotC &c, const Slot *__restrict__ slots) {
+    using EG = ElemGeo<B>;
+    for (int s = threadIdx.x; s < B; s += blockDim.x) {
+        const Slot &sl = slots[s];
+        const int o = sl.op;
+        const bool fwdlike = op_is_fwd(o) || o == OP_MEASURE;
+        const int pidx = (s % EG::EV) * EG::TPN + s / EG::EV;
+        c.thA[pidx] = fwdlike ? sl.ws_q : 0.0;
+        c.thC[pidx] = fwdlike ? sl.theta_c : 0.0;
+        c.thDp[pidx] = fwdlike || o == OP_SEQ ? 0.0 : sl.eps_b;
+        c.thDa[pidx] = fwdlike ? 0.0 : sl.eps_b;
+        c.iwsq[pidx] = sl.inv_ws_q;
+        c.ysc[pidx] = sl.ysc;
+        c.op[s] = o;
+        c.src[s] = sl.src;
+        c.qidx[s] = sl.qidx;
+    }
+}
+
+// K1: push (and ledger init / power-iteration entry) for the coming round:
+// P = r on A = {r > th}, 0 elsewhere, and the per-slot |A|, sum deg(A) and the
+// forward left-behind mass.  r_A := 0 and est_A += alpha r_A are left to K1a,
+// which re-takes the same decision on the same r; only the ledger-initialising
+// round writes r and est here.  Per element the work is predicated (the slots
+// of one warp are in different phases), loads of UNR nodes are in flight.
 template <int B, typename T, int ELEM_UNR = 4, int MINB = 1>
 __global__ void __launch_bounds__(ELEM_THREADS, MINB) k_push(ElemArgs<T> a) {
     pdl_begin();
     if (*a.active == 0) return;
     using EG = ElemGeo<B>;
     constexpr int EV = EG::EV, TPN = EG::TPN;
-    __shared__ SlotSmem sm;
+    __shared__ ElemSlotC sc;
     __shared__ int64_t red_cnt[ELEM_THREADS * EV];
     __shared__ int64_t red_np[ELEM_THREADS * EV];
     __shared__ double red_left[ELEM_THREADS * EV];
-    load_slot_smem<B>(sm, a.slots);
+    load_elem_consts<B>(sc, a.slots);
     __syncthreads();
-    const int j0 = (threadIdx.x % TPN) * EV;  // first slot of this thread (fixed: blockDim % TPN == 0)
-    int op[EV];
-    bool any_work = false, init_any = false;
+    const int grp = threadIdx.x % TPN;
+    const int j0 = grp * EV;  // first slot of this thread (fixed: blockDim % TPN == 0)
+    uint32_t m_push = 0, m_init = 0, m_fwd = 0, m_entry = 0, m_x0 = 0, m_keep = 0;
 #pragma unroll
     for (int v = 0; v < EV; v++) {
-        op[v] = sm.op[j0 + v];
-        any_work |= op_is_push(op[v]) || op[v] == OP_PIENTRY || op[v] == OP_PIENTRY0;
-        init_any |= op[v] == OP_BSEL_INIT;
+        const int o = sc.op[j0 + v];
+        const bool x0 = a.x0 && sc.qidx[j0 + v] >= 0;
+        m_push |= (uint32_t)op_is_push(o) << v;
+        m_init |= (uint32_t)(o == OP_BSEL_INIT) << v;
+        m_fwd |= (uint32_t)op_is_fwd(o) << v;
+        m_entry |= (uint32_t)(o == OP_PIENTRY || o == OP_PIENTRY0) << v;
+        m_x0 |= (uint32_t)((o == OP_PIENTRY || o == OP_PIENTRY0) && x0) << v;
     }
-    int64_t cnt[EV], npu[EV];
+    m_keep = ((1u << EV) - 1u) & ~(m_push | m_entry);  // P kept (iterate / idle)
+    int32_t cnt[EV];  // nodes per thread < 2^31
+    int64_t npu[EV];
     double left[EV];
 #pragma unroll
     for (int v = 0; v < EV; v++) {
-        cnt[v] = npu[v] = 0;
+        cnt[v] = 0;
+        npu[v] = 0;
         left[v] = 0.0;
     }
-    if (any_work) {
-        // UNR nodes per thread in flight: all their loads are issued before any
-        // is consumed (the kernel is latency-bound at one node per thread).
+    // RARE: ledger-initialising slots or raw power-iteration starts in this
+    // thread's group (one round per query); the common body has neither
+    auto run = [&](auto rare_tag) {
+        constexpr bool RARE = decltype(rare_tag)::value;
         const int64_t total = a.n_u * TPN;
         const int64_t stride = (int64_t)gridDim.x * blockDim.x;
         for (int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t0 < total; t0 += ELEM_UNR * stride) {
             T rv[ELEM_UNR][EV];
-            double iwsk[ELEM_UNR];
+            double iwsk[ELEM_UNR], wsk[ELEM_UNR];
             int32_t degk[ELEM_UNR];
 #pragma unroll
             for (int k = 0; k < ELEM_UNR; k++) {
@@ -228,6 +283,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, MINB) k_push(ElemArgs<T> a) {
                     const int64_t u = t / TPN;
                     VecIO<T, EV>::ld(a.R + u * B + j0, rv[k]);
                     iwsk[k] = a.inv_ws_u[u];
+                    wsk[k] = m_fwd ? a.ws_u[u] : 0.0;
                     degk[k] = a.deg_u[u];
                 }
             }
@@ -239,67 +295,58 @@ __global__ void __launch_bounds__(ELEM_THREADS, MINB) k_push(ElemArgs<T> a) {
                 const int64_t i = u * B + j0;
                 const double iws = iwsk[k];
                 T pv[EV];
-                bool act[EV], any_act = false, wrote_r = false;
+                bool act[EV];
                 double rr[EV];
 #pragma unroll
                 for (int v = 0; v < EV; v++) {
-                    const int s = j0 + v;
-                    const int o = op[v];
-                    pv[v] = (T)0;
-                    act[v] = false;
-                    rr[v] = 0.0;
-                    if (o == OP_PIENTRY || o == OP_PIENTRY0) {
-                        const double *x0 = (a.x0 && sm.qidx[s] >= 0) ? a.x0 + (int64_t)sm.qidx[s] * a.n_u : nullptr;
-                        if (x0) {  // raw power iteration: y0 = start / ws  (push_engine.py:112, on a = acc / ws)
-                            const T y = (T)(x0[u] * iws);
-                            rv[k][v] = y;
-                            pv[v] = y;
-                            wrote_r = true;
-                        } else {   // PI-Push tail: y0 = (w_ratio r) / ws = r / ws(q)  (push_engine.py:246)
-                            pv[v] = (T)((double)rv[k][v] * sm.ysc[s]);
+                    const int c = v * TPN + grp;
+                    const bool push = (m_push >> v) & 1u;
+                    const bool init = RARE && ((m_init >> v) & 1u);
+                    const double r = init ? (u == sc.src[j0 + v] ? 1.0 : 0.0) : (double)rv[k][v];
+                    const double th = fma(sc.thA[c] * iws, sc.thC[c], sc.thDp[c]);
+                    const bool pushed = push && r > th;
+                    act[v] = pushed;
+                    rr[v] = r;
+                    cnt[v] += pushed;
+                    npu[v] += pushed ? degk[k] : 0;
+                    if (((m_fwd >> v) & 1u) && !pushed)
+                        left[v] += (wsk[k] * sc.iwsq[c]) * r;  // w_ratio r left behind this round
+                    T p = pushed ? (T)r : (T)0;
+                    if ((m_entry >> v) & 1u) {
+                        // y0 = (w_ratio r) / ws = r / ws(q) (PI-Push tail, push_engine.py:246), or
+                        // start / ws for a raw power iteration (push_engine.py:112 on a = acc / ws)
+                        p = (T)((double)rv[k][v] * sc.ysc[c]);
+                        if (RARE && ((m_x0 >> v) & 1u)) {
+                            p = (T)(a.x0[(int64_t)sc.qidx[j0 + v] * a.n_u + u] * iws);
+                            rv[k][v] = p;
                         }
-                    } else if (op_is_push(o)) {
-                        const bool init = o == OP_BSEL_INIT;
-                        const double r = init ? (u == sm.src[s] ? 1.0 : 0.0) : (double)rv[k][v];
-                        double th;
-                        if (op_is_fwd(o)) th = (sm.wsq[s] * iws) * sm.thc[s];  // (ws_q / ws_i)(eps_f / lam)
-                        else th = (o == OP_SEQ) ? 0.0 : sm.eps_b[s];
-                        rr[v] = r;
-                        if (r > th) {
-                            act[v] = true;
-                            any_act = true;
-                            pv[v] = (T)r;
-                            rv[k][v] = (T)0;
-                            cnt[v] += 1;
-                            npu[v] += degk[k];
-                            wrote_r = true;
-                        } else if (init) {
-                            rv[k][v] = (T)r;
-                            wrote_r = true;
-                        } else if (op_is_fwd(o)) {
-                            left[v] += (a.ws_u[u] * sm.iwsq[s]) * r;  // w_ratio r left behind this round
-                        }
-                    } else {
-                        pv[v] = a.P[i + v];  // keep (power-iteration iterate / idle)
                     }
+                    if (init) rv[k][v] = pushed ? (T)0 : (T)r;
+                    pv[v] = p;
                 }
-                if (any_act || init_any) {  // est += alpha r on the pushed slots (ledger reset on init)
-                    T ev[EV];
-                    VecIO<T, EV>::ld(a.EST + i, ev);
+                if (m_keep) {  // slots whose P is kept (iterate / idle) are not written
 #pragma unroll
-                    for (int v = 0; v < EV; v++) {
-                        const bool init = op[v] == OP_BSEL_INIT;
-                        double e = init ? 0.0 : (double)ev[v];
-                        if (act[v]) e += a.alpha * rr[v];
-                        ev[v] = (T)e;
-                    }
-                    VecIO<T, EV>::st(a.EST + i, ev);
+                    for (int v = 0; v < EV; v++)
+                        if (!((m_keep >> v) & 1u)) a.P[i + v] = pv[v];
+                } else {
+                    VecIO<T, EV>::st(a.P + i, pv);
                 }
-                VecIO<T, EV>::st(a.P + i, pv);
-                if (wrote_r) VecIO<T, EV>::st(a.R + i, rv[k]);
+                if constexpr (RARE) {
+                    VecIO<T, EV>::st(a.R + i, rv[k]);
+                    if (m_init) {  // ledger reset: est := alpha r on the pushed nodes of init slots
+                        T ev[EV];
+                        VecIO<T, EV>::ld(a.EST + i, ev);
+#pragma unroll
+                        for (int v = 0; v < EV; v++)
+                            if ((m_init >> v) & 1u) ev[v] = (T)(act[v] ? 0.0 + a.alpha * rr[v] : 0.0);
+                        VecIO<T, EV>::st(a.EST + i, ev);
+                    }
+                }
             }
         }
-    }
+    };
+    if (m_init | m_x0) run(std::true_type{});
+    else if (m_push | m_entry) run(std::false_type{});
 #pragma unroll
     for (int v = 0; v < EV; v++) {
         red_cnt[threadIdx.x * EV + v] = cnt[v];
@@ -323,26 +370,31 @@ __global__ void __launch_bounds__(ELEM_THREADS, MINB) k_push(ElemArgs<T> a) {
 }
 
 // K1a: combine r_u += Y (push slots) / a = y0 + Y (power-iteration slots), and
-// the exit-test reductions of the round that just ran.
+// the exit-test reductions of the round that just ran.  For push slots it also
+// completes K1's push: the nodes over threshold (same decision, same r) have
+// their residue replaced by Y and est += alpha r.  Per element predicated.
 template <int B, typename T, int ELEM_UNR = 4, int MINB = 1>
 __global__ void __launch_bounds__(ELEM_THREADS, MINB) k_combine(ElemArgs<T> a) {
     pdl_begin();
     if (*a.active == 0) return;
     using EG = ElemGeo<B>;
     constexpr int EV = EG::EV, TPN = EG::TPN;
-    __shared__ SlotSmem sm;
+    __shared__ ElemSlotC sc;
     __shared__ double red_sum[ELEM_THREADS * EV];
     __shared__ double red_wsum[ELEM_THREADS * EV];
     __shared__ int32_t red_any[ELEM_THREADS * EV];
-    load_slot_smem<B>(sm, a.slots);
+    load_elem_consts<B>(sc, a.slots);
     __syncthreads();
-    const int j0 = (threadIdx.x % TPN) * EV;
-    int op[EV];
-    bool any_work = false;
+    const int grp = threadIdx.x % TPN;
+    const int j0 = grp * EV;
+    uint32_t m_push = 0, m_rw = 0, m_stat = 0, m_pi = 0;
 #pragma unroll
     for (int v = 0; v < EV; v++) {
-        op[v] = sm.op[j0 + v];
-        any_work |= op_is_push(op[v]) || op[v] == OP_PIENTRY || op[v] == OP_PI || op[v] == OP_MEASURE;
+        const int o = sc.op[j0 + v];
+        m_push |= (uint32_t)(op_is_push(o) && o != OP_BSEL_INIT) << v;  // pushed by K1 this round
+        m_rw |= (uint32_t)op_is_push(o) << v;                            // r_u += Y
+        m_stat |= (uint32_t)(op_is_push(o) || o == OP_MEASURE) << v;     // exit-test reductions
+        m_pi |= (uint32_t)(o == OP_PIENTRY || o == OP_PI) << v;          // a = y0 + Y
     }
     double sum[EV], wsum[EV];
     int32_t any[EV];
@@ -351,11 +403,11 @@ __global__ void __launch_bounds__(ELEM_THREADS, MINB) k_combine(ElemArgs<T> a) {
         sum[v] = wsum[v] = 0.0;
         any[v] = 0;
     }
-    if (any_work) {
+    if (m_stat | m_pi) {
         const int64_t total = a.n_u * TPN;
         const int64_t stride = (int64_t)gridDim.x * blockDim.x;
         for (int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t0 < total; t0 += ELEM_UNR * stride) {
-            T rv[ELEM_UNR][EV], yv[ELEM_UNR][EV];
+            T rv[ELEM_UNR][EV], yv[ELEM_UNR][EV], ev[ELEM_UNR][EV];
             double wsk[ELEM_UNR], iwsk[ELEM_UNR];
 #pragma unroll
             for (int k = 0; k < ELEM_UNR; k++) {
@@ -364,6 +416,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, MINB) k_combine(ElemArgs<T> a) {
                     const int64_t u = t / TPN;
                     VecIO<T, EV>::ld(a.R + u * B + j0, rv[k]);
                     VecIO<T, EV>::ld(a.Y + u * B + j0, yv[k]);
+                    if (m_push) VecIO<T, EV>::ld(a.EST + u * B + j0, ev[k]);
                     wsk[k] = a.ws_u[u];
                     iwsk[k] = a.inv_ws_u[u];
                 }
@@ -375,29 +428,29 @@ __global__ void __launch_bounds__(ELEM_THREADS, MINB) k_combine(ElemArgs<T> a) {
                 const int64_t u = t / TPN;
                 const int64_t i = u * B + j0;
                 const double ws = wsk[k], iws = iwsk[k];
-                bool wrote_r = false;
+                bool wrote_e = false;
 #pragma unroll
                 for (int v = 0; v < EV; v++) {
-                    const int s = j0 + v;
-                    const int o = op[v];
-                    if (op_is_push(o) || o == OP_MEASURE) {
-                        T nr = rv[k][v];
-                        if (o != OP_MEASURE) {
-                            nr = (T)((double)rv[k][v] + (double)yv[k][v]);
-                            rv[k][v] = nr;
-                            wrote_r = true;
-                        }
-                        const double r = (double)nr;
-                        sum[v] += r;
-                        wsum[v] += (ws * sm.iwsq[s]) * r;  // w_ratio * r  (push_engine.py:220,237)
-                        const double th =
-                            (op_is_fwd(o) || o == OP_MEASURE) ? (sm.wsq[s] * iws) * sm.thc[s] : sm.eps_b[s];
-                        any[v] |= r > th;
-                    } else if (o == OP_PIENTRY || o == OP_PI) {
-                        a.P[i + v] = (T)((double)rv[k][v] * sm.ysc[s] + (double)yv[k][v]);
+                    const int c = v * TPN + grp;
+                    const double r0 = (double)rv[k][v];
+                    const double y = (double)yv[k][v];
+                    const double tA = sc.thA[c] * iws;
+                    const bool pushed = ((m_push >> v) & 1u) && r0 > fma(tA, sc.thC[c], sc.thDp[c]);
+                    if (pushed) {
+                        ev[k][v] = (T)((double)ev[k][v] + a.alpha * r0);
+                        wrote_e = true;
                     }
+                    if ((m_pi >> v) & 1u) a.P[i + v] = (T)(r0 * sc.ysc[c] + y);
+                    const T nr = ((m_rw >> v) & 1u) ? (T)((pushed ? 0.0 : r0) + y) : rv[k][v];
+                    rv[k][v] = nr;
+                    const double r = (double)nr;
+                    const bool st = (m_stat >> v) & 1u;
+                    if (st) sum[v] += r;
+                    if (st) wsum[v] = fma(ws * sc.iwsq[c], r, wsum[v]);  // w_ratio * r  (push_engine.py:220,237)
+                    any[v] |= st && r > fma(tA, sc.thC[c], sc.thDa[c]);
                 }
-                if (wrote_r) VecIO<T, EV>::st(a.R + i, rv[k]);
+                if (m_rw) VecIO<T, EV>::st(a.R + i, rv[k]);
+                if (wrote_e) VecIO<T, EV>::st(a.EST + i, ev[k]);
             }
         }
     }
@@ -451,6 +504,8 @@ struct PullArgs {
     // go straight into the combine instead of through Y
     T *R;                  // residues r_u [n_u][B]
     T *Pn;                 // power-iteration iterate [n_u][B] (PI slots)
+    T *EST;                // estimates [n_u][B] (push slots: est += alpha r on the pushed nodes)
+    double alpha;
     const double *ws_u, *inv_ws_u;
     int32_t *p_any;        // partial rows [slot][part_rows]: one per warp, then one per cut row
     double *p_sum, *p_wsum;
@@ -736,8 +791,11 @@ struct RowCombine {
     }
     __device__ __forceinline__ void row(const PullArgs<T> &a, const SlotSmem &sm, int slot0, int64_t u,
                                         const double (&acc)[VEC], const T (&rv)[VEC], double ws, double iws) {
-        T nr[VEC];
-        bool wrote_r = false;
+        T nr[VEC], ev[VEC];
+        bool wrote_r = false, wrote_e = false, any_push = false;
+#pragma unroll
+        for (int v = 0; v < VEC; v++) any_push |= op_is_push(sm.op[slot0 + v]) && sm.op[slot0 + v] != OP_BSEL_INIT;
+        if (any_push) VecIO<T, VEC>::ld(a.EST + u * B + slot0, ev);
 #pragma unroll
         for (int v = 0; v < VEC; v++) {
             const int s = slot0 + v;
@@ -746,7 +804,13 @@ struct RowCombine {
             nr[v] = rv[v];
             if (op_is_push(o) || o == OP_MEASURE) {
                 if (o != OP_MEASURE) {
-                    nr[v] = (T)((double)rv[v] + (double)y);
+                    double r0 = (double)rv[v];
+                    if (o != OP_BSEL_INIT && r0 > push_threshold(sm, s, o, iws)) {  // pushed by K1 (see k_combine)
+                        ev[v] = (T)((double)ev[v] + a.alpha * r0);
+                        wrote_e = true;
+                        r0 = 0.0;
+                    }
+                    nr[v] = (T)(r0 + (double)y);
                     wrote_r = true;
                 }
                 const double r = (double)nr[v];
@@ -759,6 +823,7 @@ struct RowCombine {
             }
         }
         if (wrote_r) VecIO<T, VEC>::st(a.R + u * B + slot0, nr);
+        if (wrote_e) VecIO<T, VEC>::st(a.EST + u * B + slot0, ev);
     }
     __device__ __forceinline__ void store(const PullArgs<T> &a, int row, int slot0) const {
 #pragma unroll
@@ -1511,6 +1576,192 @@ __global__ void __launch_bounds__(PULL_THREADS, 2) k_pull_half(PullArgs<T> a) {
 
 // B < 32 (single-query and small blocks): G lanes per edge group, 32/G groups
 // split each row; plain loads.  Same partition, cut rows and epilogue.
+// Half-warp workers with shared-memory windows (k_pull_swh): the k_pull_sw
+// edge loop run by each 16-lane half of a warp on its own cost-balanced edge
+// range (the half-warp plan of k_pull_half), a lane owning VEC = B/16 slots, so
+// one warp instruction gathers two operand rows (LDG.128 at B = 64 fp32) and
+// the per-edge (col, val) read, address arithmetic and loop overhead are paid
+// once per two edges.  Row emits diverge between the halves.
+template <int B, typename T, int SIDE, int S = (HalfPipe<B, T>::S < 8 ? HalfPipe<B, T>::S : 8), int MINB = 2>
+__global__ void __launch_bounds__(PULL_THREADS, MINB) k_pull_swh(PullArgs<T> a) {
+    pdl_begin();
+    if (*a.active == 0) return;
+    constexpr int VEC = B / 16;
+    static_assert(2 * S <= 16, "a half-warp stages two windows per load");
+    constexpr int WSTRIDE = 2 * S + 1;  // +1 entry: the two halves' windows on different banks
+    __shared__ EdgeCV<T> s_win[PULL_WARPS * 2][WSTRIDE];
+    __shared__ int32_t s_re[PULL_WARPS * 2][33];
+    const int lane = threadIdx.x & 31;
+    const int h = lane >> 4, q = lane & 15;
+    const uint32_t hmask = h ? 0xffff0000u : 0x0000ffffu;
+    const int warp = threadIdx.x >> 5;
+    const int gw = blockIdx.x * PULL_WARPS + warp;
+    const int wid = gw * 2 + h;
+    const int slot0 = q * VEC;
+    uint32_t cmask = 0;
+    if constexpr (SIDE == SIDE_V) {
+#pragma unroll
+        for (int v = 0; v < VEC; v++) cmask |= (op_is_push(a.slots[slot0 + v].op) ? 1u : 0u) << v;
+    }
+    const double scale = SIDE == SIDE_V ? a.one_minus_alpha : 1.0;
+    int32_t np[VEC];
+    int64_t np_cut[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; v++) {
+        np[v] = 0;
+        np_cut[v] = 0;
+    }
+    const int n_workers = a.n_warps;  // work entries (two per warp)
+    WarpWork wk;
+    wk.e0 = wk.e1 = 0;
+    wk.r0 = 0;
+    wk.cut0 = wk.cut1 = wk.part0 = wk.part1 = -1;
+    if (wid < n_workers) wk = a.work[wid];
+    const int64_t e0 = wk.e0;
+    const int n = (int)(wk.e1 - e0);
+    const int n_max = max(n, __shfl_xor_sync(0xffffffffu, n, 16));
+    if (n_max > 0) {
+        const int32_t *cols = a.indices + e0;
+        const T *vals = a.vals + e0;
+        const T *X = a.X + slot0;
+        T *Y0 = a.Y + (int64_t)wk.r0 * B + slot0;
+        const int64_t *rp = a.indptr + wk.r0;
+        const int64_t nrow_left = a.n_rows - wk.r0;
+        const int cutA = wk.cut0 >= 0 ? 0 : -1;
+        const int cutB = wk.cut1 >= 0 ? (int)(a.cuts[wk.cut1].row - wk.r0) : -1;
+        auto col_at = [&](int o) { return o < n ? __ldg(cols + o) : 0; };
+        auto val_at = [&](int o) { return o < n ? __ldg(vals + o) : (T)0; };
+        auto rend_at = [&](int i) {
+            if (n <= 0) return 0;
+            const int64_t r = i + 1 <= nrow_left ? __ldg(rp + i + 1) : __ldg(rp + nrow_left);
+            return (int)imin64(r - e0, (int64_t)n);
+        };
+        EdgeCV<T> *win = s_win[warp * 2 + h];
+        int32_t *re = s_re[warp * 2 + h];
+        re[q] = rend_at(q);
+        re[16 + q] = rend_at(16 + q);
+        if (q < 2 * S) win[q] = EdgeCV<T>{col_at(q), val_at(q)};  // blocks 0 and 1
+        int cw = col_at(2 * S + q);               // block 2 (lanes q < S)
+        T vw = val_at(2 * S + q);
+        __syncwarp();
+        T xs[S][VEC];
+        T wsv[S];
+#pragma unroll
+        for (int t = 0; t < S; t++) {
+            const EdgeCV<T> e = win[t];
+            wsv[t] = e.v;
+            ldg_vec<T, VEC>(X + (int64_t)e.c * B, xs[t]);
+        }
+        int rw = 0;  // row-end ring holds local rows [rw, rw + 32)
+        int lr = 0;
+        int rstart = n > 0 ? (int)(__ldg(rp) - e0) : 0;
+        int rend = n > 0 ? re[0] : (1 << 30);  // idle worker: never emits
+        double acc[VEC];
+        T accs[VEC];
+#pragma unroll
+        for (int v = 0; v < VEC; v++) {
+            acc[v] = 0.0;
+            accs[v] = (T)0;
+        }
+        int b = 0;
+        for (int base = 0; base < n_max; base += S, b ^= 1) {
+            const EdgeCV<T> *nxt = win + (b ^ 1) * S;
+            int d = rend - base - 1;
+#pragma unroll
+            for (int t = 0; t < S; t++) {
+                if constexpr (sizeof(T) == 8) {
+#pragma unroll
+                    for (int v = 0; v < VEC; v++) acc[v] = fma((double)wsv[t], (double)xs[t][v], acc[v]);
+                } else {
+#pragma unroll
+                    for (int v = 0; v < VEC; v++) accs[v] = fmaf(wsv[t], xs[t][v], accs[v]);
+                }
+                if (d == t) {  // row emit (this half only)
+                    if constexpr (sizeof(T) == 4) {
+#pragma unroll
+                        for (int v = 0; v < VEC; v++) {
+                            acc[v] += (double)accs[v];
+                            accs[v] = (T)0;
+                        }
+                    }
+                    if (lr == cutA || lr == cutB) {
+                        double *dst = a.scratch + (int64_t)(lr == cutA ? wk.part0 : wk.part1) * B + slot0;
+#pragma unroll
+                        for (int v = 0; v < VEC; v++) dst[v] = acc[v];
+                    } else {
+                        T out[VEC];
+#pragma unroll
+                        for (int v = 0; v < VEC; v++) {
+                            out[v] = (T)(scale * acc[v]);
+                            if constexpr (SIDE == SIDE_V)
+                                np[v] += (((cmask >> v) & 1u) && out[v] > (T)0) ? rend - rstart : 0;
+                        }
+                        VecIO<T, VEC>::st(Y0 + (int64_t)lr * B, out);
+                    }
+#pragma unroll
+                    for (int v = 0; v < VEC; v++) acc[v] = 0.0;
+                    lr++;
+                    rstart = rend;
+                    rend = re[lr & 31];
+                    d = rend - base - 1;
+                }
+                const EdgeCV<T> e = nxt[t];
+                wsv[t] = e.v;
+                ldg_vec<T, VEC>(X + (int64_t)e.c * B, xs[t]);
+            }
+            if constexpr (sizeof(T) == 4) {
+#pragma unroll
+                for (int v = 0; v < VEC; v++) {
+                    acc[v] += (double)accs[v];
+                    accs[v] = (T)0;
+                }
+            }
+            // stage block (base/S + 2) into the window block read during this one,
+            // refill the row-end ring half that is behind lr
+            if (q < S) win[b * S + q] = EdgeCV<T>{cw, vw};
+            if (lr - rw >= 16) {
+                re[(rw + 32 + q) & 31] = rend_at(rw + 32 + q);
+                rw += 16;
+            }
+            cw = col_at(base + 3 * S + q);
+            vw = val_at(base + 3 * S + q);
+            __syncwarp();
+        }
+        const CutCtx<T> cx{a.scratch, a.cut_count, a.cuts, a.Y, a.indptr, scale};
+        for (int hh = 0; hh < 2; hh++) {
+            if (h == hh) {
+                if (cutA >= 0) {
+                    DVec<VEC> av;
+#pragma unroll
+                    for (int v = 0; v < VEC; v++) av.v[v] = a.scratch[(int64_t)wk.part0 * B + slot0 + v];
+                    const IVec<VEC> inc = pull_cut_half<B, T, VEC>(cx, wk.cut0, wk.part0, slot0, cmask, av, hmask);
+#pragma unroll
+                    for (int v = 0; v < VEC; v++) np_cut[v] += inc.v[v];
+                }
+                if (cutB >= 0) {
+                    DVec<VEC> av;
+#pragma unroll
+                    for (int v = 0; v < VEC; v++) av.v[v] = a.scratch[(int64_t)wk.part1 * B + slot0 + v];
+                    const IVec<VEC> inc = pull_cut_half<B, T, VEC>(cx, wk.cut1, wk.part1, slot0, cmask, av, hmask);
+#pragma unroll
+                    for (int v = 0; v < VEC; v++) np_cut[v] += inc.v[v];
+                }
+            }
+            __syncwarp();
+        }
+    }
+    if constexpr (SIDE == SIDE_V) {
+        // both halves cover the same slots: combine, half 0 writes the warp's row
+        const int n_rows_out = (n_workers + 1) / 2;
+#pragma unroll
+        for (int v = 0; v < VEC; v++) {
+            int64_t t = (int64_t)np[v] + np_cut[v];
+            t += __shfl_xor_sync(0xffffffffu, t, 16);
+            if (h == 0 && gw < n_rows_out) a.np_v[(int64_t)(slot0 + v) * n_rows_out + gw] = t;
+        }
+    }
+}
+
 template <int B, typename T, int SIDE>
 __global__ void __launch_bounds__(PULL_THREADS) k_pull_small(PullArgs<T> a) {
     pdl_begin();

@@ -261,6 +261,8 @@ def test_scaled_configs_fp32(name):
     {"BH_PULL_SW": "0", "BH_PULL_HALF": "0"},   # lane-register windows (k_pull)
     {"BH_PULL_SW": "0", "BH_PULL_HALF": "3"},   # half-warp workers (k_pull_half)
     {"BH_PULL_SW": "1", "BH_PULL_HALF": "0"},   # shared-memory windows (k_pull_sw)
+    {"BH_PULL_SW": "1", "BH_PULL_HALF": "3"},   # half-warp workers, shared-memory windows (k_pull_swh)
+    {"BH_PULL_SW": "1", "BH_PULL_HALF": "1"},   # k_pull_swh on the U side, k_pull_sw on the V side
     {"BH_PULL_SW": "1", "BH_FUSE_COMBINE": "1"},  # k_pull_sw with K1a fused into the U pull
     {"BH_PULL_TMA": "1"},                        # TMA gather4 ring (k_pull_tma)
 ])
