@@ -196,6 +196,7 @@ struct Control {
     int32_t rounds_active;  // rounds K4 processed with work in flight
     int32_t arrive;         // K4 block arrival counter (last block assigns queries)
     int32_t error;          // set by K4's runaway guard
+    int32_t fin_rounds;     // rounds with a finishing slot (K5 launched under the graph's IF node)
     int32_t fin_slots[256];
     int32_t free_slot[256];
 };

@@ -30,6 +30,8 @@ struct ControlArgs {
     int32_t use_cond;     // running inside a CUDA-graph WHILE node: set its condition
     int32_t max_rounds;   // safety stop
     cudaGraphConditionalHandle cond;
+    int32_t use_fin_cond; // K5 sits under an IF node: set it when a slot finished
+    cudaGraphConditionalHandle fin_cond;
 };
 
 __device__ __forceinline__ int32_t required_iterations_dev(double alpha, double eps_f, double mass) {
@@ -117,6 +119,7 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
         if (s == 0 && tid == 0) {
             ctl->n_fin = 0;
             if (a.use_cond) cudaGraphSetConditional(a.cond, 0);
+            if (a.use_fin_cond) cudaGraphSetConditional(a.fin_cond, 0);
         }
         return;
     }
@@ -127,8 +130,9 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
     double sum = 0.0, wsum = 0.0, left = 0.0;
     int32_t any = 0;
     if (!a.first) {
-        constexpr int U4 = 4, STEP = CONTROL_THREADS * U4;
-        // partial rows are stored slot-major: [slot][row]
+        // partial rows are stored slot-major: [slot][row]; the loads of all six
+        // row sets are issued together (one memory round trip for the usual sizes)
+        constexpr int U4 = 4, U16 = 16;
         const int64_t *pc = a.part.cnt + (int64_t)s * a.part.rows_k1;
         const int64_t *pn = a.part.np_u + (int64_t)s * a.part.rows_k1;
         const double *pl = a.part.lmass + (int64_t)s * a.part.rows_k1;
@@ -136,52 +140,39 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
         const int32_t *pa = a.part.any + (int64_t)s * a.part.rows_k3;
         const double *ps = a.part.sum + (int64_t)s * a.part.rows_k3;
         const double *pw = a.part.wsum + (int64_t)s * a.part.rows_k3;
-        for (int r0 = 0; r0 < a.part.rows_k1; r0 += STEP) {
-            int64_t c4[U4], n4[U4];
-            double l4[U4];
+        const int n1 = a.part.rows_k1, n2 = a.part.rows_k2, n3 = a.part.rows_k3;
+        for (int it = 0; it * CONTROL_THREADS * U4 < n1 || it * CONTROL_THREADS * U16 < n2 ||
+                         it * CONTROL_THREADS * U4 < n3; it++) {
+            int64_t c4[U4], n4[U4], n16[U16];
+            double l4[U4], s4[U4], w4[U4];
+            int32_t a4[U4];
 #pragma unroll
             for (int j = 0; j < U4; j++) {
-                const int r = r0 + j * CONTROL_THREADS + tid;
-                const bool ok = r < a.part.rows_k1;
-                c4[j] = ok ? __ldcg(pc + r) : 0;
-                n4[j] = ok ? __ldcg(pn + r) : 0;
-                l4[j] = ok ? __ldcg(pl + r) : 0.0;
+                const int r = (it * U4 + j) * CONTROL_THREADS + tid;
+                const bool ok1 = r < n1, ok3 = r < n3;
+                c4[j] = ok1 ? __ldcg(pc + r) : 0;
+                n4[j] = ok1 ? __ldcg(pn + r) : 0;
+                l4[j] = ok1 ? __ldcg(pl + r) : 0.0;
+                a4[j] = ok3 ? __ldcg(pa + r) : 0;
+                s4[j] = ok3 ? __ldcg(ps + r) : 0.0;
+                w4[j] = ok3 ? __ldcg(pw + r) : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < U16; j++) {
+                const int r = (it * U16 + j) * CONTROL_THREADS + tid;
+                n16[j] = r < n2 ? __ldcg(pv + r) : 0;
             }
 #pragma unroll
             for (int j = 0; j < U4; j++) {
                 cnt += c4[j];
                 np += n4[j];
                 left += l4[j];
-            }
-        }
-        constexpr int U16 = 16, STEP16 = CONTROL_THREADS * U16;  // per-warp n_p rows: many, all in flight
-        for (int r0 = 0; r0 < a.part.rows_k2; r0 += STEP16) {
-            int64_t n16[U16];
-#pragma unroll
-            for (int j = 0; j < U16; j++) {
-                const int r = r0 + j * CONTROL_THREADS + tid;
-                n16[j] = r < a.part.rows_k2 ? __ldcg(pv + r) : 0;
-            }
-#pragma unroll
-            for (int j = 0; j < U16; j++) np += n16[j];
-        }
-        for (int r0 = 0; r0 < a.part.rows_k3; r0 += STEP) {
-            int32_t a4[U4];
-            double s4[U4], w4[U4];
-#pragma unroll
-            for (int j = 0; j < U4; j++) {
-                const int r = r0 + j * CONTROL_THREADS + tid;
-                const bool ok = r < a.part.rows_k3;
-                a4[j] = ok ? __ldcg(pa + r) : 0;
-                s4[j] = ok ? __ldcg(ps + r) : 0.0;
-                w4[j] = ok ? __ldcg(pw + r) : 0.0;
-            }
-#pragma unroll
-            for (int j = 0; j < U4; j++) {
                 any |= a4[j];
                 sum += s4[j];
                 wsum += w4[j];
             }
+#pragma unroll
+            for (int j = 0; j < U16; j++) np += n16[j];
         }
     }
 #pragma unroll
@@ -350,10 +341,31 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
         a.slots[s] = sl;
         ctl->free_slot[s] = (free_now ? 1 : 0) | (fin ? 2 : 0);
         __threadfence();
-        s_last = atomicAdd(&ctl->arrive, 1) == B - 1;
+        // arrival count in the low 16 bits, free slots above: the last block
+        // learns whether any slot needs the refill pass
+        const int32_t prev = atomicAdd(&ctl->arrive, 1 + (free_now ? (1 << 16) : 0));
+        const int32_t now = prev + 1 + (free_now ? (1 << 16) : 0);
+        s_last = (now & 0xffff) == B ? 1 + (now >> 16) : 0;
     }
     __syncthreads();
     if (!s_last) return;
+    if (s_last == 1 && !a.first) {  // no slot freed this round: all stay busy, nothing to refill
+        if (tid == 0) {
+            ctl->n_fin = 0;
+            ctl->rounds_active++;
+            int32_t busy = 1;
+            if (ctl->rounds_active > a.max_rounds) {  // runaway guard (never expected)
+                busy = 0;
+                ctl->error = 1;
+            }
+            ctl->active = busy;
+            ctl->arrive = 0;
+            if (a.use_cond) cudaGraphSetConditional(a.cond, busy ? 1u : 0u);
+            if (a.use_fin_cond) cudaGraphSetConditional(a.fin_cond, 0);
+            __threadfence();
+        }
+        return;
+    }
     // last block: refill free slots in slot order (prefix count), publish flags
     __threadfence();
     // slot-order prefix counts of the free / finishing slots (ballots per warp)
@@ -402,6 +414,8 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
     if (tid == 0) {
         ctl->next_q = min(n_q, next0 + nfree);
         ctl->n_fin = nfin;
+        ctl->fin_rounds += nfin > 0;
+        if (a.use_fin_cond) cudaGraphSetConditional(a.fin_cond, nfin > 0 ? 1u : 0u);
         if (!a.first) ctl->rounds_active++;
         if (ctl->rounds_active > a.max_rounds) {  // runaway guard (never expected)
             busy = 0;

@@ -569,7 +569,7 @@ struct Engine final : EngineBase {
         if (!fuse_combine) launch_pdl(combine_kernel(), grid_comb, ELEM_THREADS, 0, st, ea);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 4), st));
         launch_pdl(k_control, B, CONTROL_THREADS, 0, st, ca);
-        launch_pdl(k_finalize<T>, grid_k5, TOPK_THREADS, 0, st, fa);
+        if (!ca.use_fin_cond) launch_pdl(k_finalize<T>, grid_k5, TOPK_THREADS, 0, st, fa);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 5), st));
         const int launches = launches_per_round();
         count_launch(launches);
@@ -628,13 +628,45 @@ struct Engine final : EngineBase {
         cudaGraph_t body = cp.conditional.phGraph_out[0];
         ca.use_cond = 1;
         ca.cond = h;
+        // K5 (finalize) under an IF node set by K4: launched only in rounds where
+        // a slot finished (a handful per batch) instead of as a no-op every round
+        cudaGraphConditionalHandle hf;
+        BH_CUDA(cudaGraphConditionalHandleCreate(&hf, body, 0, cudaGraphCondAssignDefault));
+        ca.use_fin_cond = 1;
+        ca.fin_cond = hf;
         BH_CUDA(cudaStreamBeginCaptureToGraph(cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
         const int64_t launches0 = stats.launches;
         launch_round(rs, ca, fa, cap_stream, 0, false);
         stats.launches = launches0;
-        count_launch(-launches_per_round());  // captured, not launched
+        count_launch(-(launches_per_round() - 1));  // captured, not launched
         cudaGraph_t captured;
         BH_CUDA(cudaStreamEndCapture(cap_stream, &captured));
+        {  // the IF node after the body's leaf (K4)
+            size_t n_nodes = 0;
+            BH_CUDA(cudaGraphGetNodes(body, nullptr, &n_nodes));
+            std::vector<cudaGraphNode_t> nodes(n_nodes);
+            BH_CUDA(cudaGraphGetNodes(body, nodes.data(), &n_nodes));
+            std::vector<cudaGraphNode_t> leaves;
+            for (cudaGraphNode_t nd : nodes) {
+                size_t n_dep = 0;
+                BH_CUDA(cudaGraphNodeGetDependentNodes(nd, nullptr, &n_dep));
+                if (n_dep == 0) leaves.push_back(nd);
+            }
+            cudaGraphNodeParams ip = {};
+            ip.type = cudaGraphNodeTypeConditional;
+            ip.conditional.handle = hf;
+            ip.conditional.type = cudaGraphCondTypeIf;
+            ip.conditional.size = 1;
+            cudaGraphNode_t if_node;
+            BH_CUDA(cudaGraphAddNode(&if_node, body, leaves.data(), leaves.size(), &ip));
+            cudaGraph_t if_body = ip.conditional.phGraph_out[0];
+            BH_CUDA(cudaStreamBeginCaptureToGraph(cap_stream, if_body, nullptr, nullptr, 0,
+                                                  cudaStreamCaptureModeThreadLocal));
+            k_finalize<T><<<grid_k5, TOPK_THREADS, 0, cap_stream>>>(fa);
+            BH_CUDA(cudaGetLastError());
+            cudaGraph_t captured_if;
+            BH_CUDA(cudaStreamEndCapture(cap_stream, &captured_if));
+        }
         BH_CUDA(cudaGraphInstantiate(&graph_exec, graph, 0));
         graph_key = key;
     }
@@ -761,8 +793,10 @@ struct Engine final : EngineBase {
         BH_CUDA(cudaStreamSynchronize(st));
         if (h_ctl->error) throw CudaError("query batch did not terminate");
         stats.rounds = h_ctl->rounds_active;
-        stats.launches += launches_per_round() * (int64_t)h_ctl->rounds_active;
-        count_launch((int)(launches_per_round() * h_ctl->rounds_active));
+        // graph path: K5 only in the rounds where a slot finished (IF node)
+        const int64_t n_launch = (launches_per_round() - 1) * (int64_t)h_ctl->rounds_active + h_ctl->fin_rounds;
+        stats.launches += n_launch;
+        count_launch((int)n_launch);
     }
 
     void read_ledger(int s, double *r_dev, double *est_dev, cudaStream_t st) override {
