@@ -59,3 +59,20 @@ def test_mcsp_query_two_sided_bound_and_deadline():
     assert r.method == "mcsp" and r.phase_trace["forward"]["n_walks"] == bh.mc_walk_count(eps / 2, 1e-6, g.u_count)
     with pytest.raises(bh.DeadlineExceeded):
         bh.mcsp_query(g, alias, 0, 0.15, 1e-3, deadline=time.perf_counter() - 1.0)
+
+
+def test_similarity_rows_batched_prefetch_matches_single_queries():
+    """evalkit's row factory (evalkit.py:270-308) on the batched engine: one
+    prefetch call, rows equal to per-node bhpp_query scores; memoised."""
+    g = config_graph("c1")
+    meta = bh.build_index_meta(g, 0.15)
+    row = bh.similarity_rows("ssbipush", g, meta, epsilon=1e-6)
+    nodes = [0, 17, 5, 17, 999]
+    row.prefetch(nodes)
+    assert sorted(row.cache) == [0, 5, 17, 999]
+    for ui in (0, 17, 999):
+        np.testing.assert_allclose(row(ui), bh.bhpp_query(g, meta, ui, 1e-6).scores, atol=1e-12, rtol=0)
+    first = row(5)
+    assert row(5) is first  # memoised
+    extra = row(3)          # uncached node: a batch of one
+    np.testing.assert_allclose(extra, bh.bhpp_query(g, meta, 3, 1e-6).scores, atol=1e-12, rtol=0)

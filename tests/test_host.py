@@ -248,3 +248,10 @@ def test_host_side_abi_error_paths():
         _capi.check(_capi.BH_EINVAL)
     with pytest.raises(MemoryError):
         _capi.check(_capi.BH_ENOMEM)
+
+
+def test_similarity_rows_rejects_methods_off_the_bhpp_path():
+    g = bh.BipartiteGraph(["a", "b"], ["x"], [0, 1], [0, 0], [1.0, 2.0])
+    for m in ("jaccard", "naive-ppr", "nope"):
+        with pytest.raises(bh.DataError):
+            bh.similarity_rows(m, g)
