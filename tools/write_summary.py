@@ -16,8 +16,9 @@ tab = subprocess.run([sys.executable, "tools/ncu_extract.py", rep], capture_outp
 steps = d["steps"]
 print(f"""# Round 1 profiles (B200, sm_100a) -- config c2, fp32 storage / fp64 accumulation, B = 64 slots
 
-Build: `k_pull_sw` pulls (S = 8 rows in flight, shared-memory windows, 3 blocks/SM), batched
-elementwise K1/K1a, shuffle-tree K4, one CUDA graph per batch (WHILE node, PDL launches).
+Build: `k_pull_sw` pulls (S = 8 rows in flight, shared-memory windows, 3 blocks/SM), predicated
+elementwise K1/K1a (one node per thread, 4 blocks/SM; r_A := 0 and est += alpha r done in K1a),
+K4 with one load round trip, one CUDA graph per batch (WHILE node, PDL launches, K5 under an IF node).
 Commands: `tools/measure_round.sh` (bench line, reference arm, launch list, ncu full set).
 
 ## Bench line (`python bench.py`: {steps} timed steps, {d['warmup']} warm-up)
@@ -58,7 +59,9 @@ Reading:
 - The two pulls are ~58 % of device time; each gathers 2e6 operand rows of 256 B per round from
   L2 (~69 % L2 hit); k_pull_sw executes 19-20 warp instructions per edge on the V side and 16 on
   the U side (22.5 / 18 for the round-1 baseline k_pull).
-- K1/K1a are latency-bound elementwise passes (issue 27-36 %, occupancy 24 % at 99-105
-  registers); four nodes per thread in flight made them 12 % faster in the event timing.
-- K4 is ~11.5 us of latency-bound control per round; K5 returns at once unless a slot finished.
+- K1/K1a are latency-bound elementwise passes.  Moving the residue zeroing and the estimate
+  update from K1 into K1a (K1a re-takes K1's threshold decision on the same r), predicating the
+  per-slot logic and running one node per thread at 4 blocks/SM took prep from 6.5 to 5.6 ms per step.
+- K4 is latency-bound control (~9 us per round); K5 runs only in rounds where a slot finished
+  (CUDA-graph IF node); its radix select no longer uses a 64-bit shared atomic (a CAS loop).
 """)
