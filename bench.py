@@ -279,12 +279,6 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-    # the submitting thread stays on one core for the GPU legs (restored for the
-    # CPU baseline): a migrating host thread adds scheduling stalls to the
-    # host-API (e2e) steps
-    all_cpus = os.sched_getaffinity(0)
-    cpus = sorted(all_cpus)
-    os.sched_setaffinity(0, {cpus[(2 * local + 1) % len(cpus)]})
 
     cfg, g, src = workload(args.config, rank)
     meta = bh.build_index_meta(g, cfg.alpha)
@@ -402,23 +396,34 @@ def run_ours(args):
     for _ in range(2):
         bh.bhpp_query_batch(g, meta, src, eps, k=k, dtype=args.dtype, slots=args.slots or None,
                             stream=stream.cuda_stream)
-    e2e_n = max(args.steps, 10)  # more samples: host-scheduling outliers on a fresh box
+    e2e_n = max(args.steps, 10)  # e2e steps are cheap: at least 10 samples
+    gc_events = [0]
+    if os.environ.get("BH_BENCH_E2E_DIAG"):
+        import gc
+        gc.callbacks.append(lambda phase, info: gc_events.__setitem__(0, gc_events[0] + (phase == "start")))
     for _ in range(e2e_n):
         with torch.cuda.stream(stream):
             flush_buf.fill_(1.0)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
+        th0 = time.perf_counter()
         e0.record(stream)
         res = bh.bhpp_query_batch(g, meta, src, eps, k=k, dtype=args.dtype, slots=args.slots or None,
                                   stream=stream.cuda_stream)
+        th1 = time.perf_counter()
         if world > 1:
             from paper_2312_06724_b200.distributed import gather_results as _gr
             with torch.cuda.stream(stream):
                 _gr(res.topk_index, res.topk_score, res.traces, world * n, rank, world, device=dev)
         e1.record(stream)
+        th2 = time.perf_counter()
         e1.synchronize()
         e2e_ms += e0.elapsed_time(e1)
         e2e_steps.append(round(e0.elapsed_time(e1), 3))
+        if os.environ.get("BH_BENCH_E2E_DIAG"):
+            print(f"[e2e diag] event {e0.elapsed_time(e1):.3f} ms, host call {1e3 * (th1 - th0):.3f} ms, "
+                  f"engine {1e3 * res.timing['total']:.3f} ms, to e1 {1e3 * (th2 - th0):.3f} ms, gc {gc_events[0]}",
+                  file=sys.stderr, flush=True)
     if world > 1:
         t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -435,7 +440,6 @@ def run_ours(args):
                 "roofline_achieved_gbs": alg64 / (k64 / 1e3) / 1e9 if k64 else None}
 
     cpu = None
-    os.sched_setaffinity(0, all_cpus)
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_leg(g, src, cfg.alpha, eps_b, eps_f, meta.lam, args.cpu_seconds)
 

@@ -21,6 +21,13 @@
 #include "topk.cuh"
 
 namespace bh {
+// BH_TRACE_E2E diagnostics: host timestamps (us) of the stages of a host-pointer batch
+static double g_tstamp[8];
+static inline double host_us() {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+}  // namespace bh
+namespace bh {
 
 bh_graph *graph_create(int64_t, int64_t, int64_t, const int64_t *, const int32_t *, const double *,
                        const int64_t *, const int32_t *, const double *, const double *, const double *,
@@ -741,8 +748,11 @@ struct Engine final : EngineBase {
         stats.launches = 1;
         ca.max_rounds = 100000000;
         if (!rs.hook && !prof && !dbg_v && !getenv("BH_NO_GRAPH")) {
+            g_tstamp[3] = host_us();
             ensure_graph(rs, ca, fa);
+            g_tstamp[4] = host_us();
             BH_CUDA(cudaGraphLaunch(graph_exec, st));
+            g_tstamp[5] = host_us();
             BH_CUDA(cudaMemcpyAsync(h_ctl, ctl, sizeof(Control), cudaMemcpyDeviceToHost, st));
             pending = st;
             if (!rs.async) finish();
@@ -830,7 +840,7 @@ struct EngineCache {
     int64_t cap_sc = 0;
     double *d_vec_a = nullptr, *d_vec_b = nullptr;
     int64_t cap_vec = 0;
-    unsigned char *h_stage = nullptr;  // pinned staging for the host-pointer outputs
+    unsigned char *h_stage = nullptr;  // pinned staging for the host-pointer inputs and outputs
     size_t cap_stage = 0;
     ~EngineCache() {
         by_b.clear();
@@ -871,10 +881,13 @@ static EngineBase *make_engine(bh_graph *g, int B) {
     }
 }
 
-static int auto_slots(const bh_graph *g, int64_t n_q) {
+static int auto_slots(bh_graph *g, int64_t n_q) {
     // 128 slots once the batch fills them: per-round cost grows sub-linearly in B
     // (c5 on B200: 2189 q/s at 64 slots, 2625 at 128)
     int b = n_q <= 1 ? 1 : n_q <= 4 ? 4 : n_q <= 16 ? 16 : n_q <= 32 ? 32 : n_q <= 64 ? 64 : 128;
+    // an engine of that width exists: no device-memory query (cudaMemGetInfo goes to
+    // the driver and was measured stalling a call by up to 100 ms on a busy host)
+    if (cache_of(g).by_b.count(b)) return b;
     // keep the per-slot state within a fraction of device memory
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
@@ -1061,6 +1074,7 @@ int bh_query_wait(bh_graph *g) {
         std::lock_guard<std::mutex> lock(g->mu);
         BH_CUDA(cudaSetDevice(g->device));
         EngineCache &c = cache_of(g);
+        g_tstamp[0] = host_us();
         EngineBase *e = c.pending;
         c.pending = nullptr;
         if (e) e->finish();
@@ -1130,6 +1144,8 @@ int bh_graph_get_info(const bh_graph *g, bh_graph_info *out) {
 int bh_query_batch(bh_graph *g, const bh_query_params *p, const int32_t *sources, int64_t n_q,
                    const int32_t *tie_skip, int32_t *topk_idx, double *topk_score, bh_trace *trace,
                    double *scores, void *stream) {
+    const double t_entry =
+        std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
     return guarded([&] {
         if (!g || !p || !trace) throw InvalidArg("null argument");
         if (n_q < 0 || n_q > (1LL << 31) - 1) throw InvalidArg("bad query count");
@@ -1139,6 +1155,7 @@ int bh_query_batch(bh_graph *g, const bh_query_params *p, const int32_t *sources
         std::lock_guard<std::mutex> lock(g->mu);
         BH_CUDA(cudaSetDevice(g->device));
         EngineCache &c = cache_of(g);
+        g_tstamp[0] = host_us();
         if (c.pending) {  // an async batch not yet waited for: complete it first
             EngineBase *e0 = c.pending;
             c.pending = nullptr;
@@ -1170,15 +1187,14 @@ int bh_query_batch(bh_graph *g, const bh_query_params *p, const int32_t *sources
             e.run(rs, st);
             return;
         }
-        // host pointers: validate, stage in, run, stage out
+        // host pointers: validate, stage in, run, stage out.  Inputs and outputs go
+        // through one pinned staging buffer (a pageable H2D copy would synchronise the
+        // stream first), the outputs copied device -> pinned right behind the batch on
+        // the stream: one synchronisation, no host turnaround between the batch and its copies.
         for (int64_t i = 0; i < n_q; i++)
             if (sources[i] < 0 || sources[i] >= g->n_u) throw InvalidArg("node index out of range");
         grow(c.d_src, c.cap_q, n_q);
-        BH_CUDA(cudaMemcpyAsync(c.d_src, sources, n_q * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-        if (tie_skip) {
-            grow(c.d_tie, c.cap_tie, n_q);
-            BH_CUDA(cudaMemcpyAsync(c.d_tie, tie_skip, n_q * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-        }
+        if (tie_skip) grow(c.d_tie, c.cap_tie, n_q);
         grow(c.d_trace, c.cap_tr, n_q);
         rs.sources = c.d_src;
         rs.tie = tie_skip ? c.d_tie : nullptr;
@@ -1193,14 +1209,13 @@ int bh_query_batch(bh_graph *g, const bh_query_params *p, const int32_t *sources
             grow(c.d_scores, c.cap_sc, n_q * g->n_u);
             rs.scores = c.d_scores;
         }
-        // outputs go device -> pinned staging right behind the batch on the stream
-        // (one synchronisation, no host turnaround between the batch and its copies),
-        // then staging -> caller arrays on the host
+        const size_t b_in = n_q * sizeof(int32_t) * (tie_skip ? 2 : 1);
         const size_t b_tr = n_q * sizeof(bh_trace);
         const size_t b_ti = rs.topk_idx ? n_q * p->k * sizeof(int32_t) : 0;
         const size_t b_ts = rs.topk_idx && topk_score ? n_q * p->k * sizeof(double) : 0;
         const size_t b_sc = rs.want_scores ? n_q * g->n_u * sizeof(double) : 0;  // large: copied directly
-        const size_t need = b_tr + b_ti + b_ts;
+        const size_t off_tr = (b_in + 15) / 16 * 16;
+        const size_t need = off_tr + b_tr + b_ti + b_ts;
         if (need > c.cap_stage) {
             if (c.h_stage) cudaFreeHost(c.h_stage);
             c.h_stage = nullptr;
@@ -1208,7 +1223,15 @@ int bh_query_batch(bh_graph *g, const bh_query_params *p, const int32_t *sources
             BH_CUDA(cudaMallocHost(&c.h_stage, need));
             c.cap_stage = need;
         }
-        unsigned char *h_tr = c.h_stage, *h_ti = h_tr + b_tr, *h_ts = h_ti + b_ti;
+        g_tstamp[1] = host_us();
+        int32_t *h_src = reinterpret_cast<int32_t *>(c.h_stage);
+        std::memcpy(h_src, sources, n_q * sizeof(int32_t));
+        BH_CUDA(cudaMemcpyAsync(c.d_src, h_src, n_q * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+        if (tie_skip) {
+            std::memcpy(h_src + n_q, tie_skip, n_q * sizeof(int32_t));
+            BH_CUDA(cudaMemcpyAsync(c.d_tie, h_src + n_q, n_q * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+        }
+        unsigned char *h_tr = c.h_stage + off_tr, *h_ti = h_tr + b_tr, *h_ts = h_ti + b_ti;
         rs.async = true;
         // BH_TRACE_E2E=1: host-path phase times on stderr (diagnostic)
         static const bool trace_e2e = getenv("BH_TRACE_E2E") != nullptr;
@@ -1216,7 +1239,8 @@ int bh_query_batch(bh_graph *g, const bh_query_params *p, const int32_t *sources
         auto now_us = [] {
             return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
         };
-        double th[4] = {now_us(), 0, 0, 0};
+        double th[4] = {t_entry, 0, 0, 0};
+        g_tstamp[2] = host_us();
         if (trace_e2e) {
             for (auto &x : tev) BH_CUDA(cudaEventCreate(&x));
             BH_CUDA(cudaEventRecord(tev[0], st));
@@ -1237,8 +1261,11 @@ int bh_query_batch(bh_graph *g, const bh_query_params *p, const int32_t *sources
             float d_graph = 0.f, d_out = 0.f;
             BH_CUDA(cudaEventElapsedTime(&d_graph, tev[0], tev[1]));
             BH_CUDA(cudaEventElapsedTime(&d_out, tev[1], tev[2]));
-            fprintf(stderr, "[bh e2e] host: launch %.1f us, copies enqueued %.1f us, wait %.1f us; device: batch %.3f ms, "
-                    "outputs %.3f ms\n", th[1] - th[0], th[2] - th[1], th[3] - th[2], d_graph, d_out);
+            fprintf(stderr, "[bh e2e] host: entry to launch %.1f us (lock %.1f, setup %.1f, inputs %.1f, run %.1f, graph %.1f, "
+                    "launch %.1f), copies enqueued %.1f us, wait %.1f us; device: batch %.3f ms, outputs %.3f ms\n",
+                    th[1] - th[0], g_tstamp[0] - th[0], g_tstamp[1] - g_tstamp[0], g_tstamp[2] - g_tstamp[1],
+                    g_tstamp[3] - g_tstamp[2], g_tstamp[4] - g_tstamp[3], g_tstamp[5] - g_tstamp[4], th[2] - th[1],
+                    th[3] - th[2], d_graph, d_out);
             for (auto &x : tev) cudaEventDestroy(x);
         }
         std::memcpy(trace, h_tr, b_tr);
@@ -1261,6 +1288,7 @@ int bh_push_run(bh_graph *g, int32_t job, int32_t source, double alpha, double l
         std::lock_guard<std::mutex> lock(g->mu);
         BH_CUDA(cudaSetDevice(g->device));
         EngineCache &c = cache_of(g);
+        g_tstamp[0] = host_us();
         cudaStream_t st = c.stream;
         EngineBase &e = engine_for(g, 1);
         const int64_t nu = g->n_u;
@@ -1322,6 +1350,7 @@ int bh_power_iteration(bh_graph *g, const double *start, int64_t n_vec, double a
         std::lock_guard<std::mutex> lock(g->mu);
         BH_CUDA(cudaSetDevice(g->device));
         EngineCache &c = cache_of(g);
+        g_tstamp[0] = host_us();
         cudaStream_t st = c.stream;
         const int64_t nu = g->n_u;
         const int B = auto_slots(g, n_vec);

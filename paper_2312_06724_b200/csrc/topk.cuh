@@ -306,18 +306,39 @@ __global__ void __launch_bounds__(TOPK_THREADS) k_finalize(FinalArgs<T> a) {
             double *dst = score_row(a, s, f);
             const int64_t u0 = (int64_t)c * a.chunk;
             const int64_t u1 = imin64(a.n_u, u0 + a.chunk);
-            for (int64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
-                const double est = (double)a.EST[u * B + s];
-                const double ws = a.ws_u[u];
-                double v;
-                if (f.job == BH_JOB_POWER) {
-                    v = a.alpha * (ws * (double)a.P[u * B + s]);
-                } else {
-                    v = (ws * f.inv_ws_q) * est;                                  // w_ratio * est
-                    if (f.has_pi) v = v + a.alpha * (ws * (double)a.P[u * B + s]);  // + alpha acc_t
-                    if (f.job == BH_JOB_BHPP) v = v + est;                         // + backward est
+            // SEL_ITEMS nodes per thread, all loads issued before any is used
+            // (a chunk is SEL_ITEMS * blockDim nodes; the columns are strided reads)
+            const bool need_p = f.job == BH_JOB_POWER || f.has_pi;
+            for (int64_t ub = u0; ub < u1; ub += (int64_t)SEL_ITEMS * blockDim.x) {
+                T ev[SEL_ITEMS], pv[SEL_ITEMS];
+                double wv[SEL_ITEMS];
+#pragma unroll
+                for (int j = 0; j < SEL_ITEMS; j++) {
+                    const int64_t u = ub + threadIdx.x + (int64_t)j * blockDim.x;
+                    ev[j] = pv[j] = (T)0;
+                    wv[j] = 0.0;
+                    if (u < u1) {
+                        ev[j] = a.EST[u * B + s];
+                        wv[j] = a.ws_u[u];
+                        if (need_p) pv[j] = a.P[u * B + s];
+                    }
                 }
-                dst[u] = v;
+#pragma unroll
+                for (int j = 0; j < SEL_ITEMS; j++) {
+                    const int64_t u = ub + threadIdx.x + (int64_t)j * blockDim.x;
+                    if (u >= u1) continue;
+                    const double est = (double)ev[j];
+                    const double ws = wv[j];
+                    double v;
+                    if (f.job == BH_JOB_POWER) {
+                        v = a.alpha * (ws * (double)pv[j]);
+                    } else {
+                        v = (ws * f.inv_ws_q) * est;                               // w_ratio * est
+                        if (f.has_pi) v = v + a.alpha * (ws * (double)pv[j]);       // + alpha acc_t
+                        if (f.job == BH_JOB_BHPP) v = v + est;                      // + backward est
+                    }
+                    dst[u] = v;
+                }
             }
             if (a.k > 0) {
                 __syncthreads();
