@@ -339,7 +339,9 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
         const bool free_now = fin || sl.op == OP_IDLE;
         if (free_now) sl.qidx = fin ? sl.qidx : -1;
         a.slots[s] = sl;
-        ctl->free_slot[s] = (free_now ? 1 : 0) | (fin ? 2 : 0);
+        // a slot that finished this round is refilled one round later: K5 reads its
+        // columns concurrently with the next round's K1 (which would initialise them)
+        ctl->free_slot[s] = (free_now && !fin ? 1 : 0) | (fin ? 2 : 0);
         __threadfence();
         // arrival count in the low 16 bits, free slots above: the last block
         // learns whether any slot needs the refill pass
@@ -410,7 +412,7 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
             busy = *(volatile int32_t *)&a.slots[tid].op != OP_IDLE;
         }
     }
-    busy = __syncthreads_or(busy);
+    busy = __syncthreads_or(busy) || next0 + nfree < n_q;  // queries left for the draining slots
     if (tid == 0) {
         ctl->next_q = min(n_q, next0 + nfree);
         ctl->n_fin = nfin;

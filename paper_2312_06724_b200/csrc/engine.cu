@@ -549,9 +549,12 @@ struct Engine final : EngineBase {
         }
     }
 
+    // One round: K5 (the slots K4 finished last round) | K1 K2 K3 K1a | K4.  In the
+    // batch graph K5 sits under an IF node on a branch parallel to K1..K1a (a finished
+    // slot is refilled one round later, so nothing else touches its columns meanwhile).
     void launch_round(const RunSpec &rs, const ControlArgs &ca, const FinalArgs<T> &fa, cudaStream_t st,
-                      int64_t round, bool prof) {
-        const size_t e0 = (size_t)round * 6;
+                      int64_t round, bool prof, bool with_k5 = true, bool with_k4 = true) {
+        const size_t e0 = (size_t)round * 7;
         ElemArgs<T> ea{};
         ea.n_u = g->n_u;
         ea.R = R;
@@ -567,18 +570,19 @@ struct Engine final : EngineBase {
         ea.part = part;
         ea.alpha = rs.alpha;
         if (prof) BH_CUDA(cudaEventRecord(ev(e0), st));
-        launch_pdl(push_kernel(), grid_elem, ELEM_THREADS, 0, st, ea);
+        if (with_k5) launch_pdl(k_finalize<T>, grid_k5, TOPK_THREADS, 0, st, fa);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 1), st));
-        launch_pull(SIDE_V, pull_args(SIDE_V, rs.alpha), st);
+        launch_pdl(push_kernel(), grid_elem, ELEM_THREADS, 0, st, ea);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 2), st));
-        launch_pull(SIDE_U, pull_args(SIDE_U, rs.alpha), st);
+        launch_pull(SIDE_V, pull_args(SIDE_V, rs.alpha), st);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 3), st));
-        if (!fuse_combine) launch_pdl(combine_kernel(), grid_comb, ELEM_THREADS, 0, st, ea);
+        launch_pull(SIDE_U, pull_args(SIDE_U, rs.alpha), st);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 4), st));
-        launch_pdl(k_control, B, CONTROL_THREADS, 0, st, ca);
-        if (!ca.use_fin_cond) launch_pdl(k_finalize<T>, grid_k5, TOPK_THREADS, 0, st, fa);
+        if (!fuse_combine) launch_pdl(combine_kernel(), grid_comb, ELEM_THREADS, 0, st, ea);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 5), st));
-        const int launches = launches_per_round();
+        if (with_k4) launch_pdl(k_control, B, CONTROL_THREADS, 0, st, ca);
+        if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 6), st));
+        const int launches = launches_per_round() - (with_k5 ? 0 : 1) - (with_k4 ? 0 : 1);
         count_launch(launches);
         stats.launches += launches;
         BH_CUDA(cudaGetLastError());
@@ -587,18 +591,19 @@ struct Engine final : EngineBase {
     int launches_per_round() const { return fuse_combine ? 5 : 6; }
 
     void collect_profile(int64_t rounds) {
-        double t[5] = {0, 0, 0, 0, 0};
+        // events per round: K5 | K1 | K2 | K3 | K1a | K4
+        double t[6] = {0, 0, 0, 0, 0, 0};
         for (int64_t r = 0; r < rounds; r++) {
-            for (int j = 0; j < 5; j++) {
+            for (int j = 0; j < 6; j++) {
                 float ms = 0.f;
-                BH_CUDA(cudaEventElapsedTime(&ms, ev((size_t)r * 6 + j), ev((size_t)r * 6 + j + 1)));
+                BH_CUDA(cudaEventElapsedTime(&ms, ev((size_t)r * 7 + j), ev((size_t)r * 7 + j + 1)));
                 t[j] += ms;
             }
         }
-        stats.ms_prep = t[0] + t[3];
-        stats.ms_vpull = t[1];
-        stats.ms_upull = t[2];
-        stats.ms_control = t[4];
+        stats.ms_prep = t[1] + t[4];
+        stats.ms_vpull = t[2];
+        stats.ms_upull = t[3];
+        stats.ms_control = t[0] + t[5];
         stats.profiled = 1;
     }
 
@@ -635,45 +640,39 @@ struct Engine final : EngineBase {
         cudaGraph_t body = cp.conditional.phGraph_out[0];
         ca.use_cond = 1;
         ca.cond = h;
-        // K5 (finalize) under an IF node set by K4: launched only in rounds where
-        // a slot finished (a handful per batch) instead of as a no-op every round
+        // K5 (finalize of the slots the previous round's K4 finished) under an IF node
+        // set by K4, on a branch parallel to K1..K1a; K4 waits for both
         cudaGraphConditionalHandle hf;
         BH_CUDA(cudaGraphConditionalHandleCreate(&hf, body, 0, cudaGraphCondAssignDefault));
         ca.use_fin_cond = 1;
         ca.fin_cond = hf;
-        BH_CUDA(cudaStreamBeginCaptureToGraph(cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-        const int64_t launches0 = stats.launches;
-        launch_round(rs, ca, fa, cap_stream, 0, false);
-        stats.launches = launches0;
-        count_launch(-(launches_per_round() - 1));  // captured, not launched
+        cudaGraphNodeParams ip = {};
+        ip.type = cudaGraphNodeTypeConditional;
+        ip.conditional.handle = hf;
+        ip.conditional.type = cudaGraphCondTypeIf;
+        ip.conditional.size = 1;
+        cudaGraphNode_t if_node;
+        BH_CUDA(cudaGraphAddNode(&if_node, body, nullptr, 0, &ip));
+        cudaGraph_t if_body = ip.conditional.phGraph_out[0];
         cudaGraph_t captured;
+        BH_CUDA(cudaStreamBeginCaptureToGraph(cap_stream, if_body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        k_finalize<T><<<grid_k5, TOPK_THREADS, 0, cap_stream>>>(fa);
+        BH_CUDA(cudaGetLastError());
         BH_CUDA(cudaStreamEndCapture(cap_stream, &captured));
-        {  // the IF node after the body's leaf (K4)
-            size_t n_nodes = 0;
-            BH_CUDA(cudaGraphGetNodes(body, nullptr, &n_nodes));
-            std::vector<cudaGraphNode_t> nodes(n_nodes);
-            BH_CUDA(cudaGraphGetNodes(body, nodes.data(), &n_nodes));
-            std::vector<cudaGraphNode_t> leaves;
-            for (cudaGraphNode_t nd : nodes) {
-                size_t n_dep = 0;
-                BH_CUDA(cudaGraphNodeGetDependentNodes(nd, nullptr, &n_dep));
-                if (n_dep == 0) leaves.push_back(nd);
-            }
-            cudaGraphNodeParams ip = {};
-            ip.type = cudaGraphNodeTypeConditional;
-            ip.conditional.handle = hf;
-            ip.conditional.type = cudaGraphCondTypeIf;
-            ip.conditional.size = 1;
-            cudaGraphNode_t if_node;
-            BH_CUDA(cudaGraphAddNode(&if_node, body, leaves.data(), leaves.size(), &ip));
-            cudaGraph_t if_body = ip.conditional.phGraph_out[0];
-            BH_CUDA(cudaStreamBeginCaptureToGraph(cap_stream, if_body, nullptr, nullptr, 0,
-                                                  cudaStreamCaptureModeThreadLocal));
-            k_finalize<T><<<grid_k5, TOPK_THREADS, 0, cap_stream>>>(fa);
-            BH_CUDA(cudaGetLastError());
-            cudaGraph_t captured_if;
-            BH_CUDA(cudaStreamEndCapture(cap_stream, &captured_if));
-        }
+        const int64_t launches0 = stats.launches;
+        BH_CUDA(cudaStreamBeginCaptureToGraph(cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        launch_round(rs, ca, fa, cap_stream, 0, false, /*with_k5=*/false, /*with_k4=*/false);
+        BH_CUDA(cudaStreamUpdateCaptureDependencies(cap_stream, &if_node, 1, cudaStreamAddCaptureDependencies));
+        launch_pdl(k_control, B, CONTROL_THREADS, 0, cap_stream, ca);
+        BH_CUDA(cudaGetLastError());
+        BH_CUDA(cudaStreamEndCapture(cap_stream, &captured));
+        // after the loop: K5 for the slots the last round finished
+        BH_CUDA(cudaStreamBeginCaptureToGraph(cap_stream, graph, &node, nullptr, 1, cudaStreamCaptureModeThreadLocal));
+        k_finalize<T><<<grid_k5, TOPK_THREADS, 0, cap_stream>>>(fa);
+        BH_CUDA(cudaGetLastError());
+        BH_CUDA(cudaStreamEndCapture(cap_stream, &captured));
+        stats.launches = launches0;
+        count_launch(-(launches_per_round() - 2));  // launch_round counted K1..K1a: captured, not launched
         BH_CUDA(cudaGraphInstantiate(&graph_exec, graph, 0));
         graph_key = key;
     }
