@@ -115,14 +115,11 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
     const int s = blockIdx.x;
     const int B = a.B;
     Control *ctl = a.ctl;
-    if (ctl->active == 0 && !a.first) {
-        if (s == 0 && tid == 0) {
-            ctl->n_fin = 0;
-            if (a.use_cond) cudaGraphSetConditional(a.cond, 0);
-            if (a.use_fin_cond) cudaGraphSetConditional(a.fin_cond, 0);
-        }
-        return;
-    }
+    // loads issued before any is used: the activity flag, the slot (thread 0) and
+    // the partial rows below are independent
+    const int32_t active = ctl->active;
+    Slot sl;
+    if (tid == 0) sl = a.slots[s];
     // Deterministic reduction of the slot's partial rows: each thread adds a
     // fixed strided subset (4 independent loads in flight), then a fixed-shape
     // shuffle tree per warp and across the warps.
@@ -175,6 +172,14 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
             for (int j = 0; j < U16; j++) np += n16[j];
         }
     }
+    if (active == 0 && !a.first) {
+        if (s == 0 && tid == 0) {
+            ctl->n_fin = 0;
+            if (a.use_cond) cudaGraphSetConditional(a.cond, 0);
+            if (a.use_fin_cond) cudaGraphSetConditional(a.fin_cond, 0);
+        }
+        return;
+    }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
         cnt += __shfl_down_sync(0xffffffffu, cnt, off);
@@ -204,7 +209,6 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
         }
     }
     if (tid == 0) {
-        Slot sl = a.slots[s];
         bool fin = false;
         const int op = a.first ? OP_IDLE : sl.op;
         const int64_t cnt = w_cnt[0];
