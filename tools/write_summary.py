@@ -18,7 +18,8 @@ print(f"""# Round 1 profiles (B200, sm_100a) -- config c2, fp32 storage / fp64 a
 
 Build: `k_pull_sw` pulls (S = 8 rows in flight, shared-memory windows, 3 blocks/SM), predicated
 elementwise K1/K1a (one node per thread, 4 blocks/SM; r_A := 0 and est += alpha r done in K1a),
-K4 with one load round trip, one CUDA graph per batch (WHILE node, PDL launches, K5 under an IF node).
+K4 with one load round trip, one CUDA graph per batch (WHILE node, PDL launches; K5 under an IF node on a
+branch parallel to the next round's K1..K1a).
 Commands: `tools/measure_round.sh` (bench line, reference arm, launch list, ncu full set).
 
 ## Bench line (`python bench.py`: {steps} timed steps, {d['warmup']} warm-up)
@@ -62,6 +63,9 @@ Reading:
 - K1/K1a are latency-bound elementwise passes.  Moving the residue zeroing and the estimate
   update from K1 into K1a (K1a re-takes K1's threshold decision on the same r), predicating the
   per-slot logic and running one node per thread at 4 blocks/SM took prep from 6.5 to 5.6 ms per step.
-- K4 is latency-bound control (~9 us per round); K5 runs only in rounds where a slot finished
-  (CUDA-graph IF node); its radix select no longer uses a 64-bit shared atomic (a CAS loop).
+- K4 is latency-bound control (~8 us per round).  K5 runs only after rounds where a slot
+  finished, under a CUDA-graph IF node, concurrently with the next round's K1..K1a.  A finished
+  slot is refilled one round later.  Its radix select no longer uses a 64-bit shared atomic,
+  which compiled to a CAS loop.  In the eager launch list below, K5 is still launched every
+  round and is a no-op when no slot finished.
 """)
