@@ -245,10 +245,12 @@ struct Engine final : EngineBase {
     using ElemFn = void (*)(ElemArgs<T>);
     // K1 / K1a geometry (nodes in flight per thread, blocks per SM): one node at
     // 4 blocks/SM measured fastest for fp32 at c2 (prep 6.5 -> 5.6 ms per step
-    // against 2 nodes at 3 blocks/SM); tuning override BH_ELEM_PUSH /
-    // BH_ELEM_COMBINE = "UNR,MINB" (wide engines only).
+    // against 2 nodes at 3 blocks/SM), K1a software-pipelined at 3 blocks/SM;
+    // tuning override BH_ELEM_PUSH / BH_ELEM_COMBINE = "UNR,MINB" or "pUNR,MINB"
+    // (pipelined) for the wide engines.
     int push_cfg = 0, comb_cfg = 0;
-    static constexpr const char *ELEM_CFGS[] = {"", "2,2", "4,2", "1,4", "1,3", "1,5", "1,6", "2,3", "2,4"};
+    static constexpr const char *ELEM_CFGS[] = {"", "2,2", "4,2", "1,4", "1,3", "1,5", "1,6", "2,3", "2,4",
+                                                "p1,4", "p1,3"};
     template <template <int, typename, int, int> class K>
     static ElemFn elem_variant(int cfg) {
         if constexpr (B < 32) cfg = 0;  // tuning variants only for the wide engines
@@ -261,13 +263,16 @@ struct Engine final : EngineBase {
             case 6: return K<B, T, 1, 6>::fn;
             case 7: return K<B, T, 2, 3>::fn;
             case 8: return K<B, T, 2, 4>::fn;
+            case 9: return K<B, T, -1, 4>::fn;   // "p": software-pipelined, one node per thread
+            case 10: return K<B, T, -1, 3>::fn;
             default: return sizeof(T) == 4 ? K<B, T, 1, 4>::fn : K<B, T, 2, 2>::fn;
         }
     }
+    // U_ = -1: software-pipelined variant (one node per thread)
     template <int B_, typename T_, int U_, int M_>
-    struct PushK { static constexpr ElemFn fn = k_push<B_, T_, U_, M_>; };
+    struct PushK { static constexpr ElemFn fn = k_push<B_, T_, (U_ < 0 ? 1 : U_), M_, (U_ < 0)>; };
     template <int B_, typename T_, int U_, int M_>
-    struct CombK { static constexpr ElemFn fn = k_combine<B_, T_, U_, M_>; };
+    struct CombK { static constexpr ElemFn fn = k_combine<B_, T_, (U_ < 0 ? 1 : U_), M_, (U_ < 0)>; };
     static int elem_cfg_from_env(const char *name) {
         const char *m = getenv(name);
         if (!m) return 0;
@@ -394,6 +399,8 @@ struct Engine final : EngineBase {
         }
         push_cfg = elem_cfg_from_env("BH_ELEM_PUSH");
         comb_cfg = elem_cfg_from_env("BH_ELEM_COMBINE");
+        // K1a fp32: software-pipelined at 3 blocks/SM (c2: prep 5.51 -> 5.32 ms per step)
+        if (getenv("BH_ELEM_COMBINE") == nullptr && sizeof(T) == 4) comb_cfg = 10;
         {  // one resident wave of the elementwise kernels
             int occ_p = 1, occ_c = 1;
             BH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, push_kernel(), ELEM_THREADS, 0));

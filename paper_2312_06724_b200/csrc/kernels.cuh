@@ -231,7 +231,7 @@ __device__ __forceinline__ void load_elem_consts(ElemSlotC &c, const Slot *__res
 // which re-takes the same decision on the same r; only the ledger-initialising
 // round writes r and est here.  Per element the work is predicated (the slots
 // of one warp are in different phases), loads of UNR nodes are in flight.
-template <int B, typename T, int ELEM_UNR = 4, int MINB = 1>
+template <int B, typename T, int ELEM_UNR = 4, int MINB = 1, bool PIPE = false>
 __global__ void __launch_bounds__(ELEM_THREADS, MINB) k_push(ElemArgs<T> a) {
     pdl_begin();
     if (*a.active == 0) return;
@@ -270,77 +270,96 @@ __global__ void __launch_bounds__(ELEM_THREADS, MINB) k_push(ElemArgs<T> a) {
     // thread's group (one round per query); the common body has neither
     auto run = [&](auto rare_tag) {
         constexpr bool RARE = decltype(rare_tag)::value;
-        const int64_t total = a.n_u * TPN;
-        const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-        for (int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t0 < total; t0 += ELEM_UNR * stride) {
-            T rv[ELEM_UNR][EV];
-            double iwsk[ELEM_UNR], wsk[ELEM_UNR];
-            int32_t degk[ELEM_UNR];
+        auto node = [&](int64_t u, T (&rv)[EV], double iwsv, double wsv, int32_t degv) {
+            const int64_t i = u * B + j0;
+            const double iws = iwsv;
+            T pv[EV];
+            bool act[EV];
+            double rr[EV];
 #pragma unroll
-            for (int k = 0; k < ELEM_UNR; k++) {
-                const int64_t t = t0 + k * stride;
-                if (t < total) {
-                    const int64_t u = t / TPN;
-                    VecIO<T, EV>::ld(a.R + u * B + j0, rv[k]);
-                    iwsk[k] = a.inv_ws_u[u];
-                    wsk[k] = m_fwd ? a.ws_u[u] : 0.0;
-                    degk[k] = a.deg_u[u];
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < ELEM_UNR; k++) {
-                const int64_t t = t0 + k * stride;
-                if (t >= total) break;
-                const int64_t u = t / TPN;
-                const int64_t i = u * B + j0;
-                const double iws = iwsk[k];
-                T pv[EV];
-                bool act[EV];
-                double rr[EV];
-#pragma unroll
-                for (int v = 0; v < EV; v++) {
-                    const int c = v * TPN + grp;
-                    const bool push = (m_push >> v) & 1u;
-                    const bool init = RARE && ((m_init >> v) & 1u);
-                    const double r = init ? (u == sc.src[j0 + v] ? 1.0 : 0.0) : (double)rv[k][v];
-                    const double th = fma(sc.thA[c] * iws, sc.thC[c], sc.thDp[c]);
-                    const bool pushed = push && r > th;
-                    act[v] = pushed;
-                    rr[v] = r;
-                    cnt[v] += pushed;
-                    npu[v] += pushed ? degk[k] : 0;
-                    if (((m_fwd >> v) & 1u) && !pushed)
-                        left[v] += (wsk[k] * sc.iwsq[c]) * r;  // w_ratio r left behind this round
-                    T p = pushed ? (T)r : (T)0;
-                    if ((m_entry >> v) & 1u) {
-                        // y0 = (w_ratio r) / ws = r / ws(q) (PI-Push tail, push_engine.py:246), or
-                        // start / ws for a raw power iteration (push_engine.py:112 on a = acc / ws)
-                        p = (T)((double)rv[k][v] * sc.ysc[c]);
-                        if (RARE && ((m_x0 >> v) & 1u)) {
-                            p = (T)(a.x0[(int64_t)sc.qidx[j0 + v] * a.n_u + u] * iws);
-                            rv[k][v] = p;
-                        }
+            for (int v = 0; v < EV; v++) {
+                const int c = v * TPN + grp;
+                const bool push = (m_push >> v) & 1u;
+                const bool init = RARE && ((m_init >> v) & 1u);
+                const double r = init ? (u == sc.src[j0 + v] ? 1.0 : 0.0) : (double)rv[v];
+                const double th = fma(sc.thA[c] * iws, sc.thC[c], sc.thDp[c]);
+                const bool pushed = push && r > th;
+                act[v] = pushed;
+                rr[v] = r;
+                cnt[v] += pushed;
+                npu[v] += pushed ? degv : 0;
+                if (((m_fwd >> v) & 1u) && !pushed)
+                    left[v] += (wsv * sc.iwsq[c]) * r;  // w_ratio r left behind this round
+                T p = pushed ? (T)r : (T)0;
+                if ((m_entry >> v) & 1u) {
+                    // y0 = (w_ratio r) / ws = r / ws(q) (PI-Push tail, push_engine.py:246), or
+                    // start / ws for a raw power iteration (push_engine.py:112 on a = acc / ws)
+                    p = (T)((double)rv[v] * sc.ysc[c]);
+                    if (RARE && ((m_x0 >> v) & 1u)) {
+                        p = (T)(a.x0[(int64_t)sc.qidx[j0 + v] * a.n_u + u] * iws);
+                        rv[v] = p;
                     }
-                    if (init) rv[k][v] = pushed ? (T)0 : (T)r;
-                    pv[v] = p;
                 }
-                if (m_keep) {  // slots whose P is kept (iterate / idle) are not written
+                if (init) rv[v] = pushed ? (T)0 : (T)r;
+                pv[v] = p;
+            }
+            if (m_keep) {  // slots whose P is kept (iterate / idle) are not written
+#pragma unroll
+                for (int v = 0; v < EV; v++)
+                    if (!((m_keep >> v) & 1u)) a.P[i + v] = pv[v];
+            } else {
+                VecIO<T, EV>::st(a.P + i, pv);
+            }
+            if constexpr (RARE) {
+                VecIO<T, EV>::st(a.R + i, rv);
+                if (m_init) {  // ledger reset: est := alpha r on the pushed nodes of init slots
+                    T ev[EV];
+                    VecIO<T, EV>::ld(a.EST + i, ev);
 #pragma unroll
                     for (int v = 0; v < EV; v++)
-                        if (!((m_keep >> v) & 1u)) a.P[i + v] = pv[v];
-                } else {
-                    VecIO<T, EV>::st(a.P + i, pv);
+                        if ((m_init >> v) & 1u) ev[v] = (T)(act[v] ? 0.0 + a.alpha * rr[v] : 0.0);
+                    VecIO<T, EV>::st(a.EST + i, ev);
                 }
-                if constexpr (RARE) {
-                    VecIO<T, EV>::st(a.R + i, rv[k]);
-                    if (m_init) {  // ledger reset: est := alpha r on the pushed nodes of init slots
-                        T ev[EV];
-                        VecIO<T, EV>::ld(a.EST + i, ev);
+            }
+        };
+        auto load = [&](int64_t u, T (&rv)[EV], double &iwsv, double &wsv, int32_t &degv) {
+            VecIO<T, EV>::ld(a.R + u * B + j0, rv);
+            iwsv = a.inv_ws_u[u];
+            wsv = m_fwd ? a.ws_u[u] : 0.0;
+            degv = a.deg_u[u];
+        };
+        const int64_t total = a.n_u * TPN;
+        const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+        const int64_t first = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+        if constexpr (PIPE) {  // the next node's loads in flight while this one computes
+            T rn[EV];
+            double in = 0.0, wn = 0.0;
+            int32_t dn = 0;
+            if (first < total) load(first / TPN, rn, in, wn, dn);
+            for (int64_t t = first; t < total; t += stride) {
+                T rv[EV];
 #pragma unroll
-                        for (int v = 0; v < EV; v++)
-                            if ((m_init >> v) & 1u) ev[v] = (T)(act[v] ? 0.0 + a.alpha * rr[v] : 0.0);
-                        VecIO<T, EV>::st(a.EST + i, ev);
-                    }
+                for (int v = 0; v < EV; v++) rv[v] = rn[v];
+                const double iwsv = in, wsv = wn;
+                const int32_t degv = dn;
+                if (t + stride < total) load((t + stride) / TPN, rn, in, wn, dn);
+                node(t / TPN, rv, iwsv, wsv, degv);
+            }
+        } else {
+            for (int64_t t0 = first; t0 < total; t0 += ELEM_UNR * stride) {
+                T rv[ELEM_UNR][EV];
+                double iwsk[ELEM_UNR], wsk[ELEM_UNR];
+                int32_t degk[ELEM_UNR];
+#pragma unroll
+                for (int k = 0; k < ELEM_UNR; k++) {
+                    const int64_t t = t0 + k * stride;
+                    if (t < total) load(t / TPN, rv[k], iwsk[k], wsk[k], degk[k]);
+                }
+#pragma unroll
+                for (int k = 0; k < ELEM_UNR; k++) {
+                    const int64_t t = t0 + k * stride;
+                    if (t >= total) break;
+                    node(t / TPN, rv[k], iwsk[k], wsk[k], degk[k]);
                 }
             }
         }
@@ -373,7 +392,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, MINB) k_push(ElemArgs<T> a) {
 // the exit-test reductions of the round that just ran.  For push slots it also
 // completes K1's push: the nodes over threshold (same decision, same r) have
 // their residue replaced by Y and est += alpha r.  Per element predicated.
-template <int B, typename T, int ELEM_UNR = 4, int MINB = 1>
+template <int B, typename T, int ELEM_UNR = 4, int MINB = 1, bool PIPE = false>
 __global__ void __launch_bounds__(ELEM_THREADS, MINB) k_combine(ElemArgs<T> a) {
     pdl_begin();
     if (*a.active == 0) return;
@@ -403,54 +422,76 @@ __global__ void __launch_bounds__(ELEM_THREADS, MINB) k_combine(ElemArgs<T> a) {
         sum[v] = wsum[v] = 0.0;
         any[v] = 0;
     }
+    // one node's elements (EV slots)
+    auto node = [&](int64_t u, T (&rv)[EV], const T (&yv)[EV], T (&ev)[EV], double ws, double iws) {
+        const int64_t i = u * B + j0;
+        bool wrote_e = false;
+#pragma unroll
+        for (int v = 0; v < EV; v++) {
+            const int c = v * TPN + grp;
+            const double r0 = (double)rv[v];
+            const double y = (double)yv[v];
+            const double tA = sc.thA[c] * iws;
+            const bool pushed = ((m_push >> v) & 1u) && r0 > fma(tA, sc.thC[c], sc.thDp[c]);
+            if (pushed) {
+                ev[v] = (T)((double)ev[v] + a.alpha * r0);
+                wrote_e = true;
+            }
+            if ((m_pi >> v) & 1u) a.P[i + v] = (T)(r0 * sc.ysc[c] + y);
+            const T nr = ((m_rw >> v) & 1u) ? (T)((pushed ? 0.0 : r0) + y) : rv[v];
+            rv[v] = nr;
+            const double r = (double)nr;
+            const bool st = (m_stat >> v) & 1u;
+            if (st) sum[v] += r;
+            if (st) wsum[v] = fma(ws * sc.iwsq[c], r, wsum[v]);  // w_ratio * r  (push_engine.py:220,237)
+            any[v] |= st && r > fma(tA, sc.thC[c], sc.thDa[c]);
+        }
+        if (m_rw) VecIO<T, EV>::st(a.R + i, rv);
+        if (wrote_e) VecIO<T, EV>::st(a.EST + i, ev);
+    };
+    auto load = [&](int64_t u, T (&rv)[EV], T (&yv)[EV], T (&ev)[EV], double &ws, double &iws) {
+        VecIO<T, EV>::ld(a.R + u * B + j0, rv);
+        VecIO<T, EV>::ld(a.Y + u * B + j0, yv);
+        if (m_push) VecIO<T, EV>::ld(a.EST + u * B + j0, ev);
+        ws = a.ws_u[u];
+        iws = a.inv_ws_u[u];
+    };
     if (m_stat | m_pi) {
         const int64_t total = a.n_u * TPN;
         const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-        for (int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t0 < total; t0 += ELEM_UNR * stride) {
-            T rv[ELEM_UNR][EV], yv[ELEM_UNR][EV], ev[ELEM_UNR][EV];
-            double wsk[ELEM_UNR], iwsk[ELEM_UNR];
-#pragma unroll
-            for (int k = 0; k < ELEM_UNR; k++) {
-                const int64_t t = t0 + k * stride;
-                if (t < total) {
-                    const int64_t u = t / TPN;
-                    VecIO<T, EV>::ld(a.R + u * B + j0, rv[k]);
-                    VecIO<T, EV>::ld(a.Y + u * B + j0, yv[k]);
-                    if (m_push) VecIO<T, EV>::ld(a.EST + u * B + j0, ev[k]);
-                    wsk[k] = a.ws_u[u];
-                    iwsk[k] = a.inv_ws_u[u];
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < ELEM_UNR; k++) {
-                const int64_t t = t0 + k * stride;
-                if (t >= total) break;
-                const int64_t u = t / TPN;
-                const int64_t i = u * B + j0;
-                const double ws = wsk[k], iws = iwsk[k];
-                bool wrote_e = false;
+        const int64_t first = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+        if constexpr (PIPE) {
+            // software pipeline: the next node's loads are in flight while this one computes
+            T rn[EV], yn[EV], en[EV];
+            double wn = 0.0, in = 0.0;
+            if (first < total) load(first / TPN, rn, yn, en, wn, in);
+            for (int64_t t = first; t < total; t += stride) {
+                T rv[EV], yv[EV], ev[EV];
 #pragma unroll
                 for (int v = 0; v < EV; v++) {
-                    const int c = v * TPN + grp;
-                    const double r0 = (double)rv[k][v];
-                    const double y = (double)yv[k][v];
-                    const double tA = sc.thA[c] * iws;
-                    const bool pushed = ((m_push >> v) & 1u) && r0 > fma(tA, sc.thC[c], sc.thDp[c]);
-                    if (pushed) {
-                        ev[k][v] = (T)((double)ev[k][v] + a.alpha * r0);
-                        wrote_e = true;
-                    }
-                    if ((m_pi >> v) & 1u) a.P[i + v] = (T)(r0 * sc.ysc[c] + y);
-                    const T nr = ((m_rw >> v) & 1u) ? (T)((pushed ? 0.0 : r0) + y) : rv[k][v];
-                    rv[k][v] = nr;
-                    const double r = (double)nr;
-                    const bool st = (m_stat >> v) & 1u;
-                    if (st) sum[v] += r;
-                    if (st) wsum[v] = fma(ws * sc.iwsq[c], r, wsum[v]);  // w_ratio * r  (push_engine.py:220,237)
-                    any[v] |= st && r > fma(tA, sc.thC[c], sc.thDa[c]);
+                    rv[v] = rn[v];
+                    yv[v] = yn[v];
+                    ev[v] = en[v];
                 }
-                if (m_rw) VecIO<T, EV>::st(a.R + i, rv[k]);
-                if (wrote_e) VecIO<T, EV>::st(a.EST + i, ev[k]);
+                const double ws = wn, iws = in;
+                if (t + stride < total) load((t + stride) / TPN, rn, yn, en, wn, in);
+                node(t / TPN, rv, yv, ev, ws, iws);
+            }
+        } else {
+            for (int64_t t0 = first; t0 < total; t0 += ELEM_UNR * stride) {
+                T rv[ELEM_UNR][EV], yv[ELEM_UNR][EV], ev[ELEM_UNR][EV];
+                double wsk[ELEM_UNR], iwsk[ELEM_UNR];
+#pragma unroll
+                for (int k = 0; k < ELEM_UNR; k++) {
+                    const int64_t t = t0 + k * stride;
+                    if (t < total) load(t / TPN, rv[k], yv[k], ev[k], wsk[k], iwsk[k]);
+                }
+#pragma unroll
+                for (int k = 0; k < ELEM_UNR; k++) {
+                    const int64_t t = t0 + k * stride;
+                    if (t >= total) break;
+                    node(t / TPN, rv[k], yv[k], ev[k], wsk[k], iwsk[k]);
+                }
             }
         }
     }
