@@ -400,7 +400,8 @@ struct Engine final : EngineBase {
         push_cfg = elem_cfg_from_env("BH_ELEM_PUSH");
         comb_cfg = elem_cfg_from_env("BH_ELEM_COMBINE");
         // K1a fp32: software-pipelined at 3 blocks/SM (c2: prep 5.51 -> 5.32 ms per step)
-        if (getenv("BH_ELEM_COMBINE") == nullptr && sizeof(T) == 4) comb_cfg = 10;
+        const char *comb_env = getenv("BH_ELEM_COMBINE");
+        if (comb_env == nullptr && sizeof(T) == 4) comb_cfg = 10;
         {  // one resident wave of the elementwise kernels
             int occ_p = 1, occ_c = 1;
             BH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, push_kernel(), ELEM_THREADS, 0));
