@@ -288,7 +288,38 @@ struct Engine final : EngineBase {
     PullFn sw_kernel() const {
         if constexpr (SIDE == SIDE_U) {
             if (fuse_combine) return k_pull_sw<B, T, SIDE_U, true>;
+        }
+        // tuning override BH_PULL_SW_CFG_V / _U = "S,MINB" (rows in flight per warp,
+        // blocks per SM) for the fp32 wide engines
+        if constexpr (sizeof(T) == 4 && B >= 32) {
+            if (const char *m = getenv(SIDE == SIDE_V ? "BH_PULL_SW_CFG_V" : "BH_PULL_SW_CFG_U")) {
+                const std::string v(m);
+                if (v == "8,4") return k_pull_sw<B, T, SIDE, false, 8, 4>;
+                if (v == "6,4") return k_pull_sw<B, T, SIDE, false, 6, 4>;
+                if (v == "6,3") return k_pull_sw<B, T, SIDE, false, 6, 3>;
+                if (v == "12,2") return k_pull_sw<B, T, SIDE, false, 12, 2>;
+                if (v == "10,3") return k_pull_sw<B, T, SIDE, false, 10, 3>;
+                if (v == "8,3") return k_pull_sw<B, T, SIDE, false, 8, 3>;
+                if (v == "4,5") return k_pull_sw<B, T, SIDE, false, 4, 5>;
+                if (v == "6,5") return k_pull_sw<B, T, SIDE, false, 6, 5>;
+                if (v == "5,5") return k_pull_sw<B, T, SIDE, false, 5, 5>;
+                if (v == "7,4") return k_pull_sw<B, T, SIDE, false, 7, 4>;
+                if (v == "4,6") return k_pull_sw<B, T, SIDE, false, 4, 6>;
+                if (v == "4,4") return k_pull_sw<B, T, SIDE, false, 4, 4>;
+                if (v == "5,4") return k_pull_sw<B, T, SIDE, false, 5, 4>;
+                if (v == "5,3") return k_pull_sw<B, T, SIDE, false, 5, 3>;
+            }
+        }
+        if constexpr (SIDE == SIDE_U) {
             if (u_minb4) return k_pull_sw<B, T, SIDE_U, false, SwPipe<B, T>::S, 4>;
+            // 16-byte lanes (128 fp32 slots): 6 rows in flight at 3 blocks/SM (c5-style
+            // 128-slot run: 4613 -> 4775 queries/s against 8 rows at 2 blocks/SM)
+            if constexpr (SwPipe<B, T>::LANE_BYTES == 16 && sizeof(T) == 4)
+                return k_pull_sw<B, T, SIDE_U, false, 6, 3>;
+        } else if constexpr (SwPipe<B, T>::LANE_BYTES == 8) {
+            // V pull, 8-byte lanes: 7 rows in flight at 4 blocks/SM (c2: V pull
+            // 9.0 -> 8.2 ms per step against 8 rows at 3 blocks/SM)
+            return k_pull_sw<B, T, SIDE_V, false, 7, 4>;
         }
         return k_pull_sw<B, T, SIDE>;
     }
