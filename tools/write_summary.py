@@ -16,8 +16,8 @@ tab = subprocess.run([sys.executable, "tools/ncu_extract.py", rep], capture_outp
 steps = d["steps"]
 print(f"""# Round 1 profiles (B200, sm_100a) -- config c2, fp32 storage / fp64 accumulation, B = 64 slots
 
-Build: `k_pull_sw` pulls (S = 8 rows in flight, shared-memory windows, 3 blocks/SM), predicated
-elementwise K1/K1a (one node per thread, 4 blocks/SM; r_A := 0 and est += alpha r done in K1a),
+Build: `k_pull_sw` pulls (shared-memory windows; V 7 rows in flight at 4 blocks/SM, U 8 rows at 4 blocks/SM), predicated
+elementwise K1/K1a (one node per thread; K1 4 blocks/SM, K1a software-pipelined at 3; r_A := 0 and est += alpha r in K1a),
 K4 with one load round trip, one CUDA graph per batch (WHILE node, PDL launches; K5 under an IF node on a
 branch parallel to the next round's K1..K1a).
 Commands: `tools/measure_round.sh` (bench line, reference arm, launch list, ncu full set).
