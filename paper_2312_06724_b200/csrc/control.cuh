@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
     if (!a.first) {
         // partial rows are stored slot-major: [slot][row]; the loads of all six
         // row sets are issued together (one memory round trip for the usual sizes)
-        constexpr int U4 = 4, U16 = 16;
+        constexpr int U4 = 4, UNP = 20;  // UNP x 256 covers the V pull's per-warp n_p rows (4736 at c2)
         const int64_t *pc = a.part.cnt + (int64_t)s * a.part.rows_k1;
         const int64_t *pn = a.part.np_u + (int64_t)s * a.part.rows_k1;
         const double *pl = a.part.lmass + (int64_t)s * a.part.rows_k1;
@@ -138,9 +138,9 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
         const double *ps = a.part.sum + (int64_t)s * a.part.rows_k3;
         const double *pw = a.part.wsum + (int64_t)s * a.part.rows_k3;
         const int n1 = a.part.rows_k1, n2 = a.part.rows_k2, n3 = a.part.rows_k3;
-        for (int it = 0; it * CONTROL_THREADS * U4 < n1 || it * CONTROL_THREADS * U16 < n2 ||
+        for (int it = 0; it * CONTROL_THREADS * U4 < n1 || it * CONTROL_THREADS * UNP < n2 ||
                          it * CONTROL_THREADS * U4 < n3; it++) {
-            int64_t c4[U4], n4[U4], n16[U16];
+            int64_t c4[U4], n4[U4], nnp[UNP];
             double l4[U4], s4[U4], w4[U4];
             int32_t a4[U4];
 #pragma unroll
@@ -155,9 +155,9 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
                 w4[j] = ok3 ? __ldcg(pw + r) : 0.0;
             }
 #pragma unroll
-            for (int j = 0; j < U16; j++) {
-                const int r = (it * U16 + j) * CONTROL_THREADS + tid;
-                n16[j] = r < n2 ? __ldcg(pv + r) : 0;
+            for (int j = 0; j < UNP; j++) {
+                const int r = (it * UNP + j) * CONTROL_THREADS + tid;
+                nnp[j] = r < n2 ? __ldcg(pv + r) : 0;
             }
 #pragma unroll
             for (int j = 0; j < U4; j++) {
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
                 wsum += w4[j];
             }
 #pragma unroll
-            for (int j = 0; j < U16; j++) np += n16[j];
+            for (int j = 0; j < UNP; j++) np += nnp[j];
         }
     }
     if (active == 0 && !a.first) {

@@ -290,8 +290,8 @@ struct Engine final : EngineBase {
             if (fuse_combine) return k_pull_sw<B, T, SIDE_U, true>;
         }
         // tuning override BH_PULL_SW_CFG_V / _U = "S,MINB" (rows in flight per warp,
-        // blocks per SM) for the fp32 wide engines
-        if constexpr (sizeof(T) == 4 && B >= 32) {
+        // blocks per SM) for the 64-slot engines and fp32 128-slot engines
+        if constexpr (B == 64 || (sizeof(T) == 4 && B >= 32)) {
             if (const char *m = getenv(SIDE == SIDE_V ? "BH_PULL_SW_CFG_V" : "BH_PULL_SW_CFG_U")) {
                 const std::string v(m);
                 if (v == "8,4") return k_pull_sw<B, T, SIDE, false, 8, 4>;
