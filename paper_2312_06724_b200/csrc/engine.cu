@@ -227,10 +227,10 @@ struct Engine final : EngineBase {
     static constexpr int64_t HALF_MIN_AVG_DEG = 16;
 
     // Full-warp workers: (col, val) windows in shared memory (k_pull_sw) or in
-    // lane registers (k_pull).  Measured at c2 on B200: fp32 is fastest with
-    // k_pull_sw on both sides; fp64 (16 B per lane, S = 8) with k_pull and
-    // half-warp workers on the long-row side.
-    bool pull_sw = sizeof(T) == 4;
+    // lane registers (k_pull).  Measured at c2 on B200: k_pull_sw on both sides for
+    // fp32 and for fp64 at 64 slots (sw_kernel picks rows in flight / blocks per SM);
+    // the other fp64 widths keep k_pull with half-warp workers on the long-row side.
+    bool pull_sw = sizeof(T) == 4 || B == 64;
     bool pull_tma = false;             // TMA gather4 pull (k_pull_tma), BH_PULL_TMA=1
     CUtensorMap tmap_p{}, tmap_xv{};   // operands of the V pull (P) and the U pull (XV)
     // K1a fused into the U pull's row emit (k_pull_sw<..., SIDE_U, true>): no Y
@@ -309,6 +309,11 @@ struct Engine final : EngineBase {
                 if (v == "5,4") return k_pull_sw<B, T, SIDE, false, 5, 4>;
                 if (v == "5,3") return k_pull_sw<B, T, SIDE, false, 5, 3>;
             }
+        }
+        if constexpr (sizeof(T) == 8 && B == 64) {
+            // fp64, 16-byte lanes: 6 rows in flight at 3 blocks/SM on both sides (c2 fp64:
+            // 1808 -> 2027 queries/s against lane-register windows with half-warp U workers)
+            return k_pull_sw<B, T, SIDE, false, 6, 3>;
         }
         if constexpr (SIDE == SIDE_U) {
             if (u_minb4) return k_pull_sw<B, T, SIDE_U, false, SwPipe<B, T>::S, 4>;
