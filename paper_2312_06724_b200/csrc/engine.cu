@@ -308,6 +308,12 @@ struct Engine final : EngineBase {
                 if (v == "4,4") return k_pull_sw<B, T, SIDE, false, 4, 4>;
                 if (v == "5,4") return k_pull_sw<B, T, SIDE, false, 5, 4>;
                 if (v == "5,3") return k_pull_sw<B, T, SIDE, false, 5, 3>;
+                if (v == "10,2") return k_pull_sw<B, T, SIDE, false, 10, 2>;
+                if (v == "14,2") return k_pull_sw<B, T, SIDE, false, 14, 2>;
+                if (v == "16,2") return k_pull_sw<B, T, SIDE, false, 16, 2>;
+                if (v == "11,2") return k_pull_sw<B, T, SIDE, false, 11, 2>;
+                if (v == "6,2") return k_pull_sw<B, T, SIDE, false, 6, 2>;
+                if (v == "4,3") return k_pull_sw<B, T, SIDE, false, 4, 3>;
             }
         }
         if constexpr (sizeof(T) == 8 && B == 64) {
