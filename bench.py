@@ -180,6 +180,26 @@ def ncu_vpull_traffic():
     return None
 
 
+def c3_hbm_reference(peak):
+    """DRAM throughput of the round kernels in the HBM-resident regime (config c3,
+    operands larger than L2) from the committed ncu capture
+    (profiles/r01_ncu_c3_round_kernels.json), as fractions of the HBM peak."""
+    p = REPO / "profiles" / "r01_ncu_c3_round_kernels.json"
+    if not p.exists() or not peak:
+        return None
+    try:
+        ks = json.loads(p.read_text())["kernels"]
+    except Exception:
+        return None
+    out = {}
+    for k, v in ks.items():
+        gbs = (v["dram_read_MB"] + v["dram_write_MB"]) / 1e3 / (v["time_us"] / 1e6)
+        out[k] = {"dram_gbs": round(gbs, 1), "frac": round(gbs / peak, 3)}
+    return {"config": "c3 (|E|=1e8, 128 slots): operands exceed L2, gathers served by HBM",
+            "source": "profiles/r01_ncu_c3_round_kernels.json (ncu --set full, one launch each)",
+            "kernels": out}
+
+
 def peak_hbm():
     p = REPO / "MEASURED_PEAKS.json"
     if p.exists():
@@ -481,6 +501,7 @@ def run_ours(args):
                           "enqueued behind a device start gate, so e0..e1 is device time only)",
                 "breakdown_ms_per_step": {k2: prof[k2] / args.steps for k2 in ("ms_prep", "ms_vpull", "ms_upull", "ms_control")},
                 "peak_source": peak_src,
+                "hbm_regime_reference": c3_hbm_reference(peak),
                 "timed_step_ms": [round(x, 3) for x in prof.get("timed_step_ms", [])],
                 "profiled_step_ms": [round(x, 3) for x in prof.get("step_ms", [])],
                 "timed_step_rounds": prof.get("timed_step_rounds"),
