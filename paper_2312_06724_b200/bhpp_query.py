@@ -197,6 +197,16 @@ def bhpp_query(g, meta: IndexMeta, query_u, epsilon: float, round_hook=None, dty
     )
 
 
+def _source_list(sources) -> list:
+    """The batch's sources one by one, each keeping its own type (a label or an
+    index); np.atleast_1d on a mixed list would turn every index into a string."""
+    if isinstance(sources, (str, bytes)) or np.isscalar(sources):
+        return [sources]
+    if isinstance(sources, np.ndarray):
+        return sources.reshape(-1).tolist()
+    return list(sources)
+
+
 def bhpp_query_batch(g, meta: IndexMeta, sources, epsilon: float, k: int | None = 50,
                      exclude_query: bool = False, dtype: str = "fp32", return_scores: bool = False,
                      slots: int | None = None, tie_skip=None, stream=None, device: int | None = None) -> BatchResult:
@@ -209,7 +219,7 @@ def bhpp_query_batch(g, meta: IndexMeta, sources, epsilon: float, k: int | None 
     fp32 with fp64 row accumulation and fp64 control; "fp64" is all fp64.
     """
     eps_b, eps_f = _split(meta, g, epsilon)
-    src = np.array([g.u_id(s) if isinstance(s, str) else int(s) for s in np.atleast_1d(sources)], dtype=np.int32)
+    src = np.array([g.u_id(s) if isinstance(s, str) else int(s) for s in _source_list(sources)], dtype=np.int32)
     if src.size and (src.min() < 0 or src.max() >= g.u_count):
         raise ValueError("node index out of range")
     kk = 0 if not k else int(k)

@@ -184,3 +184,31 @@ def test_single_process_multi_device_sharding_matches_one_call():
     np.testing.assert_array_equal(multi.topk_score, one.topk_score)
     np.testing.assert_array_equal(multi.scores, one.scores)
     assert multi.traces.tobytes() == one.traces.tobytes()
+
+
+def test_batch_edge_cases_duplicates_empty_labels_and_limits():
+    """Duplicate sources give identical rows; an empty batch returns empty
+    arrays; labels and indices mix; k is clipped to |U|; bad sources and eps
+    raise ValueError / DataError like the reference's argument checks."""
+    g = config_graph("c1")
+    meta = bh.build_index_meta(g, 0.15)
+    src = [5, 17, 5, 5, 17]
+    r = bh.bhpp_query_batch(g, meta, src, 1e-6, k=10, dtype="fp64", return_scores=True)
+    np.testing.assert_array_equal(r.scores[0], r.scores[2])
+    np.testing.assert_array_equal(r.scores[0], r.scores[3])
+    np.testing.assert_array_equal(r.scores[1], r.scores[4])
+    np.testing.assert_array_equal(r.topk_index[0], r.topk_index[3])
+    assert r.traces.tobytes()[: r.traces.itemsize] == r.traces[2:3].tobytes()
+    lab = bh.bhpp_query_batch(g, meta, [g.u_labels[5], 17], 1e-6, k=10, dtype="fp64", return_scores=True)
+    np.testing.assert_allclose(lab.scores[0], r.scores[0], atol=1e-15, rtol=0)  # other slot width
+    np.testing.assert_allclose(lab.scores[1], r.scores[1], atol=1e-15, rtol=0)
+    e = bh.bhpp_query_batch(g, meta, np.array([], dtype=np.int64), 1e-6, k=10, dtype="fp32")
+    assert e.topk_index.shape[0] == 0 and e.traces.shape[0] == 0
+    big = bh.bhpp_query_batch(g, meta, [0], 1e-6, k=2000, dtype="fp32")  # k clipped to |U| like topk
+    assert big.k == g.u_count and big.topk_index.shape == (1, g.u_count)
+    with pytest.raises(ValueError):
+        bh.bhpp_query_batch(g, meta, [g.u_count], 1e-6, k=10, dtype="fp32")
+    with pytest.raises(ValueError):
+        bh.bhpp_query_batch(g, meta, [0], -1.0, k=10, dtype="fp32")
+    with pytest.raises(bh.DataError):
+        bh.bhpp_query_batch(g, meta, ["no-such-label"], 1e-6, k=10, dtype="fp32")
