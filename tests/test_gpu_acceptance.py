@@ -16,6 +16,7 @@ import numpy as np
 import pytest
 
 import paper_2312_06724_b200 as bh
+from oracle import cpu_oracle as O
 from paper_2312_06724_b200.rng import substream
 
 pytestmark = pytest.mark.gpu
@@ -88,3 +89,45 @@ def test_crit10_gamma_monotone_in_eps_b():
             gam.append(np.array([res.trace_dicts(j)["forward"]["gamma"] for j in range(len(srcs))]))
         for a, b in zip(gam, gam[1:]):
             assert np.all(b <= a * (1 + 1e-12) + 1e-15), (i, a, b)
+
+
+def _graph(nu, nv, edges, weights=None):
+    eu = [a for a, _ in edges]
+    ev = [b for _, b in edges]
+    w = weights if weights is not None else [1.0] * len(edges)
+    return bh.BipartiteGraph([f"u{i}" for i in range(nu)], [f"v{i}" for i in range(nv)], eu, ev, w)
+
+
+@pytest.mark.parametrize("name", ["single_u", "single_v", "star_u", "star_v", "extreme_weights", "path"])
+def test_degenerate_graphs_one_sided(name):
+    """Shapes at the edges of the domain: one U node, one V node, stars, weight
+    ratios of 1e12, a long path; every eps from loose (0.5) to 1e-9."""
+    if name == "single_u":
+        g = _graph(1, 3, [(0, 0), (0, 1), (0, 2)], [1.0, 2.0, 3.0])
+    elif name == "single_v":
+        g = _graph(5, 1, [(i, 0) for i in range(5)], [1.0, 2.0, 3.0, 4.0, 5.0])
+    elif name == "star_u":  # one U hub on every V, every V also on one leaf U
+        g = _graph(9, 8, [(0, j) for j in range(8)] + [(1 + j, j) for j in range(8)])
+    elif name == "star_v":
+        g = _graph(8, 9, [(i, 0) for i in range(8)] + [(i, 1 + i) for i in range(8)])
+    elif name == "extreme_weights":
+        g = _graph(4, 3, [(0, 0), (1, 0), (1, 1), (2, 1), (2, 2), (3, 2)], [1e-6, 1e6, 1.0, 1e-6, 1e6, 1.0])
+    else:  # a path u0 - v0 - u1 - v1 - ... - u7
+        g = _graph(8, 7, [(i, i) for i in range(7)] + [(i + 1, i) for i in range(7)])
+    Pi = dense_pi(g)
+    meta = bh.build_index_meta(g, ALPHA)
+    srcs = np.arange(g.u_count)
+    for eps in (0.5, 1e-3, 1e-6, 1e-9):
+        for dtype, tol in (("fp64", 1e-10), ("fp32", 1e-5)):
+            res = bh.bhpp_query_batch(g, meta, srcs, eps, k=3, dtype=dtype, return_scores=True)
+            for j, q in enumerate(srcs):
+                diff = (Pi[q, :] + Pi[:, q]) - res.scores[j]
+                assert diff.min() >= -tol and diff.max() <= eps + tol, (name, eps, dtype, int(q), diff)
+        # the single-query path against the oracle (the reference restated bit for bit)
+        eps_b = float(meta.eps_split_policy(eps))
+        og = O.OracleGraph(g)
+        for q in range(min(g.u_count, 3)):
+            ref_scores, ref_tr = og.bhpp_query(q, ALPHA, meta.lam, eps_b, eps - eps_b)
+            one = bh.bhpp_query(g, meta, q, eps, tie_skip=O.tie_skip_for(ref_tr["forward"]))
+            np.testing.assert_allclose(one.scores, ref_scores, atol=1e-12, rtol=0, err_msg=f"{name} {eps} {q}")
+            assert one.phase_trace["backward"] == ref_tr["backward"], (name, eps, q)
