@@ -255,3 +255,14 @@ def test_similarity_rows_rejects_methods_off_the_bhpp_path():
     for m in ("jaccard", "naive-ppr", "nope"):
         with pytest.raises(bh.DataError):
             bh.similarity_rows(m, g)
+
+
+def test_batch_source_list_keeps_each_elements_type():
+    from paper_2312_06724_b200.bhpp_query import _source_list
+
+    assert _source_list(5) == [5]
+    assert _source_list("u3") == ["u3"]
+    assert _source_list(["u3", 17, np.int64(4)]) == ["u3", 17, np.int64(4)]
+    assert _source_list(np.array([[1, 2], [3, 4]])) == [1, 2, 3, 4]
+    assert _source_list(np.array(["a", "b"])) == ["a", "b"]
+    assert _source_list((x for x in (1, 2))) == [1, 2]
