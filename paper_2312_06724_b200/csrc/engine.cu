@@ -210,174 +210,48 @@ struct Engine final : EngineBase {
     int32_t *chunk_done = nullptr;
     std::vector<cudaEvent_t> evpool;
     SidePlan plan_v, plan_u;
-    uint64_t *dbg_v = nullptr, *dbg_u = nullptr;  // BH_DEBUG_WARP_TIMING
     // one batch = one CUDA graph: a WHILE node around one round, condition set by K4
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t graph_exec = nullptr;
     cudaStream_t cap_stream = nullptr;
     std::vector<unsigned char> graph_key;
-    size_t pull_smem = 0;
     int fin_chunk = SEL_ITEMS * TOPK_THREADS, n_chunks = 1;  // one register-cached select per chunk
     int grid_elem = 1, grid_comb = 1, grid_k5 = 1;  // K1 / K1a grids (one resident wave each)
 
-    // Pull mapping per side: half-warp workers (two operand rows per warp
-    // instruction) when rows are long enough that the per-row emit is
-    // amortised, full-warp workers (cheapest emit) for short rows.
-    bool half_v = false, half_u = false;
-    static constexpr int64_t HALF_MIN_AVG_DEG = 16;
-
-    // Full-warp workers: (col, val) windows in shared memory (k_pull_sw) or in
-    // lane registers (k_pull).  Measured at c2 on B200: k_pull_sw on both sides for
-    // fp32 and for fp64 at 64 slots (sw_kernel picks rows in flight / blocks per SM);
-    // the other fp64 widths keep k_pull with half-warp workers on the long-row side.
-    bool pull_sw = sizeof(T) == 4 || B == 64;
-    bool pull_tma = false;             // TMA gather4 pull (k_pull_tma), BH_PULL_TMA=1
-    CUtensorMap tmap_p{}, tmap_xv{};   // operands of the V pull (P) and the U pull (XV)
-    // K1a fused into the U pull's row emit (k_pull_sw<..., SIDE_U, true>): no Y
-    // round trip, no combine launch (BH_FUSE_COMBINE=1).
-    bool fuse_combine = false;
-    // U pull at 4 blocks/SM where the V pull runs 3 (8-byte lanes): measured at c2,
-    // U 8.2 -> 7.9 ms per step (longer rows, fewer emits per edge than the V side)
-    bool u_minb4 = SwPipe<B, T>::MINB == 3;
-
-    // elementwise K1 / K1a: 2 nodes in flight per thread at 3 blocks/SM (fp32) measured
-    // fastest at c2 (prep 7.35 -> 6.68 ms per step against 4 nodes at 2 blocks/SM)
+    // Elementwise K1 / K1a geometry (nodes in flight per thread, blocks per SM),
+    // measured at c2 on B200 (profiles/r01_pull_variants.md): fp32 K1 one node
+    // per thread at 4 blocks/SM, K1a software-pipelined at 3 blocks/SM; fp64 two
+    // nodes per thread at 2 blocks/SM.
     using ElemFn = void (*)(ElemArgs<T>);
-    // K1 / K1a geometry (nodes in flight per thread, blocks per SM): one node at
-    // 4 blocks/SM measured fastest for fp32 at c2 (prep 6.5 -> 5.6 ms per step
-    // against 2 nodes at 3 blocks/SM), K1a software-pipelined at 3 blocks/SM;
-    // tuning override BH_ELEM_PUSH / BH_ELEM_COMBINE = "UNR,MINB" or "pUNR,MINB"
-    // (pipelined) for the wide engines.
-    int push_cfg = 0, comb_cfg = 0;
-    static constexpr const char *ELEM_CFGS[] = {"", "2,2", "4,2", "1,4", "1,3", "1,5", "1,6", "2,3", "2,4",
-                                                "p1,4", "p1,3"};
-    template <template <int, typename, int, int> class K>
-    static ElemFn elem_variant(int cfg) {
-        if constexpr (B < 32) cfg = 0;  // tuning variants only for the wide engines
-        switch (cfg) {
-            case 1: return K<B, T, 2, 2>::fn;
-            case 2: return K<B, T, 4, 2>::fn;
-            case 3: return K<B, T, 1, 4>::fn;
-            case 4: return K<B, T, 1, 3>::fn;
-            case 5: return K<B, T, 1, 5>::fn;
-            case 6: return K<B, T, 1, 6>::fn;
-            case 7: return K<B, T, 2, 3>::fn;
-            case 8: return K<B, T, 2, 4>::fn;
-            case 9: return K<B, T, -1, 4>::fn;   // "p": software-pipelined, one node per thread
-            case 10: return K<B, T, -1, 3>::fn;
-            default: return sizeof(T) == 4 ? K<B, T, 1, 4>::fn : K<B, T, 2, 2>::fn;
-        }
+    static ElemFn push_kernel() {
+        if constexpr (sizeof(T) == 4 && B >= 32) return k_push<B, T, 1, 4>;
+        else return k_push<B, T, 2, 2>;
     }
-    // U_ = -1: software-pipelined variant (one node per thread)
-    template <int B_, typename T_, int U_, int M_>
-    struct PushK { static constexpr ElemFn fn = k_push<B_, T_, (U_ < 0 ? 1 : U_), M_, (U_ < 0)>; };
-    template <int B_, typename T_, int U_, int M_>
-    struct CombK { static constexpr ElemFn fn = k_combine<B_, T_, (U_ < 0 ? 1 : U_), M_, (U_ < 0)>; };
-    static int elem_cfg_from_env(const char *name) {
-        const char *m = getenv(name);
-        if (!m) return 0;
-        for (int i = 1; i < (int)(sizeof(ELEM_CFGS) / sizeof(ELEM_CFGS[0])); i++)
-            if (std::string(m) == ELEM_CFGS[i]) return i;
-        return 0;
+    static ElemFn combine_kernel() {
+        if constexpr (sizeof(T) == 4 && B >= 32) return k_combine<B, T, 1, 3, true>;
+        else return k_combine<B, T, 2, 2>;
     }
-    ElemFn push_kernel() const { return elem_variant<PushK>(push_cfg); }
-    ElemFn combine_kernel() const { return elem_variant<CombK>(comb_cfg); }
 
+    // Pull geometry per side and lane width (rows in flight per warp, 256-thread
+    // blocks per SM), measured at c2 / c5 on B200 (profiles/r01_pull_variants.md):
+    //   8-byte lanes (64 fp32 slots): V 7 rows at 4 blocks/SM, U 8 rows at 4
+    //   16-byte lanes: fp32 (128 slots) V 8 at 2, U 6 at 3; fp64 (64 slots) 6 at 3 both
+    //   otherwise SwPipe's defaults (U side at 4 blocks/SM when the default is 3)
     using PullFn = void (*)(PullArgs<T>);
     template <int SIDE>
-    PullFn sw_kernel() const {
-        if constexpr (SIDE == SIDE_U) {
-            if (fuse_combine) return k_pull_sw<B, T, SIDE_U, true>;
-        }
-        // tuning override BH_PULL_SW_CFG_V / _U = "S,MINB" (rows in flight per warp,
-        // blocks per SM) for the 64-slot engines and fp32 128-slot engines
-        if constexpr (B == 64 || (sizeof(T) == 4 && B >= 32)) {
-            if (const char *m = getenv(SIDE == SIDE_V ? "BH_PULL_SW_CFG_V" : "BH_PULL_SW_CFG_U")) {
-                const std::string v(m);
-                if (v == "8,4") return k_pull_sw<B, T, SIDE, false, 8, 4>;
-                if (v == "6,4") return k_pull_sw<B, T, SIDE, false, 6, 4>;
-                if (v == "6,3") return k_pull_sw<B, T, SIDE, false, 6, 3>;
-                if (v == "12,2") return k_pull_sw<B, T, SIDE, false, 12, 2>;
-                if (v == "10,3") return k_pull_sw<B, T, SIDE, false, 10, 3>;
-                if (v == "8,3") return k_pull_sw<B, T, SIDE, false, 8, 3>;
-                if (v == "4,5") return k_pull_sw<B, T, SIDE, false, 4, 5>;
-                if (v == "6,5") return k_pull_sw<B, T, SIDE, false, 6, 5>;
-                if (v == "5,5") return k_pull_sw<B, T, SIDE, false, 5, 5>;
-                if (v == "7,4") return k_pull_sw<B, T, SIDE, false, 7, 4>;
-                if (v == "4,6") return k_pull_sw<B, T, SIDE, false, 4, 6>;
-                if (v == "4,4") return k_pull_sw<B, T, SIDE, false, 4, 4>;
-                if (v == "5,4") return k_pull_sw<B, T, SIDE, false, 5, 4>;
-                if (v == "5,3") return k_pull_sw<B, T, SIDE, false, 5, 3>;
-                if (v == "10,2") return k_pull_sw<B, T, SIDE, false, 10, 2>;
-                if (v == "14,2") return k_pull_sw<B, T, SIDE, false, 14, 2>;
-                if (v == "16,2") return k_pull_sw<B, T, SIDE, false, 16, 2>;
-                if (v == "11,2") return k_pull_sw<B, T, SIDE, false, 11, 2>;
-                if (v == "6,2") return k_pull_sw<B, T, SIDE, false, 6, 2>;
-                if (v == "4,3") return k_pull_sw<B, T, SIDE, false, 4, 3>;
-            }
-        }
-        if constexpr (sizeof(T) == 8 && B == 64) {
-            // fp64, 16-byte lanes: 6 rows in flight at 3 blocks/SM on both sides (c2 fp64:
-            // 1808 -> 2027 queries/s against lane-register windows with half-warp U workers)
-            return k_pull_sw<B, T, SIDE, false, 6, 3>;
-        }
-        if constexpr (SIDE == SIDE_U) {
-            if (u_minb4) return k_pull_sw<B, T, SIDE_U, false, SwPipe<B, T>::S, 4>;
-            // 16-byte lanes (128 fp32 slots): 6 rows in flight at 3 blocks/SM (c5-style
-            // 128-slot run: 4613 -> 4775 queries/s against 8 rows at 2 blocks/SM)
-            if constexpr (SwPipe<B, T>::LANE_BYTES == 16 && sizeof(T) == 4)
-                return k_pull_sw<B, T, SIDE_U, false, 6, 3>;
-        } else if constexpr (SwPipe<B, T>::LANE_BYTES == 8) {
-            // V pull, 8-byte lanes: 7 rows in flight at 4 blocks/SM (c2: V pull
-            // 9.0 -> 8.2 ms per step against 8 rows at 3 blocks/SM)
-            return k_pull_sw<B, T, SIDE_V, false, 7, 4>;
-        }
-        return k_pull_sw<B, T, SIDE>;
-    }
-
-    // X as a [rows][B] tensor for tile::gather4 (box {B, 1}).
-    static void encode_rows_map(CUtensorMap *m, const T *base, int64_t rows) {
-        using EncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
-                                      const cuuint64_t *, const cuuint32_t *, const cuuint32_t *,
-                                      CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
-                                      CUtensorMapFloatOOBfill);
-        static EncodeFn encode = nullptr;
-        if (!encode) {
-            void *fn = nullptr;
-            cudaDriverEntryPointQueryResult q;
-            BH_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
-            if (!fn || q != cudaDriverEntryPointSuccess) throw CudaError("cuTensorMapEncodeTiled unavailable");
-            encode = (EncodeFn)fn;
-        }
-        const cuuint64_t dims[2] = {(cuuint64_t)B, (cuuint64_t)rows};
-        const cuuint64_t strides[1] = {(cuuint64_t)B * sizeof(T)};
-        const cuuint32_t box[2] = {(cuuint32_t)B, 1};
-        const cuuint32_t estr[2] = {1, 1};
-        const CUresult r = encode(m, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                                  2, (void *)base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
-    }
-
-    void pull_kernel(int side, void **fn) const {
-        if constexpr (WIDE) {
-            if (pull_tma) {
-                *fn = side == SIDE_V ? (void *)k_pull_tma<B, T, SIDE_V> : (void *)k_pull_tma<B, T, SIDE_U>;
-                return;
-            }
-
-            const bool half = side == SIDE_V ? half_v : half_u;
-            if (side == SIDE_V)
-                *fn = half ? (pull_sw ? (void *)k_pull_swh<B, T, SIDE_V> : (void *)k_pull_half<B, T, SIDE_V>)
-                           : (pull_sw ? (void *)sw_kernel<SIDE_V>() : (void *)k_pull<B, T, SIDE_V>);
-            else
-                *fn = half ? (pull_sw ? (void *)k_pull_swh<B, T, SIDE_U> : (void *)k_pull_half<B, T, SIDE_U>)
-                           : (pull_sw ? (void *)sw_kernel<SIDE_U>() : (void *)k_pull<B, T, SIDE_U>);
+    static PullFn sw_kernel() {
+        if constexpr (!WIDE) {
+            return k_pull_small<B, T, SIDE>;
         } else {
-            *fn = side == SIDE_V ? (void *)k_pull_small<B, T, SIDE_V> : (void *)k_pull_small<B, T, SIDE_U>;
+            constexpr int LB = SwPipe<B, T>::LANE_BYTES;
+            if constexpr (sizeof(T) == 8 && B == 64) return k_pull_sw<B, T, SIDE, 6, 3>;
+            if constexpr (SIDE == SIDE_V && LB == 8) return k_pull_sw<B, T, SIDE_V, 7, 4>;
+            if constexpr (SIDE == SIDE_U && LB == 16 && sizeof(T) == 4) return k_pull_sw<B, T, SIDE_U, 6, 3>;
+            if constexpr (SIDE == SIDE_U && SwPipe<B, T>::MINB == 3) return k_pull_sw<B, T, SIDE_U, SwPipe<B, T>::S, 4>;
+            return k_pull_sw<B, T, SIDE>;
         }
     }
+    static PullFn pull_kernel(int side) { return side == SIDE_V ? sw_kernel<SIDE_V>() : sw_kernel<SIDE_U>(); }
 
     explicit Engine(bh_graph *graph) : g(graph) {
         this->nslots = B;
@@ -400,34 +274,10 @@ struct Engine final : EngineBase {
         BH_CUDA(cudaMemset(ctl, 0, sizeof(Control)));
         int sms = 148;
         BH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
-        pull_smem = 0;
-        half_v = WIDE && !pull_sw && g->n_e >= HALF_MIN_AVG_DEG * g->n_v;
-        half_u = WIDE && !pull_sw && g->n_e >= HALF_MIN_AVG_DEG * g->n_u;
-        if (const char *m = getenv("BH_PULL_HALF")) {  // tuning override: 0 none, 1 U side, 2 V side, 3 both
-            const int h = atoi(m);
-            half_u = WIDE && (h & 1);
-            half_v = WIDE && (h & 2);
-        }
-        if (const char *m = getenv("BH_PULL_SW")) pull_sw = atoi(m) != 0;
-        if (const char *m = getenv("BH_PULL_TMA")) pull_tma = WIDE && atoi(m) != 0;
-        if (const char *m = getenv("BH_U_MINB4")) u_minb4 = atoi(m) != 0;
-        // opt-in: measured slower at c2 (U pull 8.1 -> 19.1 ms/step, K1a 3.1 ms saved):
-        // the per-row combine exposes the r_u row latency inside the gather loop
-        if (const char *m = getenv("BH_FUSE_COMBINE"))
-            fuse_combine = WIDE && pull_sw && !pull_tma && !half_u && atoi(m) != 0;
-        if (pull_tma) {
-            half_u = half_v = false;
-            encode_rows_map(&tmap_p, P, nu);
-            encode_rows_map(&tmap_xv, XV, nv);
-            pull_smem = TmaPipe<B, T>::BLOCK_BYTES;
-        }
         for (int side = 0; side < 2; side++) {
-            void *fn;
-            pull_kernel(side, &fn);
-            if (pull_smem > 48 * 1024)
-                BH_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pull_smem));
+            PullFn fn = pull_kernel(side);
             int occ = 1;
-            BH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, PULL_THREADS, pull_smem));
+            BH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, PULL_THREADS, 0));
             occ = std::max(1, occ);
             const Side &sd = side == SIDE_V ? g->V : g->U;
             SidePlan &pl = side == SIDE_V ? plan_v : plan_u;
@@ -436,27 +286,20 @@ struct Engine final : EngineBase {
             const int64_t want = (g->n_e + 2 * sd.n_rows) / 64 / PULL_WARPS + 1;
             grid = std::max<int64_t>(1, std::min(grid, want));
             pl.grid = (int)grid;
-            const bool half = side == SIDE_V ? half_v : half_u;
-            build_plan(sd, g->n_e, (int)grid * PULL_WARPS * (half ? 2 : 1), pl);
+            build_plan(sd, g->n_e, (int)grid * PULL_WARPS, pl);
         }
-        push_cfg = elem_cfg_from_env("BH_ELEM_PUSH");
-        comb_cfg = elem_cfg_from_env("BH_ELEM_COMBINE");
-        // K1a fp32: software-pipelined at 3 blocks/SM (c2: prep 5.51 -> 5.32 ms per step)
-        const char *comb_env = getenv("BH_ELEM_COMBINE");
-        if (comb_env == nullptr && sizeof(T) == 4) comb_cfg = 10;
         {  // one resident wave of the elementwise kernels
             int occ_p = 1, occ_c = 1;
             BH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, push_kernel(), ELEM_THREADS, 0));
             BH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, combine_kernel(), ELEM_THREADS, 0));
-            if (const char *m = getenv("BH_ELEM_BLOCKS_PER_SM")) occ_p = occ_c = atoi(m);
             grid_elem = grid1d(nu * (B / ElemGeo<B>::EV), ELEM_THREADS, std::max(1, occ_p) * sms);
             grid_comb = grid1d(nu * (B / ElemGeo<B>::EV), ELEM_THREADS, std::max(1, occ_c) * sms);
         }
         n_chunks = (int)((nu + fin_chunk - 1) / fin_chunk);
         grid_k5 = (int)std::min<int64_t>((int64_t)n_chunks * std::min(B, 16), 16 * sms);
         part.rows_k1 = grid_elem;
-        part.rows_k2 = half_v ? (plan_v.n_warps + 1) / 2 : plan_v.n_warps;
-        part.rows_k3 = fuse_combine ? plan_u.n_warps + plan_u.n_cuts : grid_comb;
+        part.rows_k2 = plan_v.n_warps;
+        part.rows_k3 = grid_comb;
         part.cnt = dalloc<int64_t>((size_t)grid_elem * B);
         part.np_u = dalloc<int64_t>((size_t)grid_elem * B);
         part.lmass = dalloc<double>((size_t)grid_elem * B);
@@ -474,30 +317,6 @@ struct Engine final : EngineBase {
         hook_est = dalloc<double>(nu);
         chunk_done = dalloc<int32_t>(MAX_B);
         BH_CUDA(cudaMemset(chunk_done, 0, MAX_B * sizeof(int32_t)));
-        if (getenv("BH_DEBUG_WARP_TIMING")) {
-            dbg_v = dalloc<uint64_t>((size_t)plan_v.n_warps * 4);
-            dbg_u = dalloc<uint64_t>((size_t)plan_u.n_warps * 4);
-        }
-    }
-
-    static void dump_warp_timing(const char *tag, const uint64_t *d, int n) {
-        std::vector<uint64_t> h((size_t)n * 4);
-        BH_CUDA(cudaMemcpy(h.data(), d, h.size() * 8, cudaMemcpyDeviceToHost));
-        uint64_t t0 = UINT64_MAX, t1 = 0;
-        for (int w = 0; w < n; w++) { t0 = std::min(t0, h[w * 4]); t1 = std::max(t1, h[w * 4 + 1]); }
-        std::vector<double> dur(n);
-        double sum = 0;
-        int worst = 0;
-        for (int w = 0; w < n; w++) {
-            dur[w] = (double)(h[w * 4 + 1] - h[w * 4]) / 1e3;
-            sum += dur[w];
-            if (dur[w] > dur[worst]) worst = w;
-        }
-        std::vector<double> s = dur;
-        std::sort(s.begin(), s.end());
-        fprintf(stderr, "[warp-timing %s] kernel span %.1f us, warp dur: min %.1f p50 %.1f p90 %.1f p99 %.1f max %.1f (warp %d, %llu edges, start +%.1f us)\n",
-                tag, (t1 - t0) / 1e3, s[0], s[n / 2], s[(int)(n * 0.9)], s[(int)(n * 0.99)], s[n - 1], worst,
-                (unsigned long long)h[worst * 4 + 2], (h[worst * 4] - t0) / 1e3);
     }
 
     ~Engine() override {
@@ -553,50 +372,11 @@ struct Engine final : EngineBase {
         a.active = &ctl->active;
         a.np_v = part.np_v;
         a.one_minus_alpha = one_minus_alpha;
-        a.dbg = side == SIDE_V ? dbg_v : dbg_u;
-        if (side == SIDE_U && fuse_combine) {
-            a.R = R;
-            a.Pn = P;
-            a.EST = EST;
-            a.alpha = alpha;
-            a.ws_u = g->ws_u;
-            a.inv_ws_u = g->inv_ws_u;
-            a.p_any = part.any;
-            a.p_sum = part.sum;
-            a.p_wsum = part.wsum;
-            a.part_rows = part.rows_k3;
-        }
         return a;
     }
 
     void launch_pull(int side, const PullArgs<T> &a, cudaStream_t st) {
-        const int grid = side == SIDE_V ? plan_v.grid : plan_u.grid;
-        if constexpr (WIDE) {
-            if (pull_tma) {
-                PullTmaArgs<T> ta;
-                ta.p = a;
-                ta.tmap = side == SIDE_V ? tmap_p : tmap_xv;
-                if (side == SIDE_V) launch_pdl(k_pull_tma<B, T, SIDE_V>, grid, PULL_THREADS, pull_smem, st, ta);
-                else launch_pdl(k_pull_tma<B, T, SIDE_U>, grid, PULL_THREADS, pull_smem, st, ta);
-                return;
-            }
-
-            const bool half = side == SIDE_V ? half_v : half_u;
-            if (side == SIDE_V) {
-                if (half && pull_sw) launch_pdl(k_pull_swh<B, T, SIDE_V>, grid, PULL_THREADS, pull_smem, st, a);
-                else if (half) launch_pdl(k_pull_half<B, T, SIDE_V>, grid, PULL_THREADS, pull_smem, st, a);
-                else if (pull_sw) launch_pdl(sw_kernel<SIDE_V>(), grid, PULL_THREADS, pull_smem, st, a);
-                else launch_pdl(k_pull<B, T, SIDE_V>, grid, PULL_THREADS, pull_smem, st, a);
-            } else {
-                if (half && pull_sw) launch_pdl(k_pull_swh<B, T, SIDE_U>, grid, PULL_THREADS, pull_smem, st, a);
-                else if (half) launch_pdl(k_pull_half<B, T, SIDE_U>, grid, PULL_THREADS, pull_smem, st, a);
-                else if (pull_sw) launch_pdl(sw_kernel<SIDE_U>(), grid, PULL_THREADS, pull_smem, st, a);
-                else launch_pdl(k_pull<B, T, SIDE_U>, grid, PULL_THREADS, pull_smem, st, a);
-            }
-        } else {
-            if (side == SIDE_V) launch_pdl(k_pull_small<B, T, SIDE_V>, grid, PULL_THREADS, 0, st, a);
-            else launch_pdl(k_pull_small<B, T, SIDE_U>, grid, PULL_THREADS, 0, st, a);
-        }
+        launch_pdl(pull_kernel(side), side == SIDE_V ? plan_v.grid : plan_u.grid, PULL_THREADS, 0, st, a);
     }
 
     // One round: K5 (the slots K4 finished last round) | K1 K2 K3 K1a | K4.  In the
@@ -628,7 +408,7 @@ struct Engine final : EngineBase {
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 3), st));
         launch_pull(SIDE_U, pull_args(SIDE_U, rs.alpha), st);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 4), st));
-        if (!fuse_combine) launch_pdl(combine_kernel(), grid_comb, ELEM_THREADS, 0, st, ea);
+        launch_pdl(combine_kernel(), grid_comb, ELEM_THREADS, 0, st, ea);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 5), st));
         if (with_k4) launch_pdl(k_control, B, CONTROL_THREADS, 0, st, ca);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 6), st));
@@ -638,7 +418,7 @@ struct Engine final : EngineBase {
         BH_CUDA(cudaGetLastError());
     }
 
-    int launches_per_round() const { return fuse_combine ? 5 : 6; }
+    int launches_per_round() const { return 6; }
 
     void collect_profile(int64_t rounds) {
         // events per round: K5 | K1 | K2 | K3 | K1a | K4
@@ -796,7 +576,7 @@ struct Engine final : EngineBase {
         stats.slots = B;
         stats.launches = 1;
         ca.max_rounds = 100000000;
-        if (!rs.hook && !prof && !dbg_v && !getenv("BH_NO_GRAPH")) {
+        if (!rs.hook && !prof && !getenv("BH_NO_GRAPH")) {
             g_tstamp[3] = host_us();
             ensure_graph(rs, ca, fa);
             g_tstamp[4] = host_us();
@@ -830,10 +610,6 @@ struct Engine final : EngineBase {
             }
             BH_CUDA(cudaMemcpyAsync(h_ctl, ctl, sizeof(Control), cudaMemcpyDeviceToHost, st));
             BH_CUDA(cudaStreamSynchronize(st));
-            if (dbg_v) {
-                dump_warp_timing("V", dbg_v, plan_v.n_warps);
-                dump_warp_timing("U", dbg_u, plan_u.n_warps);
-            }
             if (!h_ctl->active && h_ctl->n_fin == 0) {
                 stats.rounds = h_ctl->rounds_active;
                 if (prof) collect_profile(round);

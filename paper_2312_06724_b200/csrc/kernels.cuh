@@ -129,42 +129,6 @@ __device__ __forceinline__ bool op_is_fwd(int op) { return op == OP_FENTRY || op
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-// Per-slot constants staged in shared memory by the round kernels.
-struct SlotSmem {
-    int32_t op[MAX_B];
-    int32_t qidx[MAX_B];
-    int32_t src[MAX_B];
-    double eps_b[MAX_B];
-    double thc[MAX_B];     // eps_f / lam
-    double wsq[MAX_B];     // ws(source)
-    double iwsq[MAX_B];    // 1 / ws(source)
-    double ysc[MAX_B];
-};
-
-// Push threshold of a push op at node u: (ws_q / ws_u)(eps_f / lam) forward,
-// 0 sequential, eps_b selective.  K1 (which nodes feed the pulls) and K1a (which
-// residues it zeroes and moves into est) evaluate the same expression on the
-// same r, so they take the same decision.
-__device__ __forceinline__ double push_threshold(const SlotSmem &sm, int s, int o, double iws) {
-    if (op_is_fwd(o)) return (sm.wsq[s] * iws) * sm.thc[s];
-    return o == OP_SEQ ? 0.0 : sm.eps_b[s];
-}
-
-template <int B>
-__device__ __forceinline__ void load_slot_smem(SlotSmem &sm, const Slot *__restrict__ slots) {
-    for (int s = threadIdx.x; s < B; s += blockDim.x) {
-        const Slot &sl = slots[s];
-        sm.op[s] = sl.op;
-        sm.qidx[s] = sl.qidx;
-        sm.src[s] = sl.src;
-        sm.eps_b[s] = sl.eps_b;
-        sm.thc[s] = sl.theta_c;
-        sm.wsq[s] = sl.ws_q;
-        sm.iwsq[s] = sl.inv_ws_q;
-        sm.ysc[s] = sl.ysc;
-    }
-}
-
 // ---------------------------------------------------------------------------
 // Elementwise kernels over [n_u x B]: one thread per (node, EV consecutive slots).
 constexpr int ELEM_THREADS = 256;
@@ -540,17 +504,6 @@ struct PullArgs {
     const int32_t *active;
     int64_t *np_v;         // [n_warps][B] (V pull)
     double one_minus_alpha;
-    uint64_t *dbg;         // optional per-warp [start, end, edges, rows] globaltimer trace
-    // fused K3 + K1a (k_pull_sw<..., SIDE_U, COMBINE>): the U pull's row results
-    // go straight into the combine instead of through Y
-    T *R;                  // residues r_u [n_u][B]
-    T *Pn;                 // power-iteration iterate [n_u][B] (PI slots)
-    T *EST;                // estimates [n_u][B] (push slots: est += alpha r on the pushed nodes)
-    double alpha;
-    const double *ws_u, *inv_ws_u;
-    int32_t *p_any;        // partial rows [slot][part_rows]: one per warp, then one per cut row
-    double *p_sum, *p_wsum;
-    int32_t part_rows;
 };
 
 __device__ __forceinline__ uint64_t gtimer() {
@@ -642,273 +595,6 @@ __device__ __noinline__ IVec<VEC> pull_cut(CutCtx<T> cx, int ci, int pi, int slo
     return inc;
 }
 
-// B >= 32: lanes own slots; each warp streams its edge range with S operand
-// rows in flight in registers.  One loop of S-edge blocks, fully unrolled, no
-// range checks: the (col, val) windows are zero-padded past the range, so the
-// trailing issues gather row 0 with weight 0.  Row ends are 32-bit offsets;
-// rows cut by the range boundary keep their partial in registers and are
-// published after the loop.
-template <int B, typename T, int SIDE>
-__global__ void __launch_bounds__(PULL_THREADS, 2) k_pull(PullArgs<T> a) {
-    pdl_begin();
-    if (*a.active == 0) return;
-    constexpr int VEC = RegPipe<B, T>::VEC, S = RegPipe<B, T>::S;
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    const int gw = blockIdx.x * PULL_WARPS + warp;
-    const int slot0 = lane * VEC;
-    uint32_t cmask = 0;  // V side: slots in a push round count n_p
-    if constexpr (SIDE == SIDE_V) {
-#pragma unroll
-        for (int v = 0; v < VEC; v++) cmask |= (op_is_push(a.slots[slot0 + v].op) ? 1u : 0u) << v;
-    }
-    const double scale = SIDE == SIDE_V ? a.one_minus_alpha : 1.0;
-    int32_t np[VEC];
-#pragma unroll
-    for (int v = 0; v < VEC; v++) np[v] = 0;
-    int64_t np_cut[VEC];
-#pragma unroll
-    for (int v = 0; v < VEC; v++) np_cut[v] = 0;
-    const uint64_t t_start = a.dbg ? gtimer() : 0;
-
-    if (gw < a.n_warps) {
-        const WarpWork wk = a.work[gw];
-        const int64_t e0 = wk.e0;
-        const int n = (int)(wk.e1 - e0);
-        if (n > 0) {
-            const int32_t *cols = a.indices + e0;
-            const T *vals = a.vals + e0;
-            const T *X = a.X + slot0;
-            T *Y0 = a.Y + (int64_t)wk.r0 * B + slot0;
-            const int64_t *rp = a.indptr + wk.r0;  // row r0 + i ends at rp[i + 1]
-            const int64_t nrow_left = a.n_rows - wk.r0;
-            // local row index of the cut rows (-1: none)
-            const int cutA = wk.cut0 >= 0 ? 0 : -1;
-            const int cutB = wk.cut1 >= 0 ? (int)(a.cuts[wk.cut1].row - wk.r0) : -1;
-            auto col_at = [&](int o) { return o < n ? __ldg(cols + o) : 0; };
-            auto val_at = [&](int o) { return o < n ? __ldg(vals + o) : (T)0; };
-            auto rend_at = [&](int i) {  // clipped end offset of local row i
-                const int64_t r = i + 1 <= nrow_left ? __ldg(rp + i + 1) : __ldg(rp + nrow_left);
-                return (int)imin64(imin64(r - e0, n), (int64_t)n);
-            };
-            T xs[S][VEC];
-            T wsv[S];
-            {
-                const int c = col_at(lane);
-                const T w = val_at(lane);
-#pragma unroll
-                for (int t = 0; t < S; t++) {
-                    const int ct = __shfl_sync(0xffffffffu, c, t);
-                    wsv[t] = __shfl_sync(0xffffffffu, w, t);
-                    ldg_vec<T, VEC>(X + (int64_t)ct * B, xs[t]);
-                }
-            }
-            // windows of the next blocks' issues: lane t < S holds edge base + S + t
-            int cw = col_at(S + lane), cw1 = col_at(2 * S + lane);
-            T vw = val_at(S + lane), vw1 = val_at(2 * S + lane);
-            // row ends, 32 rows per window (current and next)
-            int rw = 0;
-            int re0 = rend_at(lane), re1 = rend_at(32 + lane);
-            int lr = 0;                                    // local row index
-            int rstart = (int)(__ldg(rp) - e0);            // may be < 0 for a cut first row
-            int rend = __shfl_sync(0xffffffffu, re0, 0);
-            double acc[VEC], accA[VEC], accB[VEC];
-            T accs[VEC];
-#pragma unroll
-            for (int v = 0; v < VEC; v++) {
-                acc[v] = accA[v] = accB[v] = 0.0;
-                accs[v] = (T)0;
-            }
-            for (int base = 0; base < n; base += S) {
-                int d = rend - base - 1;  // block offset of the current row's last edge
-#pragma unroll
-                for (int t = 0; t < S; t++) {
-                    if constexpr (sizeof(T) == 8) {
-#pragma unroll
-                        for (int v = 0; v < VEC; v++) acc[v] = fma((double)wsv[t], (double)xs[t][v], acc[v]);
-                    } else {
-#pragma unroll
-                        for (int v = 0; v < VEC; v++) accs[v] = fmaf(wsv[t], xs[t][v], accs[v]);
-                    }
-                    if (d == t) {  // ---- row emit (d is warp-uniform)
-                        if constexpr (sizeof(T) == 4) {
-#pragma unroll
-                            for (int v = 0; v < VEC; v++) {
-                                acc[v] += (double)accs[v];
-                                accs[v] = (T)0;
-                            }
-                        }
-                        if (lr == cutA) {
-#pragma unroll
-                            for (int v = 0; v < VEC; v++) accA[v] = acc[v];
-                        } else if (lr == cutB) {
-#pragma unroll
-                            for (int v = 0; v < VEC; v++) accB[v] = acc[v];
-                        } else {
-                            T out[VEC];
-#pragma unroll
-                            for (int v = 0; v < VEC; v++) {
-                                out[v] = (T)(scale * acc[v]);
-                                if constexpr (SIDE == SIDE_V)
-                                    np[v] += (((cmask >> v) & 1u) && out[v] > (T)0) ? rend - rstart : 0;
-                            }
-                            VecIO<T, VEC>::st(Y0 + (int64_t)lr * B, out);
-                        }
-#pragma unroll
-                        for (int v = 0; v < VEC; v++) acc[v] = 0.0;
-                        lr++;
-                        rstart = rend;
-                        if (lr - rw >= 32) {
-                            rw += 32;
-                            re0 = re1;
-                            re1 = rend_at(rw + 32 + lane);
-                        }
-                        rend = __shfl_sync(0xffffffffu, re0, lr - rw);
-                        d = rend - base - 1;
-                    }
-                    const int ct = __shfl_sync(0xffffffffu, cw, t);
-                    wsv[t] = __shfl_sync(0xffffffffu, vw, t);
-                    ldg_vec<T, VEC>(X + (int64_t)ct * B, xs[t]);
-                }
-                if constexpr (sizeof(T) == 4) {  // bound the fp32 partial to S terms
-#pragma unroll
-                    for (int v = 0; v < VEC; v++) {
-                        acc[v] += (double)accs[v];
-                        accs[v] = (T)0;
-                    }
-                }
-                cw = cw1;
-                vw = vw1;
-                cw1 = col_at(base + 3 * S + lane);
-                vw1 = val_at(base + 3 * S + lane);
-            }
-            // publish cut rows (rare path, out of line)
-            const CutCtx<T> cx{a.scratch, a.cut_count, a.cuts, a.Y, a.indptr, scale};
-            if (cutA >= 0) {
-                DVec<VEC> av;
-#pragma unroll
-                for (int v = 0; v < VEC; v++) av.v[v] = accA[v];
-                const IVec<VEC> inc = pull_cut<B, T, VEC>(cx, wk.cut0, wk.part0, slot0, cmask, av);
-#pragma unroll
-                for (int v = 0; v < VEC; v++) np_cut[v] += inc.v[v];
-            }
-            if (cutB >= 0) {
-                DVec<VEC> av;
-#pragma unroll
-                for (int v = 0; v < VEC; v++) av.v[v] = accB[v];
-                const IVec<VEC> inc = pull_cut<B, T, VEC>(cx, wk.cut1, wk.part1, slot0, cmask, av);
-#pragma unroll
-                for (int v = 0; v < VEC; v++) np_cut[v] += inc.v[v];
-            }
-        }
-    }
-    if (a.dbg && lane == 0 && gw < a.n_warps) {
-        a.dbg[gw * 4 + 0] = t_start;
-        a.dbg[gw * 4 + 1] = gtimer();
-        a.dbg[gw * 4 + 2] = (uint64_t)(a.work[gw].e1 - a.work[gw].e0);
-        uint32_t smid;
-        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        a.dbg[gw * 4 + 3] = smid;
-    }
-    if constexpr (SIDE == SIDE_V) {
-        if (gw < a.n_warps)
-#pragma unroll
-            for (int v = 0; v < VEC; v++) a.np_v[(int64_t)(slot0 + v) * a.n_warps + gw] = (int64_t)np[v] + np_cut[v];
-    }
-}
-
-// K1a for one U row inside the U pull: r_u += Y (push slots), a = y0 + Y (PI
-// slots), and the exit-test reductions (same arithmetic as k_combine).
-template <int B, typename T, int VEC>
-struct RowCombine {
-    double sum[VEC], wsum[VEC];
-    int32_t any[VEC];
-    __device__ __forceinline__ void init() {
-#pragma unroll
-        for (int v = 0; v < VEC; v++) {
-            sum[v] = wsum[v] = 0.0;
-            any[v] = 0;
-        }
-    }
-    __device__ __forceinline__ void row(const PullArgs<T> &a, const SlotSmem &sm, int slot0, int64_t u,
-                                        const double (&acc)[VEC], const T (&rv)[VEC], double ws, double iws) {
-        T nr[VEC], ev[VEC];
-        bool wrote_r = false, wrote_e = false, any_push = false;
-#pragma unroll
-        for (int v = 0; v < VEC; v++) any_push |= op_is_push(sm.op[slot0 + v]) && sm.op[slot0 + v] != OP_BSEL_INIT;
-        if (any_push) VecIO<T, VEC>::ld(a.EST + u * B + slot0, ev);
-#pragma unroll
-        for (int v = 0; v < VEC; v++) {
-            const int s = slot0 + v;
-            const int o = sm.op[s];
-            const T y = (T)acc[v];  // the value k_pull would have stored in Y
-            nr[v] = rv[v];
-            if (op_is_push(o) || o == OP_MEASURE) {
-                if (o != OP_MEASURE) {
-                    double r0 = (double)rv[v];
-                    if (o != OP_BSEL_INIT && r0 > push_threshold(sm, s, o, iws)) {  // pushed by K1 (see k_combine)
-                        ev[v] = (T)((double)ev[v] + a.alpha * r0);
-                        wrote_e = true;
-                        r0 = 0.0;
-                    }
-                    nr[v] = (T)(r0 + (double)y);
-                    wrote_r = true;
-                }
-                const double r = (double)nr[v];
-                sum[v] += r;
-                wsum[v] += (ws * sm.iwsq[s]) * r;  // w_ratio * r  (push_engine.py:220,237)
-                const double th = (op_is_fwd(o) || o == OP_MEASURE) ? (sm.wsq[s] * iws) * sm.thc[s] : sm.eps_b[s];
-                any[v] |= r > th;
-            } else if (o == OP_PIENTRY || o == OP_PI) {
-                a.Pn[u * B + s] = (T)((double)rv[v] * sm.ysc[s] + (double)y);
-            }
-        }
-        if (wrote_r) VecIO<T, VEC>::st(a.R + u * B + slot0, nr);
-        if (wrote_e) VecIO<T, VEC>::st(a.EST + u * B + slot0, ev);
-    }
-    __device__ __forceinline__ void store(const PullArgs<T> &a, int row, int slot0) const {
-#pragma unroll
-        for (int v = 0; v < VEC; v++) {
-            const int64_t i = (int64_t)(slot0 + v) * a.part_rows + row;
-            a.p_sum[i] = sum[v];
-            a.p_wsum[i] = wsum[v];
-            a.p_any[i] = any[v];
-        }
-    }
-};
-
-// Cut row of the fused U pull: the last warp to arrive adds the partials and
-// runs the row's combine; its reductions go to partial row n_warps + cut index.
-template <int B, typename T, int VEC>
-__device__ __noinline__ void pull_cut_combine(const PullArgs<T> &a, const SlotSmem &sm, int ci, int pi, int slot0,
-                                              DVec<VEC> acc) {
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int v = 0; v < VEC; v++) a.scratch[(int64_t)pi * B + slot0 + v] = acc.v[v];
-    __threadfence();
-    __syncwarp();
-    const CutRow cr = a.cuts[ci];
-    int last = 0;
-    if (lane == 0) last = atomicAdd(a.cut_count + ci, 1) == cr.n_parts - 1;
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (!last) return;
-    __threadfence();
-    double tot[VEC];
-#pragma unroll
-    for (int v = 0; v < VEC; v++) tot[v] = 0.0;
-    for (int p = 0; p < cr.n_parts; p++)
-#pragma unroll
-        for (int v = 0; v < VEC; v++) tot[v] += __ldcg(a.scratch + (int64_t)(cr.first_part + p) * B + slot0 + v);
-    const int64_t u = cr.row;
-    T rv[VEC];
-    VecIO<T, VEC>::ld(a.R + u * B + slot0, rv);
-    RowCombine<B, T, VEC> rc;
-    rc.init();
-    rc.row(a, sm, slot0, u, tot, rv, a.ws_u[u], a.inv_ws_u[u]);
-    rc.store(a, a.n_warps + ci, slot0);
-    if (lane == 0) a.cut_count[ci] = 0;
-}
-
 // Same streaming pull with the per-warp (col, val) windows and row ends staged
 // in shared memory instead of lane registers: the per-edge work is one
 // broadcast LDS of the next (col, val) pair, the operand-row gather and VEC
@@ -930,20 +616,11 @@ struct EdgeCV {
     T v;
 };
 
-template <int B, typename T, int SIDE, bool COMBINE = false, int S = SwPipe<B, T>::S,
-          int MINB = COMBINE ? 2 : SwPipe<B, T>::MINB>
+template <int B, typename T, int SIDE, int S = SwPipe<B, T>::S, int MINB = SwPipe<B, T>::MINB>
 __global__ void __launch_bounds__(PULL_THREADS, MINB) k_pull_sw(PullArgs<T> a) {
-    static_assert(!COMBINE || SIDE == SIDE_U, "the combine follows the U pull");
     pdl_begin();
     if (*a.active == 0) return;
     constexpr int VEC = RegPipe<B, T>::VEC;
-    __shared__ std::conditional_t<COMBINE, SlotSmem, int> sm_c;  // slot constants, fused combine only
-    if constexpr (COMBINE) {
-        load_slot_smem<B>(sm_c, a.slots);
-        __syncthreads();
-    }
-    RowCombine<B, T, VEC> rc;
-    rc.init();
     static_assert(2 * S <= 32, "two windows must fit one warp load");
     __shared__ EdgeCV<T> s_win[PULL_WARPS][2][S];
     __shared__ int32_t s_re[PULL_WARPS][64];
@@ -1000,20 +677,6 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) k_pull_sw(PullArgs<T> a) {
                 wsv[t] = e.v;
                 ldg_vec<T, VEC>(X + (int64_t)e.c * B, xs[t]);
             }
-            // fused combine: r_u row and ws of the next row to finish, one row ahead
-            T rpre[VEC];
-            double wpre = 0.0, ipre = 0.0;
-            auto prefetch_row = [&](int l) {
-                if constexpr (COMBINE) {
-                    const int64_t u = (int64_t)wk.r0 + l;
-                    if (u < a.n_rows) {
-                        VecIO<T, VEC>::ld(a.R + u * B + slot0, rpre);
-                        wpre = __ldg(a.ws_u + u);
-                        ipre = __ldg(a.inv_ws_u + u);
-                    }
-                }
-            };
-            prefetch_row(0);
             int rw = 0;       // row-end ring holds local rows [rw, rw + 64)
             int lr = 0;
             int rstart = (int)(__ldg(rp) - e0);
@@ -1050,8 +713,6 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) k_pull_sw(PullArgs<T> a) {
                             double *dst = a.scratch + (int64_t)(lr == cutA ? wk.part0 : wk.part1) * B + slot0;
 #pragma unroll
                             for (int v = 0; v < VEC; v++) dst[v] = acc[v];
-                        } else if constexpr (COMBINE) {
-                            rc.row(a, sm_c, slot0, (int64_t)wk.r0 + lr, acc, rpre, wpre, ipre);
                         } else {
                             T out[VEC];
 #pragma unroll
@@ -1068,7 +729,6 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) k_pull_sw(PullArgs<T> a) {
                         rstart = rend;
                         rend = re[lr & 63];
                         d = rend - base - 1;
-                        if constexpr (COMBINE) prefetch_row(lr);
                     }
                     const EdgeCV<T> e = nxt[t];
                     wsv[t] = e.v;
@@ -1091,254 +751,6 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) k_pull_sw(PullArgs<T> a) {
                 cw = col_at(base + 3 * S + lane);
                 vw = val_at(base + 3 * S + lane);
                 __syncwarp();
-            }
-            if constexpr (COMBINE) {
-                if (cutA >= 0) {
-                    DVec<VEC> av;
-#pragma unroll
-                    for (int v = 0; v < VEC; v++) av.v[v] = a.scratch[(int64_t)wk.part0 * B + slot0 + v];
-                    pull_cut_combine<B, T, VEC>(a, sm_c, wk.cut0, wk.part0, slot0, av);
-                }
-                if (cutB >= 0) {
-                    DVec<VEC> av;
-#pragma unroll
-                    for (int v = 0; v < VEC; v++) av.v[v] = a.scratch[(int64_t)wk.part1 * B + slot0 + v];
-                    pull_cut_combine<B, T, VEC>(a, sm_c, wk.cut1, wk.part1, slot0, av);
-                }
-            }
-            const CutCtx<T> cx{a.scratch, a.cut_count, a.cuts, a.Y, a.indptr, scale};
-            if (!COMBINE && cutA >= 0) {
-                DVec<VEC> av;
-#pragma unroll
-                for (int v = 0; v < VEC; v++) av.v[v] = a.scratch[(int64_t)wk.part0 * B + slot0 + v];
-                const IVec<VEC> inc = pull_cut<B, T, VEC>(cx, wk.cut0, wk.part0, slot0, cmask, av);
-#pragma unroll
-                for (int v = 0; v < VEC; v++) np_cut[v] += inc.v[v];
-            }
-            if (!COMBINE && cutB >= 0) {
-                DVec<VEC> av;
-#pragma unroll
-                for (int v = 0; v < VEC; v++) av.v[v] = a.scratch[(int64_t)wk.part1 * B + slot0 + v];
-                const IVec<VEC> inc = pull_cut<B, T, VEC>(cx, wk.cut1, wk.part1, slot0, cmask, av);
-#pragma unroll
-                for (int v = 0; v < VEC; v++) np_cut[v] += inc.v[v];
-            }
-        }
-    }
-    if constexpr (SIDE == SIDE_V) {
-        if (gw < a.n_warps)
-#pragma unroll
-            for (int v = 0; v < VEC; v++) a.np_v[(int64_t)(slot0 + v) * a.n_warps + gw] = (int64_t)np[v] + np_cut[v];
-    }
-    if constexpr (COMBINE) {
-        if (gw < a.n_warps) rc.store(a, gw, slot0);
-    }
-}
-
-// ---------------------------------------------------------------------------
-// TMA-gather pull (sm_100a): the operand rows are fetched by the tensor memory
-// accelerator with cp.async.bulk.tensor.2d ... tile::gather4 (four rows of
-// B * sizeof(T) bytes per instruction, issued by one lane) into a per-warp
-// ring of NS four-row stages completed on mbarriers, so 4 * NS rows per warp
-// are in flight without holding registers; the lanes read their VEC slots of
-// each row back from shared memory.  Same edge ranges, row emit, cut rows and
-// n_p accounting as k_pull_sw.
-template <typename T>
-struct PullTmaArgs {
-    PullArgs<T> p;
-    CUtensorMap tmap;  // X as a [n_rows][B] tensor, box {B, 1}
-};
-
-template <int B, typename T>
-struct TmaPipe {
-    static constexpr int ROW = B * (int)sizeof(T);
-    static constexpr int NS = ROW <= 256 ? 8 : 4;         // stages (4 rows each) per warp
-    static constexpr int STAGE = 4 * ROW;
-    // per warp, rounded to 128 B so every warp's stages are TMA-aligned
-    static constexpr int WARP_BYTES = (NS * STAGE + 3 * 32 * (int)sizeof(EdgeCV<T>) + 64 * 4 + NS * 8 + 127) / 128 * 128;
-    static constexpr int BLOCK_BYTES = PULL_WARPS * WARP_BYTES + 128;
-};
-
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    uint32_t ok = 0;
-    while (!ok) {
-        asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-            : "=r"(ok)
-            : "r"(bar), "r"(parity)
-            : "memory");
-    }
-}
-__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *map, uint32_t bar, int r0, int r1,
-                                            int r2, int r3) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
-        "l"(map), "r"(bar), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
-        : "memory");
-}
-
-template <int B, typename T, int SIDE>
-__global__ void __launch_bounds__(PULL_THREADS) k_pull_tma(const __grid_constant__ PullTmaArgs<T> ta) {
-    pdl_begin();
-    const PullArgs<T> &a = ta.p;
-    if (*a.active == 0) return;
-    using TP = TmaPipe<B, T>;
-    constexpr int VEC = B / 32, NS = TP::NS, ROW = TP::ROW, STAGE = TP::STAGE;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    unsigned char *sbase = (unsigned char *)(((uintptr_t)smem_raw + 127) & ~(uintptr_t)127);
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    const int gw = blockIdx.x * PULL_WARPS + warp;
-    const int slot0 = lane * VEC;
-    // per-warp carve: stages | windows (3 x 32 (col, val)) | row-end ring | barriers
-    unsigned char *wbase = sbase + warp * TP::WARP_BYTES;
-    unsigned char *stages = wbase;
-    EdgeCV<T>(*win)[32] = reinterpret_cast<EdgeCV<T>(*)[32]>(wbase + NS * STAGE);
-    int32_t *re = reinterpret_cast<int32_t *>(wbase + NS * STAGE + 3 * 32 * sizeof(EdgeCV<T>));
-    uint64_t *bars = reinterpret_cast<uint64_t *>(wbase + NS * STAGE + 3 * 32 * sizeof(EdgeCV<T>) + 64 * 4);
-    const uint32_t st0 = smem_u32(stages), bar0 = smem_u32(bars);
-
-    uint32_t cmask = 0;
-    if constexpr (SIDE == SIDE_V) {
-#pragma unroll
-        for (int v = 0; v < VEC; v++) cmask |= (op_is_push(a.slots[slot0 + v].op) ? 1u : 0u) << v;
-    }
-    const double scale = SIDE == SIDE_V ? a.one_minus_alpha : 1.0;
-    int32_t np[VEC];
-    int64_t np_cut[VEC];
-#pragma unroll
-    for (int v = 0; v < VEC; v++) {
-        np[v] = 0;
-        np_cut[v] = 0;
-    }
-    if (gw < a.n_warps) {
-        const WarpWork wk = a.work[gw];
-        const int64_t e0 = wk.e0;
-        const int n = (int)(wk.e1 - e0);
-        if (n > 0) {
-            const int32_t *cols = a.indices + e0;
-            const T *vals = a.vals + e0;
-            T *Y0 = a.Y + (int64_t)wk.r0 * B + slot0;
-            const int64_t *rp = a.indptr + wk.r0;
-            const int64_t nrow_left = a.n_rows - wk.r0;
-            const int cutA = wk.cut0 >= 0 ? 0 : -1;
-            const int cutB = wk.cut1 >= 0 ? (int)(a.cuts[wk.cut1].row - wk.r0) : -1;
-            auto col_at = [&](int o) { return o < n ? __ldg(cols + o) : 0; };
-            auto val_at = [&](int o) { return o < n ? __ldg(vals + o) : (T)0; };
-            auto rend_at = [&](int i) {
-                const int64_t r = i + 1 <= nrow_left ? __ldg(rp + i + 1) : __ldg(rp + nrow_left);
-                return (int)imin64(r - e0, (int64_t)n);
-            };
-            const int ngroups = (n + 3) >> 2;
-            // windows 0, 1 resident (slots 0, 1); window 2 in registers
-            win[0][lane] = EdgeCV<T>{col_at(lane), val_at(lane)};
-            win[1][lane] = EdgeCV<T>{col_at(32 + lane), val_at(32 + lane)};
-            int cw = col_at(64 + lane);
-            T vw = val_at(64 + lane);
-            re[lane] = rend_at(lane);
-            re[32 + lane] = rend_at(32 + lane);
-            if (lane < NS) mbar_init(bar0 + 8 * lane, 1);
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-            __syncwarp();
-            auto issue = [&](int g) {  // group g = edges 4g .. 4g+3 -> stage g % NS (lane 0)
-                const EdgeCV<T> *e = &win[(g >> 3) % 3][(g & 7) * 4];
-                const uint32_t bar = bar0 + 8 * (g % NS);
-                mbar_expect_tx(bar, STAGE);
-                tma_gather4(st0 + (g % NS) * STAGE, &ta.tmap, bar, e[0].c, e[1].c, e[2].c, e[3].c);
-            };
-            if (lane == 0)
-                for (int g = 0; g < NS && g < ngroups; g++) issue(g);
-            int rw = 0, lr = 0;
-            int rstart = (int)(__ldg(rp) - e0);
-            int rend = re[0];
-            double acc[VEC];
-            T accs[VEC];
-#pragma unroll
-            for (int v = 0; v < VEC; v++) {
-                acc[v] = 0.0;
-                accs[v] = (T)0;
-            }
-            for (int g = 0; g < ngroups; g++) {
-                const int base = g << 2;
-                const EdgeCV<T> *ecur = &win[(g >> 3) % 3][(g & 7) * 4];
-                T w4[4];
-#pragma unroll
-                for (int t = 0; t < 4; t++) w4[t] = ecur[t].v;
-                mbar_wait(bar0 + 8 * (g % NS), (uint32_t)((g / NS) & 1));
-                const unsigned char *stg = stages + (g % NS) * STAGE + slot0 * sizeof(T);
-                int d = rend - base - 1;
-#pragma unroll
-                for (int t = 0; t < 4; t++) {
-                    T x[VEC];
-                    VecIO<T, VEC>::ld(reinterpret_cast<const T *>(stg + t * ROW), x);
-                    if constexpr (sizeof(T) == 8) {
-#pragma unroll
-                        for (int v = 0; v < VEC; v++) acc[v] = fma((double)w4[t], (double)x[v], acc[v]);
-                    } else {
-#pragma unroll
-                        for (int v = 0; v < VEC; v++) accs[v] = fmaf(w4[t], x[v], accs[v]);
-                    }
-                    if (d == t) {  // row emit
-                        if constexpr (sizeof(T) == 4) {
-#pragma unroll
-                            for (int v = 0; v < VEC; v++) {
-                                acc[v] += (double)accs[v];
-                                accs[v] = (T)0;
-                            }
-                        }
-                        if (lr == cutA || lr == cutB) {
-                            double *dst = a.scratch + (int64_t)(lr == cutA ? wk.part0 : wk.part1) * B + slot0;
-#pragma unroll
-                            for (int v = 0; v < VEC; v++) dst[v] = acc[v];
-                        } else {
-                            T out[VEC];
-#pragma unroll
-                            for (int v = 0; v < VEC; v++) {
-                                out[v] = (T)(scale * acc[v]);
-                                if constexpr (SIDE == SIDE_V)
-                                    np[v] += (((cmask >> v) & 1u) && out[v] > (T)0) ? rend - rstart : 0;
-                            }
-                            VecIO<T, VEC>::st(Y0 + (int64_t)lr * B, out);
-                        }
-#pragma unroll
-                        for (int v = 0; v < VEC; v++) acc[v] = 0.0;
-                        lr++;
-                        rstart = rend;
-                        rend = re[lr & 63];
-                        d = rend - base - 1;
-                    }
-                }
-                if constexpr (sizeof(T) == 4) {  // bound the fp32 partial to 16 terms
-                    if ((g & 3) == 3) {
-#pragma unroll
-                        for (int v = 0; v < VEC; v++) {
-                            acc[v] += (double)accs[v];
-                            accs[v] = (T)0;
-                        }
-                    }
-                }
-                __syncwarp();  // stage g % NS and the row ends before lr are consumed
-                if ((g & 7) == 7) {
-                    // window g/8 done: window g/8 + 2 (in registers) takes the slot of
-                    // window g/8 - 1; prefetch window g/8 + 3
-                    const int wnext = (g >> 3) + 2;
-                    win[wnext % 3][lane] = EdgeCV<T>{cw, vw};
-                    cw = col_at(32 * (wnext + 1) + lane);
-                    vw = val_at(32 * (wnext + 1) + lane);
-                }
-                if (lr - rw >= 32) {
-                    re[(rw + 64 + lane) & 63] = rend_at(rw + 64 + lane);
-                    rw += 32;
-                }
-                __syncwarp();
-                if (lane == 0 && g + NS < ngroups) issue(g + NS);
             }
             const CutCtx<T> cx{a.scratch, a.cut_count, a.cuts, a.Y, a.indptr, scale};
             if (cutA >= 0) {
@@ -1366,443 +778,9 @@ __global__ void __launch_bounds__(PULL_THREADS) k_pull_tma(const __grid_constant
     }
 }
 
-// ---------------------------------------------------------------------------
-// Half-warp workers (B >= 32): each 16-lane half of a warp is an independent
-// worker with its own cost-balanced edge range; a lane owns VEC = B/16 slots
-// (16 B of fp32 at B = 64), so one warp instruction gathers two operand rows.
-// Same pipeline as k_pull: S rows in flight per worker in registers, zero-
-// padded (col, val) windows, width-16 shuffles with immediate lanes, compact
-// per-row emit, cut rows published after the loop.
-template <int B, typename T>
-struct HalfPipe {
-    static constexpr int VEC = B / 16;
-    static constexpr int LANE_BYTES = VEC * (int)sizeof(T);
-    static constexpr int S = LANE_BYTES <= 8 ? 16 : (LANE_BYTES <= 16 ? 8 : (LANE_BYTES <= 32 ? 4 : 2));
-};
-
-template <int B, typename T, int VEC>
-__device__ __noinline__ IVec<VEC> pull_cut_half(CutCtx<T> cx, int ci, int pi, int slot0, uint32_t cmask,
-                                                DVec<VEC> acc, uint32_t hmask) {
-    const int q = threadIdx.x & 15;
-    IVec<VEC> inc;
-#pragma unroll
-    for (int v = 0; v < VEC; v++) inc.v[v] = 0;
-#pragma unroll
-    for (int v = 0; v < VEC; v++) cx.scratch[(int64_t)pi * B + slot0 + v] = acc.v[v];
-    __threadfence();
-    __syncwarp(hmask);
-    const CutRow cr = cx.cuts[ci];
-    int last = 0;
-    if (q == 0) last = atomicAdd(cx.cut_count + ci, 1) == cr.n_parts - 1;
-    last = __shfl_sync(hmask, last, 0, 16);
-    if (!last) return inc;
-    __threadfence();
-    double tot[VEC];
-#pragma unroll
-    for (int v = 0; v < VEC; v++) tot[v] = 0.0;
-    int p = 0;
-    for (; p + 4 <= cr.n_parts; p += 4) {
-        double qv[4][VEC];
-#pragma unroll
-        for (int k = 0; k < 4; k++)
-#pragma unroll
-            for (int v = 0; v < VEC; v++) qv[k][v] = __ldcg(cx.scratch + (int64_t)(cr.first_part + p + k) * B + slot0 + v);
-#pragma unroll
-        for (int k = 0; k < 4; k++)
-#pragma unroll
-            for (int v = 0; v < VEC; v++) tot[v] += qv[k][v];
-    }
-    for (; p < cr.n_parts; p++)
-#pragma unroll
-        for (int v = 0; v < VEC; v++) tot[v] += __ldcg(cx.scratch + (int64_t)(cr.first_part + p) * B + slot0 + v);
-    const int64_t deg = __ldg(cx.indptr + cr.row + 1) - __ldg(cx.indptr + cr.row);
-    T out[VEC];
-#pragma unroll
-    for (int v = 0; v < VEC; v++) {
-        out[v] = (T)(cx.scale * tot[v]);
-        if (((cmask >> v) & 1u) && (double)out[v] > 0.0) inc.v[v] = deg;
-    }
-    VecIO<T, VEC>::st(cx.Y + (int64_t)cr.row * B + slot0, out);
-    if (q == 0) cx.cut_count[ci] = 0;
-    return inc;
-}
-
-template <int B, typename T, int SIDE>
-__global__ void __launch_bounds__(PULL_THREADS, 2) k_pull_half(PullArgs<T> a) {
-    pdl_begin();
-    if (*a.active == 0) return;
-    constexpr int VEC = HalfPipe<B, T>::VEC, S = HalfPipe<B, T>::S;
-    const int lane = threadIdx.x & 31;
-    const int h = lane >> 4, q = lane & 15;
-    const uint32_t hmask = h ? 0xffff0000u : 0x0000ffffu;
-    const int warp = threadIdx.x >> 5;
-    const int gw = blockIdx.x * PULL_WARPS + warp;
-    const int wid = gw * 2 + h;  // worker
-    const int slot0 = q * VEC;
-    uint32_t cmask = 0;
-    if constexpr (SIDE == SIDE_V) {
-#pragma unroll
-        for (int v = 0; v < VEC; v++) cmask |= (op_is_push(a.slots[slot0 + v].op) ? 1u : 0u) << v;
-    }
-    const double scale = SIDE == SIDE_V ? a.one_minus_alpha : 1.0;
-    int32_t np[VEC];
-    int64_t np_cut[VEC];
-#pragma unroll
-    for (int v = 0; v < VEC; v++) {
-        np[v] = 0;
-        np_cut[v] = 0;
-    }
-    const uint64_t t_start = a.dbg ? gtimer() : 0;
-    const int n_workers = a.n_warps;  // work entries (two per warp)
-    WarpWork wk;
-    wk.e0 = wk.e1 = 0;
-    wk.r0 = 0;
-    wk.cut0 = wk.cut1 = wk.part0 = wk.part1 = -1;
-    if (wid < n_workers) wk = a.work[wid];
-    const int64_t e0 = wk.e0;
-    const int n = (int)(wk.e1 - e0);
-    const int n_max = max(n, __shfl_xor_sync(0xffffffffu, n, 16));
-    if (n_max > 0) {
-        const int32_t *cols = a.indices + e0;
-        const T *vals = a.vals + e0;
-        const T *X = a.X + slot0;
-        T *Y0 = a.Y + (int64_t)wk.r0 * B + slot0;
-        const int64_t *rp = a.indptr + wk.r0;
-        const int64_t nrow_left = a.n_rows - wk.r0;
-        const int cutA = wk.cut0 >= 0 ? 0 : -1;
-        const int cutB = wk.cut1 >= 0 ? (int)(a.cuts[wk.cut1].row - wk.r0) : -1;
-        auto col_at = [&](int o) { return o < n ? __ldg(cols + o) : 0; };
-        auto val_at = [&](int o) { return o < n ? __ldg(vals + o) : (T)0; };
-        auto rend_at = [&](int i) {
-            if (n <= 0) return 0;
-            const int64_t r = i + 1 <= nrow_left ? __ldg(rp + i + 1) : __ldg(rp + nrow_left);
-            return (int)imin64(r - e0, (int64_t)n);
-        };
-        T xs[S][VEC];
-        T wsv[S];
-        {
-            const int c = col_at(q);
-            const T w = val_at(q);
-#pragma unroll
-            for (int t = 0; t < S; t++) {
-                const int ct = __shfl_sync(0xffffffffu, c, t, 16);
-                wsv[t] = __shfl_sync(0xffffffffu, w, t, 16);
-                ldg_vec<T, VEC>(X + (int64_t)ct * B, xs[t]);
-            }
-        }
-        int cw = col_at(S + q), cw1 = col_at(2 * S + q);
-        T vw = val_at(S + q), vw1 = val_at(2 * S + q);
-        int rw = 0;
-        int re0 = rend_at(q), re1 = rend_at(16 + q);
-        int lr = 0;
-        int rstart = n > 0 ? (int)(__ldg(rp) - e0) : 0;
-        int rend = __shfl_sync(0xffffffffu, re0, 0, 16);
-        if (n <= 0) rend = 1 << 30;  // idle worker: never emits
-        double acc[VEC], accA[VEC], accB[VEC];
-        T accs[VEC];
-#pragma unroll
-        for (int v = 0; v < VEC; v++) {
-            acc[v] = accA[v] = accB[v] = 0.0;
-            accs[v] = (T)0;
-        }
-        for (int base = 0; base < n_max; base += S) {
-            int d = rend - base - 1;
-            int cvec[S];
-            T wvec[S];
-#pragma unroll
-            for (int t = 0; t < S; t++) {
-                cvec[t] = __shfl_sync(0xffffffffu, cw, t, 16);
-                wvec[t] = __shfl_sync(0xffffffffu, vw, t, 16);
-            }
-#pragma unroll
-            for (int t = 0; t < S; t++) {
-                if constexpr (sizeof(T) == 8) {
-#pragma unroll
-                    for (int v = 0; v < VEC; v++) acc[v] = fma((double)wsv[t], (double)xs[t][v], acc[v]);
-                } else {
-#pragma unroll
-                    for (int v = 0; v < VEC; v++) accs[v] = fmaf(wsv[t], xs[t][v], accs[v]);
-                }
-                if (d == t) {  // ---- row emit (uniform within the half-warp)
-                    if constexpr (sizeof(T) == 4) {
-#pragma unroll
-                        for (int v = 0; v < VEC; v++) {
-                            acc[v] += (double)accs[v];
-                            accs[v] = (T)0;
-                        }
-                    }
-                    if (lr == cutA) {
-#pragma unroll
-                        for (int v = 0; v < VEC; v++) accA[v] = acc[v];
-                    } else if (lr == cutB) {
-#pragma unroll
-                        for (int v = 0; v < VEC; v++) accB[v] = acc[v];
-                    } else {
-                        T out[VEC];
-#pragma unroll
-                        for (int v = 0; v < VEC; v++) {
-                            out[v] = (T)(scale * acc[v]);
-                            if constexpr (SIDE == SIDE_V)
-                                np[v] += (((cmask >> v) & 1u) && out[v] > (T)0) ? rend - rstart : 0;
-                        }
-                        VecIO<T, VEC>::st(Y0 + (int64_t)lr * B, out);
-                    }
-#pragma unroll
-                    for (int v = 0; v < VEC; v++) acc[v] = 0.0;
-                    lr++;
-                    rstart = rend;
-                    if (lr - rw >= 16) {
-                        rw += 16;
-                        re0 = re1;
-                        re1 = rend_at(rw + 16 + q);
-                    }
-                    rend = __shfl_sync(hmask, re0, lr - rw, 16);
-                    d = rend - base - 1;
-                }
-                wsv[t] = wvec[t];
-                ldg_vec<T, VEC>(X + (int64_t)cvec[t] * B, xs[t]);
-            }
-            if constexpr (sizeof(T) == 4) {
-#pragma unroll
-                for (int v = 0; v < VEC; v++) {
-                    acc[v] += (double)accs[v];
-                    accs[v] = (T)0;
-                }
-            }
-            cw = cw1;
-            vw = vw1;
-            cw1 = col_at(base + 3 * S + q);
-            vw1 = val_at(base + 3 * S + q);
-        }
-        const CutCtx<T> cx{a.scratch, a.cut_count, a.cuts, a.Y, a.indptr, scale};
-        for (int hh = 0; hh < 2; hh++) {
-            if (h == hh) {
-                if (cutA >= 0) {
-                    DVec<VEC> av;
-#pragma unroll
-                    for (int v = 0; v < VEC; v++) av.v[v] = accA[v];
-                    const IVec<VEC> inc = pull_cut_half<B, T, VEC>(cx, wk.cut0, wk.part0, slot0, cmask, av, hmask);
-#pragma unroll
-                    for (int v = 0; v < VEC; v++) np_cut[v] += inc.v[v];
-                }
-                if (cutB >= 0) {
-                    DVec<VEC> av;
-#pragma unroll
-                    for (int v = 0; v < VEC; v++) av.v[v] = accB[v];
-                    const IVec<VEC> inc = pull_cut_half<B, T, VEC>(cx, wk.cut1, wk.part1, slot0, cmask, av, hmask);
-#pragma unroll
-                    for (int v = 0; v < VEC; v++) np_cut[v] += inc.v[v];
-                }
-            }
-            __syncwarp();
-        }
-    }
-    if (a.dbg && lane == 0 && gw * 2 < n_workers) {
-        a.dbg[gw * 4 + 0] = t_start;
-        a.dbg[gw * 4 + 1] = gtimer();
-        a.dbg[gw * 4 + 2] = (uint64_t)n;
-        a.dbg[gw * 4 + 3] = 0;
-    }
-    if constexpr (SIDE == SIDE_V) {
-        // both halves cover the same slots: combine, half 0 writes the warp's row
-        const int n_rows_out = (n_workers + 1) / 2;
-#pragma unroll
-        for (int v = 0; v < VEC; v++) {
-            int64_t t = (int64_t)np[v] + np_cut[v];
-            t += __shfl_xor_sync(0xffffffffu, t, 16);
-            if (h == 0 && gw < n_rows_out) a.np_v[(int64_t)(slot0 + v) * n_rows_out + gw] = t;
-        }
-    }
-}
 
 // B < 32 (single-query and small blocks): G lanes per edge group, 32/G groups
 // split each row; plain loads.  Same partition, cut rows and epilogue.
-// Half-warp workers with shared-memory windows (k_pull_swh): the k_pull_sw
-// edge loop run by each 16-lane half of a warp on its own cost-balanced edge
-// range (the half-warp plan of k_pull_half), a lane owning VEC = B/16 slots, so
-// one warp instruction gathers two operand rows (LDG.128 at B = 64 fp32) and
-// the per-edge (col, val) read, address arithmetic and loop overhead are paid
-// once per two edges.  Row emits diverge between the halves.
-template <int B, typename T, int SIDE, int S = (HalfPipe<B, T>::S < 8 ? HalfPipe<B, T>::S : 8), int MINB = 2>
-__global__ void __launch_bounds__(PULL_THREADS, MINB) k_pull_swh(PullArgs<T> a) {
-    pdl_begin();
-    if (*a.active == 0) return;
-    constexpr int VEC = B / 16;
-    static_assert(2 * S <= 16, "a half-warp stages two windows per load");
-    constexpr int WSTRIDE = 2 * S + 1;  // +1 entry: the two halves' windows on different banks
-    __shared__ EdgeCV<T> s_win[PULL_WARPS * 2][WSTRIDE];
-    __shared__ int32_t s_re[PULL_WARPS * 2][33];
-    const int lane = threadIdx.x & 31;
-    const int h = lane >> 4, q = lane & 15;
-    const uint32_t hmask = h ? 0xffff0000u : 0x0000ffffu;
-    const int warp = threadIdx.x >> 5;
-    const int gw = blockIdx.x * PULL_WARPS + warp;
-    const int wid = gw * 2 + h;
-    const int slot0 = q * VEC;
-    uint32_t cmask = 0;
-    if constexpr (SIDE == SIDE_V) {
-#pragma unroll
-        for (int v = 0; v < VEC; v++) cmask |= (op_is_push(a.slots[slot0 + v].op) ? 1u : 0u) << v;
-    }
-    const double scale = SIDE == SIDE_V ? a.one_minus_alpha : 1.0;
-    int32_t np[VEC];
-    int64_t np_cut[VEC];
-#pragma unroll
-    for (int v = 0; v < VEC; v++) {
-        np[v] = 0;
-        np_cut[v] = 0;
-    }
-    const int n_workers = a.n_warps;  // work entries (two per warp)
-    WarpWork wk;
-    wk.e0 = wk.e1 = 0;
-    wk.r0 = 0;
-    wk.cut0 = wk.cut1 = wk.part0 = wk.part1 = -1;
-    if (wid < n_workers) wk = a.work[wid];
-    const int64_t e0 = wk.e0;
-    const int n = (int)(wk.e1 - e0);
-    const int n_max = max(n, __shfl_xor_sync(0xffffffffu, n, 16));
-    if (n_max > 0) {
-        const int32_t *cols = a.indices + e0;
-        const T *vals = a.vals + e0;
-        const T *X = a.X + slot0;
-        T *Y0 = a.Y + (int64_t)wk.r0 * B + slot0;
-        const int64_t *rp = a.indptr + wk.r0;
-        const int64_t nrow_left = a.n_rows - wk.r0;
-        const int cutA = wk.cut0 >= 0 ? 0 : -1;
-        const int cutB = wk.cut1 >= 0 ? (int)(a.cuts[wk.cut1].row - wk.r0) : -1;
-        auto col_at = [&](int o) { return o < n ? __ldg(cols + o) : 0; };
-        auto val_at = [&](int o) { return o < n ? __ldg(vals + o) : (T)0; };
-        auto rend_at = [&](int i) {
-            if (n <= 0) return 0;
-            const int64_t r = i + 1 <= nrow_left ? __ldg(rp + i + 1) : __ldg(rp + nrow_left);
-            return (int)imin64(r - e0, (int64_t)n);
-        };
-        EdgeCV<T> *win = s_win[warp * 2 + h];
-        int32_t *re = s_re[warp * 2 + h];
-        re[q] = rend_at(q);
-        re[16 + q] = rend_at(16 + q);
-        if (q < 2 * S) win[q] = EdgeCV<T>{col_at(q), val_at(q)};  // blocks 0 and 1
-        int cw = col_at(2 * S + q);               // block 2 (lanes q < S)
-        T vw = val_at(2 * S + q);
-        __syncwarp();
-        T xs[S][VEC];
-        T wsv[S];
-#pragma unroll
-        for (int t = 0; t < S; t++) {
-            const EdgeCV<T> e = win[t];
-            wsv[t] = e.v;
-            ldg_vec<T, VEC>(X + (int64_t)e.c * B, xs[t]);
-        }
-        int rw = 0;  // row-end ring holds local rows [rw, rw + 32)
-        int lr = 0;
-        int rstart = n > 0 ? (int)(__ldg(rp) - e0) : 0;
-        int rend = n > 0 ? re[0] : (1 << 30);  // idle worker: never emits
-        double acc[VEC];
-        T accs[VEC];
-#pragma unroll
-        for (int v = 0; v < VEC; v++) {
-            acc[v] = 0.0;
-            accs[v] = (T)0;
-        }
-        int b = 0;
-        for (int base = 0; base < n_max; base += S, b ^= 1) {
-            const EdgeCV<T> *nxt = win + (b ^ 1) * S;
-            int d = rend - base - 1;
-#pragma unroll
-            for (int t = 0; t < S; t++) {
-                if constexpr (sizeof(T) == 8) {
-#pragma unroll
-                    for (int v = 0; v < VEC; v++) acc[v] = fma((double)wsv[t], (double)xs[t][v], acc[v]);
-                } else {
-#pragma unroll
-                    for (int v = 0; v < VEC; v++) accs[v] = fmaf(wsv[t], xs[t][v], accs[v]);
-                }
-                if (d == t) {  // row emit (this half only)
-                    if constexpr (sizeof(T) == 4) {
-#pragma unroll
-                        for (int v = 0; v < VEC; v++) {
-                            acc[v] += (double)accs[v];
-                            accs[v] = (T)0;
-                        }
-                    }
-                    if (lr == cutA || lr == cutB) {
-                        double *dst = a.scratch + (int64_t)(lr == cutA ? wk.part0 : wk.part1) * B + slot0;
-#pragma unroll
-                        for (int v = 0; v < VEC; v++) dst[v] = acc[v];
-                    } else {
-                        T out[VEC];
-#pragma unroll
-                        for (int v = 0; v < VEC; v++) {
-                            out[v] = (T)(scale * acc[v]);
-                            if constexpr (SIDE == SIDE_V)
-                                np[v] += (((cmask >> v) & 1u) && out[v] > (T)0) ? rend - rstart : 0;
-                        }
-                        VecIO<T, VEC>::st(Y0 + (int64_t)lr * B, out);
-                    }
-#pragma unroll
-                    for (int v = 0; v < VEC; v++) acc[v] = 0.0;
-                    lr++;
-                    rstart = rend;
-                    rend = re[lr & 31];
-                    d = rend - base - 1;
-                }
-                const EdgeCV<T> e = nxt[t];
-                wsv[t] = e.v;
-                ldg_vec<T, VEC>(X + (int64_t)e.c * B, xs[t]);
-            }
-            if constexpr (sizeof(T) == 4) {
-#pragma unroll
-                for (int v = 0; v < VEC; v++) {
-                    acc[v] += (double)accs[v];
-                    accs[v] = (T)0;
-                }
-            }
-            // stage block (base/S + 2) into the window block read during this one,
-            // refill the row-end ring half that is behind lr
-            if (q < S) win[b * S + q] = EdgeCV<T>{cw, vw};
-            if (lr - rw >= 16) {
-                re[(rw + 32 + q) & 31] = rend_at(rw + 32 + q);
-                rw += 16;
-            }
-            cw = col_at(base + 3 * S + q);
-            vw = val_at(base + 3 * S + q);
-            __syncwarp();
-        }
-        const CutCtx<T> cx{a.scratch, a.cut_count, a.cuts, a.Y, a.indptr, scale};
-        for (int hh = 0; hh < 2; hh++) {
-            if (h == hh) {
-                if (cutA >= 0) {
-                    DVec<VEC> av;
-#pragma unroll
-                    for (int v = 0; v < VEC; v++) av.v[v] = a.scratch[(int64_t)wk.part0 * B + slot0 + v];
-                    const IVec<VEC> inc = pull_cut_half<B, T, VEC>(cx, wk.cut0, wk.part0, slot0, cmask, av, hmask);
-#pragma unroll
-                    for (int v = 0; v < VEC; v++) np_cut[v] += inc.v[v];
-                }
-                if (cutB >= 0) {
-                    DVec<VEC> av;
-#pragma unroll
-                    for (int v = 0; v < VEC; v++) av.v[v] = a.scratch[(int64_t)wk.part1 * B + slot0 + v];
-                    const IVec<VEC> inc = pull_cut_half<B, T, VEC>(cx, wk.cut1, wk.part1, slot0, cmask, av, hmask);
-#pragma unroll
-                    for (int v = 0; v < VEC; v++) np_cut[v] += inc.v[v];
-                }
-            }
-            __syncwarp();
-        }
-    }
-    if constexpr (SIDE == SIDE_V) {
-        // both halves cover the same slots: combine, half 0 writes the warp's row
-        const int n_rows_out = (n_workers + 1) / 2;
-#pragma unroll
-        for (int v = 0; v < VEC; v++) {
-            int64_t t = (int64_t)np[v] + np_cut[v];
-            t += __shfl_xor_sync(0xffffffffu, t, 16);
-            if (h == 0 && gw < n_rows_out) a.np_v[(int64_t)(slot0 + v) * n_rows_out + gw] = t;
-        }
-    }
-}
-
 template <int B, typename T, int SIDE>
 __global__ void __launch_bounds__(PULL_THREADS) k_pull_small(PullArgs<T> a) {
     pdl_begin();

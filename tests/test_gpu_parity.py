@@ -258,16 +258,11 @@ def test_scaled_configs_fp32(name):
 
 
 @pytest.mark.parametrize("variant", [
-    {"BH_PULL_SW": "0", "BH_PULL_HALF": "0"},   # lane-register windows (k_pull)
-    {"BH_PULL_SW": "0", "BH_PULL_HALF": "3"},   # half-warp workers (k_pull_half)
-    {"BH_PULL_SW": "1", "BH_PULL_HALF": "0"},   # shared-memory windows (k_pull_sw)
-    {"BH_PULL_SW": "1", "BH_PULL_HALF": "3"},   # half-warp workers, shared-memory windows (k_pull_swh)
-    {"BH_PULL_SW": "1", "BH_PULL_HALF": "1"},   # k_pull_swh on the U side, k_pull_sw on the V side
-    {"BH_PULL_SW": "1", "BH_FUSE_COMBINE": "1"},  # k_pull_sw with K1a fused into the U pull
-    {"BH_PULL_TMA": "1"},                        # TMA gather4 ring (k_pull_tma)
+    {},                      # default: one CUDA graph per batch (WHILE/IF conditional nodes)
+    {"BH_NO_GRAPH": "1"},    # eager launches, host-polled round loop
 ])
-def test_every_pull_kernel_variant(variant, monkeypatch):
-    """Each pull implementation (chosen when the engine is built) reproduces
+def test_every_engine_variant(variant, monkeypatch):
+    """Each engine variant (chosen when the engine is built) reproduces
     the golden fp64 scores / traces and the fp32 top-k on c2s."""
     for k, v in variant.items():
         monkeypatch.setenv(k, v)
