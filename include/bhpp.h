@@ -41,6 +41,12 @@ extern "C" {
 
 #define BH_DTYPE_F64 0 /* fp64 storage, fp64 arithmetic                       */
 #define BH_DTYPE_F32 1 /* fp32 storage, fp64 row accumulation and control     */
+/* OR into bh_graph_create's dtype: keep the caller's node order in the device
+ * store.  By default both sides are relabelled by descending degree inside the
+ * store (hub operand rows contiguous for L2 residency); every index crossing
+ * the ABI stays in the caller's numbering either way, and ties in top-k still
+ * break by the caller's index (bhpp_query.py:210). */
+#define BH_GRAPH_KEEP_ORDER 0x100
 
 #define BH_JOB_BHPP 0      /* ss_push -> pi_push -> power iteration -> combine */
 #define BH_JOB_SS_PUSH 1   /* backward with budget switch (push_engine.py:145) */
@@ -73,7 +79,8 @@ typedef struct bh_trace {
     int32_t tie_checks;  /* budget checks taken with A == U every round   */
     int32_t tie_broke;   /* 1 if the forward phase ended at such a check  */
     int32_t source;      /* U index of the query                          */
-    int32_t status;      /* 0 ok                                          */
+    int32_t status;      /* 0 ok, BH_EINVAL: source out of range (device  */
+                         /* pointer batches; the batch returns BH_EINVAL) */
 } bh_trace;
 
 typedef struct bh_query_params {

@@ -85,13 +85,25 @@ struct CutRow {
     int32_t pad;
 };
 
+// One CSR side of the device store.  Rows and columns are in the store's node
+// order: by default both sides are relabelled by descending degree (stable in
+// the caller's index), so the hub rows of every gathered operand sit in one
+// contiguous slab (L2 residency window) and a warp's consecutive rows share
+// hub columns.  Each row keeps the caller's edge order, so every row sum adds
+// the same terms in the same order as without relabelling.  perm / inv map
+// store index -> caller index and back (null when the caller's order is kept).
 struct Side {
     int64_t n_rows = 0;
     int64_t *indptr = nullptr;   // [n_rows + 1]
-    int32_t *indices = nullptr;  // [E] column (other side) index
+    int32_t *indices = nullptr;  // [E] column (other side) index, store order
     void *vals = nullptr;        // [E] T, w / ws(row)
     int32_t *deg = nullptr;      // [n_rows]
+    int32_t *perm = nullptr;     // [n_rows] store row -> caller row (null: identity)
+    int32_t *inv = nullptr;      // [n_rows] caller row -> store row (null: identity)
     std::vector<int64_t> h_indptr;  // host copy for the per-engine partition
+    std::vector<int32_t> h_perm, h_inv;  // host copies (empty: identity)
+    // caller -> store row (host)
+    int64_t to_store(int64_t r) const { return h_inv.empty() ? r : h_inv[(size_t)r]; }
 };
 
 }  // namespace bh
@@ -102,8 +114,9 @@ struct bh_graph {
     int64_t n_u = 0, n_v = 0, n_e = 0;
     bh::Side U;  // rows u: cols v, vals w/ws(u)   (u_step, bigraph.py:148-155)
     bh::Side V;  // rows v: cols u, vals w/ws(v)   (v_step, bigraph.py:157-164)
-    double *ws_u = nullptr;
-    double *inv_ws_u = nullptr;
+    double *ws_u = nullptr;      // store order
+    double *inv_ws_u = nullptr;  // store order
+    int relabeled = 0;           // rows / columns in degree order (Side::perm / inv)
     int64_t device_bytes = 0;
     std::mutex mu;
     void *engines = nullptr;  // engine cache (engine.cu)
@@ -148,10 +161,10 @@ struct Slot {
     int32_t op;        // op of the next round
     int32_t job;       // BH_JOB_*
     int32_t qidx;      // query index in the batch, -1 if idle
-    int32_t src;       // source / target U index
+    int32_t src;       // source / target U index (store order)
     int32_t phase;     // Phase
     int32_t term_b, term_f;
-    int32_t pad0;
+    int32_t src_orig;  // the same in the caller's numbering
     int32_t tie_checks, tie_skip, tie_broke;
     int32_t pi_t, pi_done;
     int32_t last_phase;   // BH_PHASE_* of the last executed push round (-1 none)
@@ -171,7 +184,7 @@ struct Slot {
 
 // Finished-query record written by K4 for the finalize kernels.
 struct Finish {
-    int32_t qidx, src, job, has_pi;
+    int32_t qidx, src, job, has_pi;  // src: caller's numbering
     double inv_ws_q;
     bh_trace trace;
 };
@@ -195,7 +208,7 @@ struct Control {
     int32_t n_fin;     // slots finishing this round
     int32_t rounds_active;  // rounds K4 processed with work in flight
     int32_t arrive;         // K4 block arrival counter (last block assigns queries)
-    int32_t error;          // set by K4's runaway guard
+    int32_t error;          // 1: K4's runaway guard; 2: a source index out of range
     int32_t fin_rounds;     // rounds with a finishing slot (K5 launched under the graph's IF node)
     int32_t fin_slots[256];
     int32_t free_slot[256];

@@ -15,8 +15,10 @@ struct ControlArgs {
     Finish *fin;
     Control *ctl;
     Partials part;
-    const int32_t *sources;   // [n_q]
+    const int32_t *sources;   // [n_q], caller's numbering
+    const int32_t *inv_u;     // caller -> store U index (null: identity)
     const int32_t *tie_skip;  // [n_q] or null
+    bh_trace *trace;          // [n_q]: written here only for a rejected source
     const double *ws_u;
     int64_t n_u;
     double alpha, lam, eps_b, eps_f;
@@ -40,11 +42,28 @@ __device__ __forceinline__ int32_t required_iterations_dev(double alpha, double 
     return x > 0 ? (int32_t)x : 0;
 }
 
-__device__ void slot_start(Slot &sl, const ControlArgs &a, int32_t q) {
+// Starts query q in a slot.  A source outside [0, n_u) (device-pointer batches
+// are not validated on the host) finishes at once with trace.status =
+// BH_EINVAL and flags the batch (ctl->error = 2, reported as BH_EINVAL).
+__device__ bool slot_start(Slot &sl, const ControlArgs &a, int32_t q) {
     sl = Slot{};
     sl.qidx = q;
     sl.job = a.job;
-    sl.src = a.sources[q];
+    const int32_t s0 = a.sources[q];
+    if (s0 < 0 || (int64_t)s0 >= a.n_u) {
+        bh_trace t{};
+        t.source = s0;
+        t.status = BH_EINVAL;
+        t.term_b = t.term_f = -1;
+        a.trace[q] = t;
+        atomicExch(&a.ctl->error, 2);
+        sl.qidx = -1;
+        sl.op = OP_IDLE;
+        sl.phase = PH_IDLE;
+        return false;
+    }
+    sl.src_orig = s0;
+    sl.src = a.inv_u ? a.inv_u[s0] : s0;
     sl.tie_skip = a.tie_skip ? a.tie_skip[q] : 0;
     sl.ws_q = a.ws_u[sl.src];
     sl.inv_ws_q = 1.0 / sl.ws_q;
@@ -72,11 +91,12 @@ __device__ void slot_start(Slot &sl, const ControlArgs &a, int32_t q) {
             sl.op = OP_BSEL_INIT;
             break;
     }
+    return true;
 }
 
 __device__ void slot_finish(Slot &sl, Finish &f, bool has_pi) {
     f.qidx = sl.qidx;
-    f.src = sl.src;
+    f.src = sl.src_orig;
     f.job = sl.job;
     f.has_pi = has_pi;
     f.inv_ws_q = sl.inv_ws_q;
@@ -92,7 +112,7 @@ __device__ void slot_finish(Slot &sl, Finish &f, bool has_pi) {
     t.term_f = sl.term_f;
     t.tie_checks = sl.tie_checks;
     t.tie_broke = sl.tie_broke;
-    t.source = sl.src;
+    t.source = sl.src_orig;
     t.status = 0;
     sl.phase = PH_DONE;
     sl.op = OP_IDLE;

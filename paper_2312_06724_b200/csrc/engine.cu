@@ -53,18 +53,41 @@ static X *dalloc(size_t count) {
 
 // ---------------------------------------------------------------------------
 // small utility kernels
+// Slot column s of a [n][B] state array to / from a caller-order vector
+// (perm: store -> caller index, null for the identity).
 template <typename T>
-__global__ void k_col_get(const T *X, int B, int s, int64_t n, double *out) {
+__global__ void k_col_get(const T *X, int B, int s, int64_t n, const int32_t *perm, double *out) {
     for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x)
-        out[u] = (double)X[u * B + s];
+        out[perm ? perm[u] : u] = (double)X[u * B + s];
 }
 template <typename T>
-__global__ void k_col_set(T *X, int B, int s, int64_t n, const double *in) {
+__global__ void k_col_set(T *X, int B, int s, int64_t n, const int32_t *perm, const double *in) {
     for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x)
-        X[u * B + s] = (T)in[u];
+        X[u * B + s] = (T)in[perm ? perm[u] : u];
 }
 
-// Launch a round kernel with programmatic stream serialization (PDL).
+// Launch a round kernel with programmatic stream serialization (PDL) and,
+// optionally, an L2 access-policy window (persisting hub slab of the operand).
+template <typename... KArgs, typename... Args>
+static void launch_pdl_win(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t st,
+                           const cudaAccessPolicyWindow *win, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (win && win->num_bytes > 0) {
+        attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[1].val.accessPolicyWindow = *win;
+        cfg.numAttrs = 2;
+    }
+    BH_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+}
 template <typename... KArgs, typename... Args>
 static void launch_pdl(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t st, Args... args) {
     cudaLaunchConfig_t cfg = {};
@@ -210,6 +233,10 @@ struct Engine final : EngineBase {
     int32_t *chunk_done = nullptr;
     std::vector<cudaEvent_t> evpool;
     SidePlan plan_v, plan_u;
+    // L2 residency of the gathered operands' hub slabs (store rows [0, h) of P for
+    // the V pull, of XV for the U pull; degree-ordered store): empty windows
+    // unless the operands outgrow L2 (BH_L2_PERSIST_MB overrides the carve-out)
+    cudaAccessPolicyWindow win_v{}, win_u{};
     // one batch = one CUDA graph: a WHILE node around one round, condition set by K4
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t graph_exec = nullptr;
@@ -274,6 +301,7 @@ struct Engine final : EngineBase {
         BH_CUDA(cudaMemset(ctl, 0, sizeof(Control)));
         int sms = 148;
         BH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
+        setup_l2_windows(nu, nv);
         for (int side = 0; side < 2; side++) {
             PullFn fn = pull_kernel(side);
             int occ = 1;
@@ -318,6 +346,38 @@ struct Engine final : EngineBase {
         chunk_done = dalloc<int32_t>(MAX_B);
         BH_CUDA(cudaMemset(chunk_done, 0, MAX_B * sizeof(int32_t)));
     }
+
+    void setup_l2_windows(int64_t nu, int64_t nv) {
+        int l2 = 0, maxp = 0, maxwin = 0;
+        BH_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, g->device));
+        BH_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, g->device));
+        BH_CUDA(cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, g->device));
+        const double row = (double)B * sizeof(T);
+        const double operands = row * (double)(nu + nv);
+        double mb = operands > 0.5 * l2 ? 0.5 * l2 / 1048576.0 : 0.0;  // default: half of L2 when outgrown
+        if (const char *m = getenv("BH_L2_PERSIST_MB")) mb = atof(m);
+        if (!g->relabeled || mb <= 0 || maxp <= 0 || maxwin <= 0) return;
+        const size_t carve = std::min<size_t>((size_t)maxp, (size_t)(mb * 1048576.0));
+        // the carve-out is shared by the two windows (one per pull), in proportion
+        // to the operands' sizes but at most their whole size
+        const double fu = (double)nu / (double)(nu + nv);
+        auto make = [&](cudaAccessPolicyWindow &w, void *base, int64_t rows, double share) {
+            const size_t full = (size_t)(row * (double)rows);
+            size_t bytes = std::min<size_t>({full, (size_t)maxwin, (size_t)(share * (double)carve)});
+            w.base_ptr = base;
+            w.num_bytes = bytes;
+            w.hitRatio = 1.0f;
+            w.hitProp = cudaAccessPropertyPersisting;
+            w.missProp = cudaAccessPropertyStreaming;
+        };
+        make(win_v, P, nu, fu);
+        make(win_u, XV, nv, 1.0 - fu);
+        size_t cur = 0;
+        BH_CUDA(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+        if (cur < carve) BH_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve));
+        l2_carve = carve;
+    }
+    size_t l2_carve = 0;
 
     ~Engine() override {
         cudaFree(R); cudaFree(P); cudaFree(Y); cudaFree(XV); cudaFree(EST); cudaFree(OUTS);
@@ -376,7 +436,8 @@ struct Engine final : EngineBase {
     }
 
     void launch_pull(int side, const PullArgs<T> &a, cudaStream_t st) {
-        launch_pdl(pull_kernel(side), side == SIDE_V ? plan_v.grid : plan_u.grid, PULL_THREADS, 0, st, a);
+        launch_pdl_win(pull_kernel(side), side == SIDE_V ? plan_v.grid : plan_u.grid, PULL_THREADS, 0, st,
+                       side == SIDE_V ? &win_v : &win_u, a);
     }
 
     // One round: K5 (the slots K4 finished last round) | K1 K2 K3 K1a | K4.  In the
@@ -395,6 +456,7 @@ struct Engine final : EngineBase {
         ea.ws_u = g->ws_u;
         ea.inv_ws_u = g->inv_ws_u;
         ea.x0 = rs.x0;
+        ea.perm_u = g->U.perm;
         ea.slots = slots;
         ea.active = &ctl->active;
         ea.part = part;
@@ -523,6 +585,8 @@ struct Engine final : EngineBase {
         ca.ctl = ctl;
         ca.part = part;
         ca.sources = rs.sources;
+        ca.inv_u = g->U.inv;
+        ca.trace = rs.trace;
         ca.tie_skip = rs.tie;
         ca.ws_u = g->ws_u;
         ca.n_u = g->n_u;
@@ -542,8 +606,8 @@ struct Engine final : EngineBase {
         BH_CUDA(cudaGetLastError());
         ca.first = 0;
         if (rs.job == BH_JOB_PI_PUSH) {  // seed ledger into slot 0 (query 0 -> slot 0)
-            k_col_set<T><<<grid1d(g->n_u), 256, 0, st>>>(R, B, 0, g->n_u, rs.ledger_r);
-            k_col_set<T><<<grid1d(g->n_u), 256, 0, st>>>(EST, B, 0, g->n_u, rs.ledger_est);
+            k_col_set<T><<<grid1d(g->n_u), 256, 0, st>>>(R, B, 0, g->n_u, g->U.perm, rs.ledger_r);
+            k_col_set<T><<<grid1d(g->n_u), 256, 0, st>>>(EST, B, 0, g->n_u, g->U.perm, rs.ledger_est);
             count_launch(2);
         }
 
@@ -558,6 +622,7 @@ struct Engine final : EngineBase {
         fa.EST = EST;
         fa.P = P;
         fa.ws_u = g->ws_u;
+        fa.perm_u = g->U.perm;
         fa.alpha = rs.alpha;
         fa.fin = fins;
         fa.ctl = ctl;
@@ -611,6 +676,7 @@ struct Engine final : EngineBase {
             BH_CUDA(cudaMemcpyAsync(h_ctl, ctl, sizeof(Control), cudaMemcpyDeviceToHost, st));
             BH_CUDA(cudaStreamSynchronize(st));
             if (!h_ctl->active && h_ctl->n_fin == 0) {
+                check_error();
                 stats.rounds = h_ctl->rounds_active;
                 if (prof) collect_profile(round);
                 return;
@@ -621,12 +687,17 @@ struct Engine final : EngineBase {
 
     cudaStream_t pending = nullptr;
 
+    void check_error() const {
+        if (h_ctl->error == 2) throw InvalidArg("node index out of range");
+        if (h_ctl->error) throw CudaError("query batch did not terminate");
+    }
+
     void finish() override {
         if (!pending) return;
         cudaStream_t st = pending;
         pending = nullptr;
         BH_CUDA(cudaStreamSynchronize(st));
-        if (h_ctl->error) throw CudaError("query batch did not terminate");
+        check_error();
         stats.rounds = h_ctl->rounds_active;
         // graph path: K5 only in the rounds where a slot finished (IF node)
         const int64_t n_launch = (launches_per_round() - 1) * (int64_t)h_ctl->rounds_active + h_ctl->fin_rounds;
@@ -635,8 +706,8 @@ struct Engine final : EngineBase {
     }
 
     void read_ledger(int s, double *r_dev, double *est_dev, cudaStream_t st) override {
-        k_col_get<T><<<grid1d(g->n_u), 256, 0, st>>>(R, B, s, g->n_u, r_dev);
-        k_col_get<T><<<grid1d(g->n_u), 256, 0, st>>>(EST, B, s, g->n_u, est_dev);
+        k_col_get<T><<<grid1d(g->n_u), 256, 0, st>>>(R, B, s, g->n_u, g->U.perm, r_dev);
+        k_col_get<T><<<grid1d(g->n_u), 256, 0, st>>>(EST, B, s, g->n_u, g->U.perm, est_dev);
         count_launch(2);
         BH_CUDA(cudaGetLastError());
     }

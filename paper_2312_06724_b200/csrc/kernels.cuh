@@ -149,7 +149,8 @@ struct ElemArgs {
     const int32_t *deg_u;
     const double *ws_u;
     const double *inv_ws_u;
-    const double *x0;  // BH_JOB_POWER start vectors [n_q][n_u]
+    const double *x0;  // BH_JOB_POWER start vectors [n_q][n_u], caller's numbering
+    const int32_t *perm_u;  // store -> caller U index (null: identity)
     const Slot *slots;
     const int32_t *active;
     Partials part;
@@ -260,7 +261,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, MINB) k_push(ElemArgs<T> a) {
                     // start / ws for a raw power iteration (push_engine.py:112 on a = acc / ws)
                     p = (T)((double)rv[v] * sc.ysc[c]);
                     if (RARE && ((m_x0 >> v) & 1u)) {
-                        p = (T)(a.x0[(int64_t)sc.qidx[j0 + v] * a.n_u + u] * iws);
+                        p = (T)(a.x0[(int64_t)sc.qidx[j0 + v] * a.n_u + (a.perm_u ? a.perm_u[u] : u)] * iws);
                         rv[v] = p;
                     }
                 }

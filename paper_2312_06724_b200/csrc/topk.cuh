@@ -237,11 +237,12 @@ struct FinalArgs {
     const T *EST;
     const T *P;
     const double *ws_u;
+    const int32_t *perm_u;  // store -> caller U index (null: identity)
     double alpha;
     const Finish *fin;
     const Control *ctl;
-    double *outs;        // [B][n_u] per-slot score rows
-    double *out_scores;  // [n_q][n_u] or null
+    double *outs;        // [B][n_u] per-slot score rows (store order)
+    double *out_scores;  // [n_q][n_u] or null (caller's order)
     uint64_t *cand_key;  // [B][n_chunks][k]
     int64_t *cand_idx;
     int32_t *topk_idx;   // [n_q][k]
@@ -250,9 +251,12 @@ struct FinalArgs {
     int32_t *chunk_done; // [B] chunks finished per finishing slot (zero between rounds)
 };
 
+// Per-slot score row the chunk select reads: the caller's output row directly
+// when the store keeps the caller's order, else the slot's OUTS row (store
+// order; the caller's row is written through perm_u beside it).
 template <typename T>
 __device__ __forceinline__ double *score_row(const FinalArgs<T> &a, int s, const Finish &f) {
-    return a.want_scores ? a.out_scores + (int64_t)f.qidx * a.n_u : a.outs + (int64_t)s * a.n_u;
+    return a.want_scores && !a.perm_u ? a.out_scores + (int64_t)f.qidx * a.n_u : a.outs + (int64_t)s * a.n_u;
 }
 
 // Merge the chunk candidates of finished slot s, sort, write top-k + trace.
@@ -338,14 +342,16 @@ __global__ void __launch_bounds__(TOPK_THREADS) k_finalize(FinalArgs<T> a) {
                         if (f.job == BH_JOB_BHPP) v = v + est;                      // + backward est
                     }
                     dst[u] = v;
+                    if (a.want_scores && a.perm_u) a.out_scores[(int64_t)f.qidx * a.n_u + a.perm_u[u]] = v;
                 }
             }
             if (a.k > 0) {
                 __syncthreads();
                 const int64_t excl = (a.exclude && f.job == BH_JOB_BHPP) ? f.src : -1;
+                // candidates carry the caller's index: ties break by it (bhpp_query.py:210)
                 auto acc = [&](int64_t i, uint64_t &kk, int64_t &ii) -> bool {
-                    ii = u0 + i;
-                    kk = order_key(dst[ii]);
+                    kk = order_key(dst[u0 + i]);
+                    ii = a.perm_u ? (int64_t)a.perm_u[u0 + i] : u0 + i;
                     return ii != excl;
                 };
                 uint64_t *ck = a.cand_key + ((int64_t)s * a.n_chunks + c) * a.k;

@@ -72,21 +72,43 @@ X *dcopy(const X *h, size_t n) {
 
 }  // namespace
 
+// Per-slot tables of one side (caller's CSR order) into the store's row order:
+// a relabelled store row keeps its caller row's edge order, so each row's slots
+// move as one block and the local alias offsets stay valid.
+static void to_store_order(const Side &s, const double *prob, const int64_t *alias, std::vector<double> &p,
+                           std::vector<int32_t> &al) {
+    const int64_t E = s.h_indptr.back();
+    p.resize((size_t)E);
+    al.resize((size_t)E);
+    std::vector<int64_t> cip;  // caller's row offsets
+    if (!s.h_perm.empty()) {
+        cip.assign((size_t)s.n_rows + 1, 0);
+        for (int64_t i = 0; i < s.n_rows; i++) cip[(size_t)s.h_perm[i] + 1] = s.h_indptr[i + 1] - s.h_indptr[i];
+        for (int64_t r = 0; r < s.n_rows; r++) cip[r + 1] += cip[r];
+    }
+    for (int64_t i = 0; i < s.n_rows; i++) {
+        const int64_t o = s.h_perm.empty() ? s.h_indptr[i] : cip[(size_t)s.h_perm[i]];
+        for (int64_t k = 0, n = s.h_indptr[i]; n < s.h_indptr[i + 1]; k++, n++) {
+            p[(size_t)n] = prob[o + k];
+            al[(size_t)n] = (int32_t)alias[o + k];
+        }
+    }
+}
+
 bh_alias *alias_create(bh_graph *g, const double *u_prob, const int64_t *u_alias, const double *v_prob,
                        const int64_t *v_alias) {
     BH_CUDA(cudaSetDevice(g->device));
     const int64_t E = g->n_e;
-    std::vector<int32_t> ua((size_t)E), va((size_t)E);
-    for (int64_t e = 0; e < E; e++) {
-        ua[e] = (int32_t)u_alias[e];
-        va[e] = (int32_t)v_alias[e];
-    }
+    std::vector<double> up, vp;
+    std::vector<int32_t> ua, va;
+    to_store_order(g->U, u_prob, u_alias, up, ua);
+    to_store_order(g->V, v_prob, v_alias, vp, va);
     auto *a = new bh_alias();
     a->g = g;
     a->device = g->device;
     try {
-        a->u_prob = dcopy(u_prob, E);
-        a->v_prob = dcopy(v_prob, E);
+        a->u_prob = dcopy(up.data(), E);
+        a->v_prob = dcopy(vp.data(), E);
         a->u_alias = dcopy(ua.data(), E);
         a->v_alias = dcopy(va.data(), E);
     } catch (...) {
@@ -108,7 +130,7 @@ void mc_walks(const bh_alias *al, int64_t source, double alpha, int64_t first, i
     WalkSide vs{g->V.indptr, g->V.indices, al->v_prob, al->v_alias};
     const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
     if (n > 0) {
-        k_mc_walks<<<grid, 256>>>(us, vs, source, alpha, first, n, seed, dc);
+        k_mc_walks<<<grid, 256>>>(us, vs, g->U.to_store(source), alpha, first, n, seed, dc);
         count_launch();
     }
     cudaError_t e = cudaGetLastError();
@@ -116,7 +138,7 @@ void mc_walks(const bh_alias *al, int64_t source, double alpha, int64_t first, i
     if (e == cudaSuccess) e = cudaMemcpy(hc.data(), dc, g->n_u * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     cudaFree(dc);
     BH_CUDA(e);
-    for (int64_t u = 0; u < g->n_u; u++) counts_host[u] += (int64_t)hc[u];
+    for (int64_t u = 0; u < g->n_u; u++) counts_host[g->U.h_perm.empty() ? u : g->U.h_perm[u]] += (int64_t)hc[u];
 }
 
 }  // namespace bh

@@ -74,11 +74,73 @@ def _draw(rng: np.random.Generator, cdf: np.ndarray, size: int) -> np.ndarray:
     return np.searchsorted(cdf, rng.random(size), side="right").astype(np.int64)
 
 
+class _HostOps:
+    """numpy: inverse-CDF draws and first-occurrence dedupe."""
+
+    def draw(self, rng, cdf, size):
+        return _draw(rng, cdf, size)
+
+    def first_unique(self, keys):
+        _, first = np.unique(keys, return_index=True)
+        return keys[np.sort(first)]
+
+
+class _TorchOps:
+    """The same two operations on a torch device (the uniforms still come from
+    the numpy generator, so the graph is bit-identical to the host path):
+    ``searchsorted(cdf, x, right=True)`` is an exact comparison on the same
+    doubles, and a stable sort keeps the first occurrence of every key first in
+    its run.  Test/bench input generation only (c3/c4 in seconds, not minutes)."""
+
+    def __init__(self, device):
+        import torch
+
+        self.torch = torch
+        self.dev = torch.device(device)
+        self._cdf = {}
+
+    def draw(self, rng, cdf, size):
+        t = self.torch
+        key = id(cdf)
+        if key not in self._cdf:
+            self._cdf[key] = (cdf, t.from_numpy(cdf).to(self.dev))
+        dc = self._cdf[key][1]
+        out = np.empty(size, dtype=np.int64)
+        step = 1 << 26
+        for i in range(0, size, step):  # bounded device memory; same draws, same order
+            x = t.from_numpy(rng.random(min(step, size - i))).to(self.dev)
+            out[i:i + x.numel()] = t.searchsorted(dc, x, right=True).cpu().numpy()
+        return out
+
+    def first_unique(self, keys):
+        t = self.torch
+        k = t.from_numpy(keys).to(self.dev)
+        sk, order = t.sort(k, stable=True)
+        head = t.ones_like(sk, dtype=t.bool)
+        head[1:] = sk[1:] != sk[:-1]
+        keep = t.zeros_like(head)
+        keep[order[head]] = True
+        out = k[keep].cpu().numpy()
+        del k, sk, order, head, keep
+        return out
+
+
+def _ops(device):
+    if device is None:
+        return _HostOps()
+    return _TorchOps(device)
+
+
 def chung_lu_edges(u_count: int, v_count: int, edge_count: int, beta_u: float, beta_v: float,
-                   weights: str, seed: int, max_deg_v: int | None = None, max_deg_u: int | None = None):
-    """(eu, ev, ew) with exactly ``edge_count`` distinct pairs, every node covered."""
+                   weights: str, seed: int, max_deg_v: int | None = None, max_deg_u: int | None = None,
+                   device=None):
+    """(eu, ev, ew) with exactly ``edge_count`` distinct pairs, every node covered.
+
+    ``device`` (a torch device such as ``"cuda:0"``) runs the draws' inverse-CDF
+    lookups and the dedupe there; the result is identical to the host path."""
     if edge_count < max(u_count, v_count) or edge_count > u_count * v_count:
         raise ValueError("edge_count must lie in [max(|U|,|V|), |U||V|]")
+    ops = _ops(device)
     rng = substream(seed, "chung-lu", u_count, v_count, edge_count)
     pu = _expected_shares(u_count, beta_u, edge_count, max_deg_u)
     pv = _expected_shares(v_count, beta_v, edge_count, max_deg_v)
@@ -87,19 +149,16 @@ def chung_lu_edges(u_count: int, v_count: int, edge_count: int, beta_u: float, b
     cv = np.cumsum(pv)
     cv /= cv[-1]
     m = max(u_count, v_count)
-    us = np.concatenate([rng.permutation(u_count), _draw(rng, cu, m - u_count)])
-    vs = np.concatenate([rng.permutation(v_count), _draw(rng, cv, m - v_count)])
+    us = np.concatenate([rng.permutation(u_count), ops.draw(rng, cu, m - u_count)])
+    vs = np.concatenate([rng.permutation(v_count), ops.draw(rng, cv, m - v_count)])
     rng.shuffle(vs)
-    keys = us * v_count + vs
-    _, first = np.unique(keys, return_index=True)
-    keys = keys[np.sort(first)]
+    keys = ops.first_unique(us * v_count + vs)
     while keys.size < edge_count:
         need = edge_count - keys.size
         n = int(need * 1.25) + 1024
-        cand = _draw(rng, cu, n) * v_count + _draw(rng, cv, n)
-        allk = np.concatenate([keys, cand])
-        _, first = np.unique(allk, return_index=True)
-        keys = allk[np.sort(first)][:edge_count]
+        cand = ops.draw(rng, cu, n) * v_count
+        cand += ops.draw(rng, cv, n)
+        keys = ops.first_unique(np.concatenate([keys, cand]))[:edge_count]
     eu = keys // v_count
     ev = keys % v_count
     if weights == "unit":
@@ -112,11 +171,13 @@ def chung_lu_edges(u_count: int, v_count: int, edge_count: int, beta_u: float, b
 
 
 def make_graph(cfg: GraphConfig | str, seed: int | None = None, device: int | None = None) -> BipartiteGraph:
-    """The config's graph; ``device`` canonicalises the CSR on that GPU."""
+    """The config's graph; ``device`` also generates the edges (draw lookups,
+    dedupe; identical graph) and canonicalises the CSR on that GPU."""
     if isinstance(cfg, str):
         cfg = CONFIGS[cfg]
     eu, ev, ew = chung_lu_edges(cfg.u_count, cfg.v_count, cfg.edge_count, cfg.beta_u, cfg.beta_v,
-                                cfg.weights, cfg.seed if seed is None else seed, cfg.max_deg_v)
+                                cfg.weights, cfg.seed if seed is None else seed, cfg.max_deg_v,
+                                device=None if device is None else f"cuda:{device}")
     return BipartiteGraph.from_arrays(cfg.u_count, cfg.v_count, eu, ev, ew, device=device)
 
 
