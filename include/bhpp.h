@@ -192,6 +192,12 @@ void bh_edge_list_free(bh_edge_list *el);
  * alpha before every step, else U -> V -> U with alias draws.  Walk i uses the
  * Philox4x32-10 stream (seed, i).  Destroy the tables before their graph. */
 typedef struct bh_alias bh_alias;
+/* build_alias (baselines.py:41-77) for one CSR side on `device`: per-slot prob
+ * and local alias offsets, bit-identical to the reference's tables (Vose
+ * pairing per row in the reference's order, numpy's pairwise row sum).  Host
+ * pointers in and out; indptr [n_rows + 1], weights / prob / alias [n_e]. */
+int bh_alias_build(int64_t n_rows, int64_t n_e, const int64_t *indptr, const double *weights, int32_t device,
+                   double *prob, int64_t *alias);
 int bh_alias_create(bh_graph *g, const double *u_prob, const int64_t *u_alias, const double *v_prob,
                     const int64_t *v_alias, bh_alias **out);
 int bh_monte_carlo(const bh_alias *a, int64_t source, double alpha, int64_t first, int64_t n, uint64_t seed,

@@ -32,7 +32,7 @@ EXPORTS = (
     "bh_power_iteration", "bh_topk", "bh_last_error", "bh_version", "bh_kernel_launches",
     "bh_set_profiling", "bh_last_run_stats", "bh_csr_build", "bh_query_wait", "bh_stream_gate",
     "bh_edge_list_parse", "bh_edge_list_sizes", "bh_edge_list_export", "bh_edge_list_free",
-    "bh_alias_create", "bh_monte_carlo", "bh_alias_destroy",
+    "bh_alias_create", "bh_monte_carlo", "bh_alias_destroy", "bh_alias_build",
 )
 QUERY_ASYNC = 1
 
@@ -132,6 +132,8 @@ def lib():
         L.bh_edge_list_export.argtypes = [P, C.c_char_p, P, C.c_char_p, P, P, P, P]
         L.bh_edge_list_free.restype = None
         L.bh_edge_list_free.argtypes = [P]
+        L.bh_alias_build.restype = C.c_int
+        L.bh_alias_build.argtypes = [C.c_int64, C.c_int64, P, P, C.c_int32, P, P]
         L.bh_alias_create.restype = C.c_int
         L.bh_alias_create.argtypes = [P, P, P, P, P, C.POINTER(C.c_void_p)]
         L.bh_monte_carlo.restype = C.c_int

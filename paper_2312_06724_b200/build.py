@@ -18,7 +18,7 @@ CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libbhpp.so"
 INCLUDE = PKG.parent / "include"
-SOURCES = ["engine.cu", "graph_store.cu", "csr_build.cu", "edge_list.cpp", "walks.cu"]
+SOURCES = ["engine.cu", "graph_store.cu", "csr_build.cu", "edge_list.cpp", "walks.cu", "alias.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

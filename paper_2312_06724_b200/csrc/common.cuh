@@ -49,6 +49,8 @@ EdgeListResult parse_edge_list(const char *buf, int64_t len, const char *delim, 
 // walks.cu: Monte-Carlo restart walks over the device graph (MCSP forward half)
 bh_alias *alias_create(bh_graph *g, const double *u_prob, const int64_t *u_alias, const double *v_prob,
                        const int64_t *v_alias);
+void alias_build(int64_t n_rows, int64_t n_e, const int64_t *indptr, const double *weights, int device,
+                 double *prob_out, int64_t *alias_out);
 void mc_walks(const bh_alias *al, int64_t source, double alpha, int64_t first, int64_t n, uint64_t seed,
               int64_t *counts_host);
 

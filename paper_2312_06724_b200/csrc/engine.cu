@@ -784,13 +784,18 @@ static int auto_slots(bh_graph *g, int64_t n_q) {
     // an engine of that width exists: no device-memory query (cudaMemGetInfo goes to
     // the driver and was measured stalling a call by up to 100 ms on a busy host)
     if (cache_of(g).by_b.count(b)) return b;
-    // keep the per-slot state within a fraction of device memory
+    // keep the per-slot state within a fraction of device memory: step down
+    // through the engine widths, never below one slot
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+        static const int widths[] = {128, 64, 32, 16, 4, 1};
         const int s = g->dtype == BH_DTYPE_F32 ? 4 : 8;
-        while (b > 1 && (double)b * (g->n_u * (2.0 * s + 16) + g->n_v * (double)s) > 0.6 * free_b)
-            b = b == 128 ? 64 : b / 4;
-        if (b == 2 || b == 8) b = b == 2 ? 1 : 4;
+        const double per_slot = (double)g->n_u * (5.0 * s + 8) + (double)g->n_v * s;  // R P Y EST XV + OUTS
+        for (int w : widths) {
+            if (w > b) continue;
+            b = w;
+            if ((double)w * per_slot <= 0.6 * (double)free_b) break;
+        }
     }
     return b;
 }
@@ -943,6 +948,15 @@ int bh_alias_create(bh_graph *g, const double *u_prob, const int64_t *u_alias, c
         if (!g || !u_prob || !u_alias || !v_prob || !v_alias || !out) throw InvalidArg("null argument");
         std::lock_guard<std::mutex> lock(g->mu);
         *out = bh::alias_create(g, u_prob, u_alias, v_prob, v_alias);
+    });
+}
+
+int bh_alias_build(int64_t n_rows, int64_t n_e, const int64_t *indptr, const double *weights, int32_t device,
+                   double *prob, int64_t *alias) {
+    return guarded([&] {
+        if (!indptr || !weights || !prob || !alias) throw InvalidArg("null argument");
+        if (n_rows <= 0 || n_e < 0 || indptr[0] != 0 || indptr[n_rows] != n_e) throw InvalidArg("corrupt CSR offsets");
+        if (n_e > 0) alias_build(n_rows, n_e, indptr, weights, device, prob, alias);
     });
 }
 

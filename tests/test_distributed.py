@@ -63,8 +63,9 @@ def _worker(rank, world, port, sources, out_path):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n_src", [7, 12])
+@pytest.mark.parametrize("n_src", [1, 7, 12])
 def test_sharded_gather_restores_source_order(tmp_path, n_src):
+    """Includes fewer sources than ranks (rank 1 has an empty shard)."""
     sources = list(np.random.default_rng(n_src).choice(1000, n_src, replace=False))
     out = tmp_path / "res.npz"
     mp.spawn(_worker, args=(2, _free_port(), sources, str(out)), nprocs=2, join=True)
@@ -75,6 +76,50 @@ def test_sharded_gather_restores_source_order(tmp_path, n_src):
     tr = got["tr"].view(_capi.TRACE_DTYPE)
     np.testing.assert_array_equal(tr["source"], np.asarray(sources, dtype=np.int32))
     np.testing.assert_array_equal(tr["n_p_f"], ref.traces["n_p_f"])
+
+
+def _packed_worker(rank, world, port, n_total, k, out_path):
+    """The device path's driver (sharded_run + PackedShard) with a local_fn that
+    writes each query's rows straight into the packed send buffer, as K5 does."""
+    import torch
+
+    from paper_2312_06724_b200.distributed import sharded_run
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        def local(lo, count, packed):
+            q = torch.arange(lo, n_total, world, dtype=torch.int64)[:count]
+            packed.idx[:count] = (q[:, None] * 100 + torch.arange(k)[None, :]).to(torch.int32)
+            packed.score[:count] = q[:, None].double() + torch.arange(k)[None, :].double() / 1000
+            packed.trace[:count] = (q[:, None] % 251).to(torch.uint8)
+
+        gi, gs, gt = sharded_run(n_total, k, rank, world, local)
+        if rank == 0:
+            np.savez(out_path, idx=gi.numpy(), sc=gs.numpy(), tr=gt.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_total", [0, 1, 5, 8])
+def test_packed_all_gather_restores_source_order(tmp_path, n_total):
+    k = 3
+    out = tmp_path / "packed.npz"
+    mp.spawn(_packed_worker, args=(2, _free_port(), n_total, k, str(out)), nprocs=2, join=True)
+    got = np.load(out)
+    q = np.arange(n_total)
+    np.testing.assert_array_equal(got["idx"], (q[:, None] * 100 + np.arange(k)[None, :]).astype(np.int32))
+    np.testing.assert_array_equal(got["sc"], q[:, None] + np.arange(k)[None, :] / 1000)
+    assert got["tr"].shape == (n_total, _capi.TRACE_DTYPE.itemsize)
+    np.testing.assert_array_equal(got["tr"], np.broadcast_to((q % 251)[:, None], got["tr"].shape).astype(np.uint8))
+
+
+def test_source_order_index():
+    from paper_2312_06724_b200.distributed import per_rank, source_order_index
+
+    assert per_rank(7, 2) == 4 and per_rank(0, 3) == 0
+    # 7 queries over 2 ranks: rank 0 holds 0,2,4,6 (rows 0..3), rank 1 holds 1,3,5 (rows 4..6)
+    assert list(source_order_index(7, 2)) == [0, 4, 1, 5, 2, 6, 3]
 
 
 def test_shard_interleaves():

@@ -2,11 +2,13 @@
 oracle composition, MCSP / monte_carlo against their error bounds."""
 
 import time
+from pathlib import Path
 
 import numpy as np
 import pytest
 
 import paper_2312_06724_b200 as bh
+from paper_2312_06724_b200 import BipartiteGraph
 from golden_io import config_graph, load
 from oracle import cpu_oracle as O
 
@@ -76,3 +78,17 @@ def test_similarity_rows_batched_prefetch_matches_single_queries():
     assert row(5) is first  # memoised
     extra = row(3)          # uncached node: a batch of one
     np.testing.assert_allclose(extra, bh.bhpp_query(g, meta, 3, 1e-6).scores, atol=1e-12, rtol=0)
+
+
+def test_build_alias_matches_reference_tables():
+    """build_alias (baselines.py:41-77) on the device (bh_alias_build): identical tables on the config-1
+    graph and on a non-integer-weight graph (Vose pairing order, roundoff leftovers)."""
+    d = np.load(Path(__file__).resolve().parent / "golden" / "alias.npz")
+    g1 = config_graph("c1")
+    g2 = BipartiteGraph([f"a{i}" for i in range(60)], [f"b{i}" for i in range(int(d["w_ev"].max()) + 1)],
+                        d["w_eu"], d["w_ev"], d["w_ew"])
+    for name, g in (("c1", g1), ("w", g2)):
+        t = bh.build_alias(g)
+        for side in ("u", "v"):
+            np.testing.assert_array_equal(getattr(t, f"{side}_prob"), d[f"{name}_{side}_prob"])
+            np.testing.assert_array_equal(getattr(t, f"{side}_alias"), d[f"{name}_{side}_alias"])

@@ -202,20 +202,6 @@ def test_operator_views_match_reference_definitions():
         g.v_id("nope")
 
 
-def test_build_alias_matches_reference_tables():
-    """build_alias (baselines.py:42-83) restated: identical tables on the config-1
-    graph and on a non-integer-weight graph (Vose pairing order, roundoff leftovers)."""
-    d = np.load(Path(__file__).resolve().parent / "golden" / "alias.npz")
-    g1 = config_graph("c1")
-    g2 = BipartiteGraph([f"a{i}" for i in range(60)], [f"b{i}" for i in range(int(d["w_ev"].max()) + 1)],
-                        d["w_eu"], d["w_ev"], d["w_ew"])
-    for name, g in (("c1", g1), ("w", g2)):
-        t = bh.build_alias(g)
-        for side in ("u", "v"):
-            np.testing.assert_array_equal(getattr(t, f"{side}_prob"), d[f"{name}_{side}_prob"])
-            np.testing.assert_array_equal(getattr(t, f"{side}_alias"), d[f"{name}_{side}_alias"])
-
-
 def test_mc_walk_count():
     assert bh.mc_walk_count(0.1, 1e-6, 1000) == 4283  # ceil(2 (1 + 0.1/3) ln(1e9) / 0.01)
     assert bh.mc_walk_count(10.0, 0.5, 1) == 1
