@@ -249,12 +249,28 @@ struct Engine final : EngineBase {
     // measured at c2 on B200 (profiles/r01_pull_variants.md): fp32 K1 one node
     // per thread at 4 blocks/SM, K1a software-pipelined at 3 blocks/SM; fp64 two
     // nodes per thread at 2 blocks/SM.
+    // When the state outgrows L2 (HBM regime, c3/c4) the same kernels need more
+    // bytes in flight per SM to cover DRAM latency: several nodes per thread.
     using ElemFn = void (*)(ElemArgs<T>);
-    static ElemFn push_kernel() {
+    bool hbm = false;   // set in the constructor from the state size vs L2
+    int elem_var = -1;  // BH_ELEM_VAR (A/B): -1 regime default
+    ElemFn push_kernel() const {
+        if constexpr (B >= 32) {
+            const int v = elem_var >= 0 ? elem_var : (hbm ? 1 : 0);
+            if (v == 1) return k_push<B, T, 4, 2>;
+            if (v == 2) return k_push<B, T, 2, 4>;
+            if (v == 3) return k_push<B, T, 8, 1>;
+        }
         if constexpr (sizeof(T) == 4 && B >= 32) return k_push<B, T, 1, 4>;
         else return k_push<B, T, 2, 2>;
     }
-    static ElemFn combine_kernel() {
+    ElemFn combine_kernel() const {
+        if constexpr (B >= 32) {
+            const int v = elem_var >= 0 ? elem_var : (hbm ? 1 : 0);
+            if (v == 1) return k_combine<B, T, 4, 2>;
+            if (v == 2) return k_combine<B, T, 2, 4>;
+            if (v == 3) return k_combine<B, T, 8, 1>;
+        }
         if constexpr (sizeof(T) == 4 && B >= 32) return k_combine<B, T, 1, 3, true>;
         else return k_combine<B, T, 2, 2>;
     }
@@ -301,6 +317,12 @@ struct Engine final : EngineBase {
         BH_CUDA(cudaMemset(ctl, 0, sizeof(Control)));
         int sms = 148;
         BH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
+        {
+            int l2 = 0;
+            BH_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, g->device));
+            hbm = (double)B * sizeof(T) * (4.0 * (double)nu + (double)nv) > (double)l2;
+            if (const char *m = getenv("BH_ELEM_VAR")) elem_var = atoi(m);
+        }
         setup_l2_windows(nu, nv);
         for (int side = 0; side < 2; side++) {
             PullFn fn = pull_kernel(side);
