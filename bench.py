@@ -2,23 +2,35 @@
 """bench.py -- BHPP source queries/sec on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-    torchrun --nproc-per-node N ... bench.py --gpus N   (one rank per GPU, NCCL)
+                    [--scaling weak|strong] [--config c2] [--no-c3] [--no-fp64] [--no-cpu]
+
+``--gpus N`` with N > 1 and no torchrun environment re-launches itself under
+``torch.distributed.run`` (one rank per GPU, NCCL, 127.0.0.1); under torchrun
+the ranks come from RANK / WORLD_SIZE / LOCAL_RANK.
 
 Workload (N=1): BASELINE.json configs[1] ("c2"): seeded Chung-Lu bipartite
 graph |U|=1e5, |V|=2e5, |E|=2e6, exponent 2.2, integer weights U{1..10},
 alpha=0.15, eps=1e-7, 64 sources drawn like the reference's bench
 (cli.py:415-417), top-50 per query.  A step = one SS-BI-PUSH pass (backward
-push, forward push, power iteration, combine, top-k) over the 64 sources.
-Weak scaling: every rank runs its own 64 sources on a replica of the graph;
-the per-shard top-k is all-gathered with NCCL inside the step.
+push, forward push, power iteration, combine, top-k) over the batch.
+Scaling (N>1): "weak" (default): every rank runs its own 64 sources on a
+replica of the graph; "strong": one fixed batch (--batch, default the
+config's source count) sharded interleaved over the ranks.  Either way each
+rank's finalize kernel writes its top-k and traces into its region of one
+packed buffer and ONE NCCL all-gather per step returns the full result, in
+source order, to every rank (distributed.py).
 
 value   : queries/s, inputs resident in HBM, device-timed (CUDA events on the
           engine stream, L2 flushed with a 256 MiB write between steps,
           outside the timed interval), max over ranks.
-e2e     : same metric through the public host API bhpp_query_batch (numpy
-          sources in, numpy top-k/traces out; H2D and D2H inside the timing).
-roofline: the round kernels (K1 prep + K2 V pull + K3 U pull), algorithmic
-          bytes of SURVEY.md section 8(d) / their CUDA-event time.
+e2e     : same metric through the public host API (bhpp_query_batch; N>1
+          bhpp_query_sharded): numpy sources in, numpy top-k/traces out, H2D
+          and D2H inside the timing.  fp32 headline; fp64 beside it.
+roofline: the dominant kernel (K2 V pull): SURVEY.md 8(d) algorithmic bytes
+          per launch / its CUDA-event time in a replay of the timed steps;
+          traffic from the committed ncu capture.
+hbm_regime: the same measurement at config c3 (|E|=1e8, operands far larger
+          than L2), N=1 only (--no-c3 skips it).
 cpu_baseline / --impl reference: the bit-exact C port of the reference
           (oracle/) on all host cores, the reference's thread-pool pattern.
 """
@@ -28,6 +40,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import tempfile
@@ -50,10 +63,14 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--batch", type=int, default=0, help="strong scaling: total sources (default: the config's)")
     ap.add_argument("--dtype", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--slots", type=int, default=0)
     ap.add_argument("--no-fp64", action="store_true", help="skip the fp64 side measurement")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-c3", action="store_true", help="skip the config-c3 (HBM regime) leg")
+    ap.add_argument("--c3-sources", type=int, default=1024)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     return ap.parse_args()
 
@@ -62,30 +79,54 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
-def workload(cfg_name: str, rank: int):
+def relaunch_under_torchrun(args) -> int:
+    """bench.py --gpus N outside torchrun: start N ranks (one per GPU) and pass
+    their output through; rank 0 prints the JSON line."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def workload(cfg_name: str, rank: int, world: int, scaling: str, batch: int):
+    """(cfg, graph, this rank's sources, total sources in the job)."""
     from paper_2312_06724_b200.rng import substream
     from paper_2312_06724_b200.synth import CONFIGS, bench_sources, make_graph
 
     cfg = CONFIGS[cfg_name]
-    g = make_graph(cfg)
+    dev = 0 if not os.environ.get("BH_BENCH_HOST_GEN") else None
+    try:
+        import torch
+
+        dev = torch.cuda.current_device() if dev is not None and torch.cuda.is_available() else None
+    except Exception:  # noqa: BLE001 -- no torch CUDA: host generator
+        dev = None
+    g = make_graph(cfg, device=dev)
     n = cfg.n_sources or cfg.u_count
+    if scaling == "strong":
+        total = batch or n
+        src = bench_sources(cfg.u_count, total)
+        return cfg, g, src, total  # every rank holds the whole batch; the shard is taken per step
     if rank == 0:
         src = bench_sources(cfg.u_count, n)
     else:
         src = substream(0, "bench-queries", rank).choice(cfg.u_count, n, replace=False).astype(np.int64)
-    return cfg, g, src
+    return cfg, g, src, n * world
 
 
-def config_json(cfg, n_local, world, slots, k):
+def config_json(cfg, n_local, world, slots, k, scaling, total):
     return {
         "workload": f"{cfg.name}: |U|={cfg.u_count}, |V|={cfg.v_count}, |E|={cfg.edge_count} Chung-Lu "
                     f"beta_u={cfg.beta_u} beta_v={cfg.beta_v} weights={cfg.weights}, alpha={cfg.alpha}, "
-                    f"eps={cfg.epsilons[0]}, {n_local} sources/GPU, top-{k}",
+                    f"eps={cfg.epsilons[0]}, top-{k}, "
+                    + (f"{n_local} sources/GPU" if scaling == "weak" else f"{total} sources sharded over {world} GPU(s)"),
         "queries_per_gpu": int(n_local),
-        "global_batch": int(n_local * world),
+        "global_batch": int(total),
         "top_k": int(k),
         "slots": int(slots),
-        "parallelism": f"query-shard x{world} (graph replicated)",
+        "parallelism": f"query-shard x{world} (graph replicated; one packed NCCL all-gather per step)",
         "l2": "256 MiB write between timed steps (outside the timed interval)",
     }
 
@@ -149,55 +190,30 @@ class Clocks:
                 "region_s": (self.t1 - self.t0).total_seconds()}
 
 
-def _ncu_kernels():
-    p = REPO / "profiles" / "r01_ncu_round_kernels.json"
-    if not p.exists():
-        return None
-    try:
-        return json.loads(p.read_text())["kernels"]
-    except Exception:
-        return None
+def _ncu_capture(name: str):
+    """Latest committed ncu summary profiles/rNN_<name>.json (kernels dict), or (None, None)."""
+    for p in sorted((REPO / "profiles").glob(f"r*_{name}.json"), reverse=True):
+        try:
+            return json.loads(p.read_text())["kernels"], p.name
+        except Exception:  # noqa: BLE001
+            continue
+    return None, None
 
 
-def ncu_round_traffic():
-    """DRAM bytes (read + write) of one round's K1+K2+K3+K1a from the committed
-    ncu capture (profiles/r01_ncu_round_kernels.json), or None."""
-    ks = _ncu_kernels()
+def ncu_traffic(name: str):
+    """(V-pull DRAM bytes per launch, round K1+K2+K3+K1a DRAM bytes, source file) from
+    the committed ncu --set full capture, or Nones."""
+    ks, src = _ncu_capture(name)
     if not ks:
-        return None
-    return 1e6 * sum(v.get("dram_read_MB", 0) + v.get("dram_write_MB", 0)
-                     for k, v in ks.items() if k.startswith(("k_push", "k_pull", "k_combine")))
-
-
-def ncu_vpull_traffic():
-    """DRAM bytes (read + write) of one V-pull launch from the same capture."""
-    ks = _ncu_kernels()
-    if not ks:
-        return None
+        return None, None, None
+    vp = rnd = None
     for k, v in ks.items():  # k_pull*<B, T, SIDE, ...>: SIDE 0 is the V pull
+        b = 1e6 * (v.get("dram_read_MB", 0) + v.get("dram_write_MB", 0))
+        if k.startswith(("k_push", "k_pull", "k_combine")):
+            rnd = (rnd or 0) + b
         if k.startswith("k_pull") and k.split("<", 1)[1].split(",")[2].strip().rstrip(">") == "0":
-            return 1e6 * (v.get("dram_read_MB", 0) + v.get("dram_write_MB", 0))
-    return None
-
-
-def c3_hbm_reference(peak):
-    """DRAM throughput of the round kernels in the HBM-resident regime (config c3,
-    operands larger than L2) from the committed ncu capture
-    (profiles/r01_ncu_c3_round_kernels.json), as fractions of the HBM peak."""
-    p = REPO / "profiles" / "r01_ncu_c3_round_kernels.json"
-    if not p.exists() or not peak:
-        return None
-    try:
-        ks = json.loads(p.read_text())["kernels"]
-    except Exception:
-        return None
-    out = {}
-    for k, v in ks.items():
-        gbs = (v["dram_read_MB"] + v["dram_write_MB"]) / 1e3 / (v["time_us"] / 1e6)
-        out[k] = {"dram_gbs": round(gbs, 1), "frac": round(gbs / peak, 3)}
-    return {"config": "c3 (|E|=1e8, 128 slots): operands exceed L2, gathers served by HBM",
-            "source": "profiles/r01_ncu_c3_round_kernels.json (ncu --set full, one launch each)",
-            "kernels": out}
+            vp = b
+    return vp, rnd, f"profiles/{src}"
 
 
 def peak_hbm():
@@ -205,7 +221,7 @@ def peak_hbm():
     if p.exists():
         try:
             return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
-        except Exception:
+        except Exception:  # noqa: BLE001
             pass
     return 6650.0, "fallback (B200_PROFILING.md)"
 
@@ -218,6 +234,11 @@ def algorithmic_bytes(g, traces, rounds: int, s: int) -> float:
     push_rounds = int(traces["sel_b"].sum() + traces["seq_b"].sum() + traces["sel_f"].sum())
     pi = int(traces["pi_iters"].sum())
     return rounds * (2 * E * (i + s) + (U + V + 2) * o) + push_rounds * s * (4 * U + 2 * V) + pi * s * (3 * U + 2 * V)
+
+
+def vpull_bytes(g, slots: int, s: int) -> int:
+    """SURVEY.md 8(d), one SpMM half (the V pull): E(i+s) + (|V|+1) o + B s (|U| + |V|)."""
+    return g.edge_count * (4 + s) + (g.v_count + 1) * 4 + slots * s * (g.u_count + g.v_count)
 
 
 # -----------------------------------------------------------------------------
@@ -247,7 +268,7 @@ def run_reference(args):
         return
     from oracle import cpu_oracle as O
 
-    cfg, g, src = workload(args.config, 0)
+    cfg, g, src, total = workload(args.config, 0, 1, "weak", 0)
     om = O.index_meta(g, cfg.alpha)
     eps = cfg.epsilons[0]
     eps_b = O.choose_eps_b(eps, om["mu"])
@@ -272,9 +293,10 @@ def run_reference(args):
     v = per_step * args.steps / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Chung-Lu, configs[1])",
-        "config": config_json(cfg, len(src), 1, 0, cfg.k),
+        "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded Chung-Lu, configs[1])",
+        "config": config_json(cfg, len(src), 1, 0, cfg.k, "weak", len(src)),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"{per_step} queries per step ({threads} threads) of the bench sources, "
                                    "bit-exact C port of the reference (oracle/), host wall clock"},
@@ -285,14 +307,247 @@ def run_reference(args):
 
 
 # -----------------------------------------------------------------------------
+class Runner:
+    """One rank's device-resident batch loop (timed steps, profiled replay)."""
+
+    def __init__(self, g, meta, src, eps, k, dtype, slots, rank, world, scaling, total, dev, stream, flush_buf):
+        import torch
+
+        from paper_2312_06724_b200 import _capi
+        from paper_2312_06724_b200.distributed import PackedShard, per_rank
+
+        self.g, self.meta, self.k, self.dtype, self.slots = g, meta, k, dtype, slots
+        self.rank, self.world, self.scaling, self.total = rank, world, scaling, total
+        self.dev, self.stream, self.flush_buf = dev, stream, flush_buf
+        self.eps_b = float(meta.eps_split_policy(eps))
+        self.eps_f = eps - self.eps_b
+        self.dg = _capi.device_graph(g, dtype, device=dev.index)
+        mine = src[rank::world] if scaling == "strong" else src
+        self.n = len(mine)
+        self.src_t = torch.from_numpy(np.asarray(mine, dtype=np.int32)).to(dev)
+        per = per_rank(total, world) if world > 1 else self.n
+        self.packed = PackedShard(per, k, dev)
+        self.out = torch.empty(world * self.packed.buf.numel(), dtype=torch.uint8, device=dev) if world > 1 else None
+        self.gate = torch.zeros(1, dtype=torch.int32).pin_memory()
+        self.gated = not os.environ.get("BH_NO_GRAPH") and not os.environ.get("BH_BENCH_NO_GATE")
+
+    def step(self, async_=False):
+        import torch
+        import torch.distributed as dist
+
+        from paper_2312_06724_b200.bhpp_query import query_batch_device
+
+        if self.n:
+            query_batch_device(self.dg, self.meta, self.eps_b, self.eps_f, self.src_t.data_ptr(), self.n, self.k,
+                               self.packed.idx.data_ptr(), self.packed.score.data_ptr(),
+                               self.packed.trace.data_ptr(), slots=self.slots or None,
+                               stream=self.stream.cuda_stream, async_=async_)
+        if self.world > 1:  # the shards' top-k + traces: one packed all-gather on the same stream
+            with torch.cuda.stream(self.stream):
+                dist.all_gather_into_tensor(self.out, self.packed.buf)
+
+    def run_steps(self, nsteps, profiled, use_gate=False):
+        import torch
+
+        from paper_2312_06724_b200 import _capi
+        from paper_2312_06724_b200.bhpp_query import query_wait
+
+        _capi.set_profiling(profiled)
+        ms, per_step, traces = 0.0, [], []
+        prof = {"ms_prep": 0.0, "ms_vpull": 0.0, "ms_upull": 0.0, "ms_control": 0.0, "rounds": 0, "slots": 0,
+                "step_rounds": []}
+        for _ in range(nsteps):
+            with torch.cuda.stream(self.stream):
+                self.flush_buf.fill_(1.0)  # evict L2 (256 MiB > 126 MB) outside the timed interval
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            if use_gate and self.gated and not profiled and self.n:
+                # the whole step is enqueued behind a gate before the device
+                # starts it: e0..e1 is device time only, no host submission gaps
+                self.gate[0] = 0
+                _capi.check(_capi.lib().bh_stream_gate(self.stream.cuda_stream, self.gate.data_ptr()))
+                e0.record(self.stream)
+                self.step(async_=True)
+                e1.record(self.stream)
+                self.gate[0] = 1
+                query_wait(self.dg)
+            else:
+                e0.record(self.stream)
+                self.step()
+                e1.record(self.stream)
+            e1.synchronize()
+            ms += e0.elapsed_time(e1)
+            per_step.append(e0.elapsed_time(e1))
+            st = self.dg.last_run_stats()
+            prof["step_rounds"].append(int(st["rounds"]))
+            for key in ("ms_prep", "ms_vpull", "ms_upull", "ms_control", "rounds"):
+                prof[key] += st[key]
+            prof["slots"] = st["slots"]
+            traces.append(self.packed.trace[: self.n].cpu().numpy().copy().view(_capi.TRACE_DTYPE).reshape(-1))
+        _capi.set_profiling(False)
+        prof["step_ms"] = per_step
+        return ms, prof, traces
+
+    def measure(self, steps, warmup, clocks_index=None):
+        """Timed steps (max over ranks), launches, clocks; then a profiled replay."""
+        import torch
+        import torch.distributed as dist
+
+        from paper_2312_06724_b200 import _capi
+
+        self.run_steps(max(1, warmup - 1), False)  # graph instantiation, first NCCL use
+        if warmup > 1:
+            self.run_steps(1, False, use_gate=True)
+        torch.cuda.synchronize(self.dev)
+        if self.world > 1:
+            dist.barrier()
+        clocks = Clocks(clocks_index) if clocks_index is not None and not os.environ.get("BH_BENCH_NO_CLOCKS") else None
+        if clocks:
+            clocks.start()
+        launches0 = _capi.kernel_launches()
+        ms, tprof, _ = self.run_steps(steps, False, use_gate=True)
+        launches = _capi.kernel_launches() - launches0
+        clk = clocks.stop() if clocks else {"sm_mhz": None, "reasons": ["not sampled"]}
+        torch.cuda.synchronize(self.dev)
+        if self.world > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device=self.dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            dist.barrier()
+        pms, prof, ptraces = self.run_steps(steps, True)
+        prof["timed_step_ms"] = tprof["step_ms"]
+        prof["timed_step_rounds"] = tprof["step_rounds"]
+        return ms, launches, prof, clk, ptraces, pms
+
+
+def e2e_leg(g, meta, src, eps, k, dtype, slots, rank, world, scaling, dev, stream, flush_buf, steps):
+    """The public host API per step (numpy in, numpy out): bhpp_query_batch at
+    N=1 / weak scaling, bhpp_query_sharded (device-resident shard + packed
+    all-gather, numpy in and out) for strong scaling.  Max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2312_06724_b200 as bh
+    from paper_2312_06724_b200.distributed import bhpp_query_sharded, gather_results
+
+    def one():
+        if scaling == "strong" and world > 1:
+            return bhpp_query_sharded(g, meta, src, eps, k=k, dtype=dtype, slots=slots or None, device=dev)
+        res = bh.bhpp_query_batch(g, meta, src, eps, k=k, dtype=dtype, slots=slots or None,
+                                  stream=stream.cuda_stream)
+        if world > 1:
+            gather_results(res.topk_index, res.topk_score, res.traces, world * len(src), rank, world, device=dev)
+        return res
+
+    for _ in range(2):
+        one()
+    tot, per = 0.0, []
+    for _ in range(steps):
+        with torch.cuda.stream(stream):
+            flush_buf.fill_(1.0)
+        torch.cuda.synchronize(dev)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        one()
+        e1.record(stream)
+        e1.synchronize()
+        tot += e0.elapsed_time(e1)
+        per.append(round(e0.elapsed_time(e1), 3))
+    if world > 1:
+        t = torch.tensor([tot], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot = float(t.item())
+    return tot, per
+
+
+def roofline_block(g, prof, pms, steps, s_bytes, alg, peak, peak_src, traffic_name):
+    B = prof.get("slots", 0)
+    rounds = max(1, prof["rounds"])
+    v_bytes = vpull_bytes(g, B, s_bytes)
+    v_us = prof["ms_vpull"] * 1e3 / rounds
+    v_ach = v_bytes / (v_us / 1e6) / 1e9 if v_us > 0 else None
+    kern_ms = prof["ms_prep"] + prof["ms_vpull"] + prof["ms_upull"]
+    ach = alg / (kern_ms / 1e3) / 1e9 if kern_ms > 0 else None
+    vp_t, rnd_t, t_src = ncu_traffic(traffic_name)
+    return {
+        "bound": "hbm", "achieved": v_ach, "peak": peak, "unit": "GB/s",
+        "frac": v_ach / peak if v_ach else None, "traffic": vp_t,
+        "kernel": "K2 V pull (k_pull_sw / k_pull_small, SIDE_V), the dominant kernel",
+        "algorithmic_bytes_per_launch": v_bytes,
+        "algorithmic_model": "E(i+s) + (|V|+1) o + B s (|U| + |V|), i = o = 4 (SURVEY 8(d), one SpMM half)",
+        "launch_us": v_us, "launches": int(prof["rounds"]),
+        "share_of_step": prof["ms_vpull"] / pms if pms else None,
+        "traffic_source": t_src,
+        "round": {
+            "unit": "push/PI round = K1 push + K2 V-pull + K3 U-pull + K1a combine (SURVEY 8(d) unit)",
+            "achieved_gbs": ach, "frac": ach / peak if ach else None,
+            "algorithmic_bytes_per_round": alg / rounds, "traffic_per_round": rnd_t,
+            "share_of_step": kern_ms / pms if pms else None,
+        },
+        "gather": {"bytes_per_round": 2 * g.edge_count * B * s_bytes,
+                   "achieved_tbs": (2 * g.edge_count * B * s_bytes * prof["rounds"]
+                                    / ((prof["ms_vpull"] + prof["ms_upull"]) / 1e3) / 1e12)
+                   if prof["ms_vpull"] + prof["ms_upull"] > 0 else None,
+                   "note": "operand-row gathers of the two pulls (E x B x s each)"},
+        "algorithmic_bytes_per_step": alg / steps, "kernel_ms_per_step": kern_ms / steps,
+        "rounds_per_step": prof["rounds"] / steps,
+        "timing": "per-kernel CUDA events on the engine stream, in a replay of the timed steps "
+                  "(the headline value is timed without per-kernel events; each timed step is "
+                  "enqueued behind a device start gate, so e0..e1 is device time only)",
+        "breakdown_ms_per_step": {k2: prof[k2] / steps for k2 in ("ms_prep", "ms_vpull", "ms_upull", "ms_control")},
+        "peak_source": peak_src,
+        "timed_step_ms": [round(x, 3) for x in prof.get("timed_step_ms", [])],
+        "profiled_step_ms": [round(x, 3) for x in prof.get("step_ms", [])],
+        "timed_step_rounds": prof.get("timed_step_rounds"),
+    }
+
+
+def c3_leg(n_sources, dev, stream, flush_buf, peak, peak_src):
+    """Config c3 (HBM regime): one timed batch of the config's bench sources
+    (device-resident), a profiled replay on a quarter of them for the roofline."""
+    import torch
+
+    import paper_2312_06724_b200 as bh
+    from paper_2312_06724_b200 import _capi
+    from paper_2312_06724_b200.synth import CONFIGS, bench_sources, make_graph
+
+    cfg = CONFIGS["c3"]
+    t0 = time.perf_counter()
+    g = make_graph(cfg, device=dev.index)
+    t_graph = time.perf_counter() - t0
+    meta = bh.build_index_meta(g, cfg.alpha)
+    eps = cfg.epsilons[0]
+    src = bench_sources(cfg.u_count, n_sources)
+    r = Runner(g, meta, src, eps, cfg.k, "fp32", 0, 0, 1, "weak", len(src), dev, stream, flush_buf)
+    r.run_steps(1, False)  # warm-up (engine + graph instantiation)
+    launches0 = _capi.kernel_launches()
+    ms, tprof, traces = r.run_steps(1, False, use_gate=True)
+    launches = _capi.kernel_launches() - launches0
+    sub = Runner(g, meta, src[: max(1, n_sources // 4)], eps, cfg.k, "fp32", 0, 0, 1, "weak",
+                 max(1, n_sources // 4), dev, stream, flush_buf)
+    pms, prof, ptraces = sub.run_steps(1, True)
+    alg = sum(algorithmic_bytes(g, t, prof["rounds"], 4) for t in ptraces)
+    roof = roofline_block(g, prof, pms, 1, 4, alg, peak, peak_src, "ncu_c3_round_kernels")
+    roof["profiled_on"] = f"{len(sub.src_t)} of the {n_sources} sources (per-kernel event replay)"
+    out = {"config": f"c3: |U|={cfg.u_count}, |V|={cfg.v_count}, |E|={cfg.edge_count} Chung-Lu beta 2.1, "
+                     f"int weights, alpha={cfg.alpha}, eps={eps}, {n_sources} sources, top-{cfg.k}, fp32",
+           "value": n_sources / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "slots": int(tprof["slots"]),
+           "rounds": int(tprof["rounds"]), "gpu_launches": int(launches), "graph_build_s": round(t_graph, 1),
+           "roofline": roof}
+    del r, sub
+    _capi._graph_cache.clear()
+    del g
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     import paper_2312_06724_b200 as bh
     from paper_2312_06724_b200 import _capi
-    from paper_2312_06724_b200.bhpp_query import query_batch_device, query_wait
-    from paper_2312_06724_b200.distributed import gather_results
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -300,222 +555,81 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
 
-    cfg, g, src = workload(args.config, rank)
+    cfg, g, src, total = workload(args.config, rank, world, args.scaling, args.batch)
     meta = bh.build_index_meta(g, cfg.alpha)
     eps = cfg.epsilons[0]
-    eps_b = float(meta.eps_split_policy(eps))
-    eps_f = eps - eps_b
     k = cfg.k
-    n = len(src)
     stream = torch.cuda.Stream(device=dev)
     flush_buf = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    # device-side start gate for the timed steps (graph mode only: the eager
-    # round loop synchronises inside the call)
-    gated = not os.environ.get("BH_NO_GRAPH") and not os.environ.get("BH_BENCH_NO_GATE")
-    gate = torch.zeros(1, dtype=torch.int32).pin_memory()
-
-    def measure(dtype: str, steps: int, warmup: int):
-        """Timed steps (device events around each step only), then the same
-        steps replayed with per-kernel events for the roofline breakdown."""
-        dg = _capi.device_graph(g, dtype, device=local)
-        src_t = torch.from_numpy(src.astype(np.int32)).to(dev)
-        tk_i = torch.empty((n, k), dtype=torch.int32, device=dev)
-        tk_s = torch.empty((n, k), dtype=torch.float64, device=dev)
-        tr = torch.empty((n, _capi.TRACE_DTYPE.itemsize), dtype=torch.uint8, device=dev)
-        all_i = torch.empty((world * n, k), dtype=torch.int32, device=dev)
-        all_s = torch.empty((world * n, k), dtype=torch.float64, device=dev)
-
-        def step(async_=False):
-            query_batch_device(dg, meta, eps_b, eps_f, src_t.data_ptr(), n, k, tk_i.data_ptr(), tk_s.data_ptr(),
-                               tr.data_ptr(), slots=args.slots or None, stream=stream.cuda_stream, async_=async_)
-            if world > 1:  # gather the shard top-k on the same stream (NCCL)
-                with torch.cuda.stream(stream):
-                    dist.all_gather_into_tensor(all_i, tk_i)
-                    dist.all_gather_into_tensor(all_s, tk_s)
-
-        def run_steps(nsteps, profiled, use_gate=False):
-            _capi.set_profiling(profiled)
-            ms = 0.0
-            per_step = []
-            prof = {"ms_prep": 0.0, "ms_vpull": 0.0, "ms_upull": 0.0, "ms_control": 0.0, "rounds": 0, "slots": 0}
-            traces = []
-            for _ in range(nsteps):
-                with torch.cuda.stream(stream):
-                    flush_buf.fill_(1.0)  # evict L2 (256 MiB > 126 MB) outside the timed interval
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                if use_gate and gated and not profiled:
-                    # the whole step is enqueued behind a gate before the device
-                    # starts it: e0..e1 is device time only, no host submission gaps
-                    gate[0] = 0
-                    _capi.check(_capi.lib().bh_stream_gate(stream.cuda_stream, gate.data_ptr()))
-                    e0.record(stream)
-                    step(async_=True)
-                    e1.record(stream)
-                    gate[0] = 1
-                    query_wait(dg)
-                else:
-                    e0.record(stream)
-                    step()
-                    e1.record(stream)
-                e1.synchronize()
-                ms += e0.elapsed_time(e1)
-                per_step.append(e0.elapsed_time(e1))
-                st = dg.last_run_stats()
-                prof.setdefault("step_rounds", []).append(int(st["rounds"]))
-                for key in ("ms_prep", "ms_vpull", "ms_upull", "ms_control", "rounds"):
-                    prof[key] += st[key]
-                prof["slots"] = st["slots"]
-                traces.append(tr.cpu().numpy().copy().view(_capi.TRACE_DTYPE).reshape(-1))
-            _capi.set_profiling(False)
-            prof["step_ms"] = per_step
-            return ms, prof, traces
-
-        # warm-up: ungated first (graph instantiation, first NCCL use), the last one gated
-        run_steps(max(1, warmup - 1), False)
-        if warmup > 1:
-            run_steps(1, False, use_gate=True)
-        torch.cuda.synchronize(dev)
-        if world > 1:
-            dist.barrier()
-        clocks = Clocks(local) if not os.environ.get("BH_BENCH_NO_CLOCKS") else None
-        if clocks:
-            clocks.start()
-        launches0 = _capi.kernel_launches()
-        ms, tprof, traces_all = run_steps(steps, False, use_gate=True)
-        launches = _capi.kernel_launches() - launches0
-        clk = clocks.stop() if clocks else {"sm_mhz": None, "reasons": ["not sampled (BH_BENCH_NO_CLOCKS)"]}
-        torch.cuda.synchronize(dev)
-        if world > 1:
-            t = torch.tensor([ms], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-            dist.barrier()
-        pms, prof, ptraces = run_steps(steps, True)
-        prof["timed_step_ms"] = tprof["step_ms"]
-        prof["timed_step_rounds"] = tprof["step_rounds"]
-        return ms, launches, prof, clk, ptraces, pms
-
-    # headline: fp32 storage / fp64 accumulation
-    ms, launches, prof, clk, traces_all, pms = measure(args.dtype, args.steps, args.warmup)
-    value = world * n * args.steps / (ms / 1e3)
-    s_bytes = 4 if args.dtype == "fp32" else 8
-    alg = sum(algorithmic_bytes(g, t, prof["rounds"] // args.steps, s_bytes) for t in traces_all)
-    kern_ms = prof["ms_prep"] + prof["ms_vpull"] + prof["ms_upull"]
-    # dominant kernel: the V pull, SURVEY 8(d) bytes of one SpMM half per launch
-    B_slots = prof.get("slots", 0) or n
-    v_bytes = g.edge_count * (4 + s_bytes) + (g.v_count + 1) * 4 + B_slots * s_bytes * (g.u_count + g.v_count)
-    v_launch_us = prof["ms_vpull"] * 1e3 / max(1, prof["rounds"])
-    v_achieved = v_bytes / (v_launch_us / 1e6) / 1e9 if v_launch_us > 0 else None
-    achieved = alg / (kern_ms / 1e3) / 1e9 if kern_ms > 0 else None
     peak, peak_src = peak_hbm()
 
-    # e2e through the public host API (numpy in, numpy out; copies inside)
-    e2e_ms = 0.0
-    e2e_steps = []
-    for _ in range(2):
-        bh.bhpp_query_batch(g, meta, src, eps, k=k, dtype=args.dtype, slots=args.slots or None,
-                            stream=stream.cuda_stream)
-    e2e_n = max(args.steps, 10)  # e2e steps are cheap: at least 10 samples
-    gc_events = [0]
-    if os.environ.get("BH_BENCH_E2E_DIAG"):
-        import gc
-        gc.callbacks.append(lambda phase, info: gc_events.__setitem__(0, gc_events[0] + (phase == "start")))
-    for _ in range(e2e_n):
-        with torch.cuda.stream(stream):
-            flush_buf.fill_(1.0)
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        th0 = time.perf_counter()
-        e0.record(stream)
-        res = bh.bhpp_query_batch(g, meta, src, eps, k=k, dtype=args.dtype, slots=args.slots or None,
-                                  stream=stream.cuda_stream)
-        th1 = time.perf_counter()
-        if world > 1:
-            from paper_2312_06724_b200.distributed import gather_results as _gr
-            with torch.cuda.stream(stream):
-                _gr(res.topk_index, res.topk_score, res.traces, world * n, rank, world, device=dev)
-        e1.record(stream)
-        th2 = time.perf_counter()
-        e1.synchronize()
-        e2e_ms += e0.elapsed_time(e1)
-        e2e_steps.append(round(e0.elapsed_time(e1), 3))
-        if os.environ.get("BH_BENCH_E2E_DIAG"):
-            print(f"[e2e diag] event {e0.elapsed_time(e1):.3f} ms, host call {1e3 * (th1 - th0):.3f} ms, "
-                  f"engine {1e3 * res.timing['total']:.3f} ms, to e1 {1e3 * (th2 - th0):.3f} ms, gc {gc_events[0]}",
-                  file=sys.stderr, flush=True)
-    if world > 1:
-        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-    e2e_value = world * n * e2e_n / (e2e_ms / 1e3)
+    def runner(dtype):
+        return Runner(g, meta, src, eps, k, dtype, args.slots, rank, world, args.scaling, total, dev, stream,
+                      flush_buf)
+
+    r32 = runner(args.dtype)
+    n_local = r32.n
+    ms, launches, prof, clk, traces_all, pms = r32.measure(args.steps, args.warmup, clocks_index=local)
+    value = total * args.steps / (ms / 1e3)
+    s_bytes = 4 if args.dtype == "fp32" else 8
+    alg = sum(algorithmic_bytes(g, t, prof["rounds"] // args.steps, s_bytes) for t in traces_all)
+    roof = roofline_block(g, prof, pms, args.steps, s_bytes, alg, peak, peak_src, "ncu_round_kernels")
+
+    e2e_src = src  # strong: the whole batch (sharded inside); weak: this rank's sources
+    e2e_n = max(args.steps, 10)
+    e2e_ms, e2e_steps = e2e_leg(g, meta, e2e_src, eps, k, args.dtype, args.slots, rank, world, args.scaling, dev,
+                                stream, flush_buf, e2e_n)
+    e2e_value = total * e2e_n / (e2e_ms / 1e3)
+    n_in = len(src)
 
     fp64 = None
     if not args.no_fp64 and args.dtype != "fp64":
         st64 = max(2, args.steps // 2)
-        ms64, _, prof64, _, tr64, _ = measure("fp64", st64, 1)
+        r64 = runner("fp64")
+        ms64, _, prof64, _, tr64, _ = r64.measure(st64, 1)
         alg64 = sum(algorithmic_bytes(g, t, prof64["rounds"] // st64, 8) for t in tr64)
         k64 = prof64["ms_prep"] + prof64["ms_vpull"] + prof64["ms_upull"]
-        fp64 = {"value": world * n * st64 / (ms64 / 1e3), "unit": UNIT, "ms_per_step": ms64 / st64,
-                "roofline_achieved_gbs": alg64 / (k64 / 1e3) / 1e9 if k64 else None}
+        e64_ms, e64_steps = e2e_leg(g, meta, e2e_src, eps, k, "fp64", args.slots, rank, world, args.scaling, dev,
+                                    stream, flush_buf, max(3, st64))
+        fp64 = {"value": total * st64 / (ms64 / 1e3), "unit": UNIT, "ms_per_step": ms64 / st64,
+                "roofline_achieved_gbs": alg64 / (k64 / 1e3) / 1e9 if k64 else None,
+                "e2e": {"value": total * max(3, st64) / (e64_ms / 1e3), "unit": UNIT,
+                        "ms_per_step": e64_ms / max(3, st64), "step_ms": e64_steps,
+                        "h2d_bytes_per_step": int(n_in * 4),
+                        "d2h_bytes_per_step": int(n_in * k * (4 + 8) + n_in * _capi.TRACE_DTYPE.itemsize)}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_leg(g, src, cfg.alpha, eps_b, eps_f, meta.lam, args.cpu_seconds)
+        eb = float(meta.eps_split_policy(eps))
+        cpu = cpu_leg(g, src, cfg.alpha, eb, eps - eb, meta.lam, args.cpu_seconds)
+
+    hbm = None
+    if world == 1 and not args.no_c3 and args.config == "c2":
+        hbm = c3_leg(args.c3_sources, dev, stream, flush_buf, peak, peak_src)
 
     if rank == 0:
         t0 = traces_all[0]
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32" if args.dtype == "fp32" else "f64",
-            "data": "synthetic (seeded Chung-Lu stand-in for configs[1]; reference sampler for sources)",
-            "config": config_json(cfg, n, world, prof.get("slots", 0), k),
-            "roofline": {
-                "bound": "hbm", "achieved": v_achieved, "peak": peak, "unit": "GB/s",
-                "frac": v_achieved / peak if v_achieved else None, "traffic": ncu_vpull_traffic(),
-                "kernel": "K2 V pull (k_pull_sw, SIDE_V), the dominant kernel",
-                "algorithmic_bytes_per_launch": v_bytes,
-                "algorithmic_model": "E(i+s) + (|V|+1) o + B s (|U| + |V|), i = o = 4 (SURVEY 8(d), one SpMM half)",
-                "launch_us": v_launch_us, "launches": int(prof["rounds"]),
-                "share_of_step": prof["ms_vpull"] / pms if pms else None,
-                "traffic_note": "DRAM read+write bytes of one V-pull launch from one ncu --set full capture "
-                                "(profiles/r01_ncu_round_kernels.json, cold cache)",
-                "round": {
-                    "unit": "push/PI round = K1 push + K2 V-pull + K3 U-pull + K1a combine (SURVEY 8(d) unit)",
-                    "achieved_gbs": achieved, "frac": achieved / peak if achieved else None,
-                    "algorithmic_bytes_per_round": alg / max(1, prof["rounds"]),
-                    "traffic_per_round": ncu_round_traffic(),
-                    "share_of_step": kern_ms / pms if pms else None,
-                },
-                "gather": {"bytes_per_round": 2 * g.edge_count * prof.get("slots", 0) * s_bytes,
-                           "achieved_tbs": (2 * g.edge_count * prof.get("slots", 0) * s_bytes * prof["rounds"]
-                                            / ((prof["ms_vpull"] + prof["ms_upull"]) / 1e3) / 1e12)
-                           if prof["ms_vpull"] + prof["ms_upull"] > 0 else None,
-                           "note": "operand-row gathers of the two pulls (E x B x s each), L2-served; "
-                                   "tools/gather_bench.cu ceiling 13-17 TB/s"},
-                "algorithmic_bytes_per_step": alg / args.steps, "kernel_ms_per_step": kern_ms / args.steps,
-                "rounds_per_step": prof["rounds"] / args.steps,
-                "timing": "per-kernel CUDA events on the engine stream, in a replay of the timed steps "
-                          "(the headline value is timed without per-kernel events; each timed step is "
-                          "enqueued behind a device start gate, so e0..e1 is device time only)",
-                "breakdown_ms_per_step": {k2: prof[k2] / args.steps for k2 in ("ms_prep", "ms_vpull", "ms_upull", "ms_control")},
-                "peak_source": peak_src,
-                "hbm_regime_reference": c3_hbm_reference(peak),
-                "timed_step_ms": [round(x, 3) for x in prof.get("timed_step_ms", [])],
-                "profiled_step_ms": [round(x, 3) for x in prof.get("step_ms", [])],
-                "timed_step_rounds": prof.get("timed_step_rounds"),
-            },
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f32" if args.dtype == "fp32" else "f64",
+            "data": f"synthetic (seeded Chung-Lu stand-in for {cfg.name}; reference sampler for sources)",
+            "config": config_json(cfg, n_local, world, prof.get("slots", 0), k, args.scaling, total),
+            "roofline": roof,
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(n * 4),
-                    "d2h_bytes_per_step": int(n * k * (4 + 8) + n * _capi.TRACE_DTYPE.itemsize),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(n_in * 4),
+                    "d2h_bytes_per_step": int(n_in * k * (4 + 8) + n_in * _capi.TRACE_DTYPE.itemsize),
                     "ms_per_step": e2e_ms / e2e_n, "steps": e2e_n, "step_ms": e2e_steps,
-                    "path": "bhpp_query_batch (numpy sources in, numpy top-k / traces out), one call per step"},
+                    "path": ("bhpp_query_sharded (numpy in, device shard + packed all-gather, numpy out)"
+                             if args.scaling == "strong" and world > 1 else
+                             "bhpp_query_batch (numpy sources in, numpy top-k / traces out), one call per step"
+                             + (" + host all-gather of the shards" if world > 1 else ""))},
             "gpu_launches": int(launches),
             "clocks": clk,
             "fp64": fp64,
+            "hbm_regime": hbm,
             "trace_sample": {"sel_b": int(t0["sel_b"][0]), "seq_b": int(t0["seq_b"][0]), "sel_f": int(t0["sel_f"][0]),
-                             "pi_iters": int(t0["pi_iters"][0]), "n_p_f": int(t0["n_p_f"][0])},
+                             "pi_iters": int(t0["pi_iters"][0]), "n_p_f": int(t0["n_p_f"][0])} if len(t0) else None,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -525,6 +639,20 @@ def run_ours(args):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        if args.impl == "reference":  # the CPU reference arm: rank 0 alone does the work
+            run_reference(args)
+            return
+        try:
+            import torch
+
+            have = torch.cuda.device_count()
+        except Exception:  # noqa: BLE001
+            have = 0
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible CUDA devices, found {have}", file=sys.stderr)
+            sys.exit(2)
+        sys.exit(relaunch_under_torchrun(args))
     if args.impl == "reference":
         run_reference(args)
     else:

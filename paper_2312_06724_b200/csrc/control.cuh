@@ -118,6 +118,155 @@ __device__ void slot_finish(Slot &sl, Finish &f, bool has_pi) {
     sl.op = OP_IDLE;
 }
 
+// Reductions of one slot's round (K1 push statistics, K2 n_p, K1a exit tests).
+struct RoundRed {
+    int64_t cnt;   // |A|
+    int64_t np;    // sum deg(A) + sum deg(N(A))
+    double sum;    // sum r_u after the round
+    double wsum;   // sum w_ratio r_u after the round
+    double left;   // forward: weighted residue left below threshold
+    int32_t any;   // any r_u > threshold after the round
+};
+
+// The per-query state transition after a round with op `op` (push_engine.py
+// ss_push 164-184, selective_push 131-142, pi_push 230-250, power iteration
+// 113-117): counters, exit tests, budget switches (Eq. 10, Eq. 12 in exact
+// form), phase changes.  Returns true when the query finished (f written).
+__device__ bool slot_transition(Slot &sl, int op, const RoundRed &red, double alpha, double budget_scale,
+                                double log_decay, Finish &f) {
+    bool fin = false;
+    const int64_t cnt = red.cnt;
+    const int32_t any = red.any;
+    const double sum = red.sum, wsum = red.wsum;
+    if (op == OP_MEASURE) {  // pi_push entry: gamma of the uploaded ledger (push_engine.py:222)
+        sl.gamma = wsum;
+        sl.mass_prev = wsum;
+        sl.defsum = 0.0;
+        sl.op = OP_FENTRY;
+    } else if (op_is_push(op)) {
+        sl.push_seq++;
+        const int64_t worked = cnt > 0;
+        sl.n_p += red.np;
+        bool end_backward = false;
+        if (op == OP_BSEL_INIT || op == OP_BSEL) {
+            sl.sel_b += worked;
+            sl.last_phase = BH_PHASE_SELECTIVE;
+            sl.last_rounds = sl.sel_b;
+            if (!any) {
+                sl.term_b = BH_TERM_THRESHOLD;
+                end_backward = true;
+            } else if (!sl.budget) {
+                sl.op = OP_BSEL;
+            } else if (sum <= 0.0) {
+                sl.term_b = BH_TERM_DRAINED;
+                end_backward = true;
+            } else if ((double)sl.n_p >= budget_scale * (log(1.0 / sum) / log_decay)) {
+                if (sum > sl.eps_b) {  // any is true here
+                    sl.op = OP_SEQ;
+                    sl.phase = PH_SEQ;
+                } else {
+                    sl.term_b = BH_TERM_BUDGET;
+                    end_backward = true;
+                }
+            } else {
+                sl.op = OP_BSEL;
+            }
+        } else if (op == OP_SEQ) {
+            sl.seq_b += worked;
+            sl.last_phase = BH_PHASE_SEQUENTIAL;
+            sl.last_rounds = sl.seq_b;
+            if (any && sum > sl.eps_b) {
+                sl.op = OP_SEQ;
+            } else {
+                sl.term_b = BH_TERM_BUDGET;
+                end_backward = true;
+            }
+        } else {  // forward round
+            sl.sel_f += worked;
+            sl.last_phase = BH_PHASE_FORWARD;
+            sl.last_rounds = sl.sel_f;
+            // Eq. 12 in exact (telescoped) form.  By detailed balance a forward
+            // round maps the weighted residue mass m = P + L (P pushed, L left
+            // below threshold) to (1-alpha) P + L, so
+            //   ln(gamma / wmass_k) = sum_j [ln(1/(1-alpha)) - log1p(alpha f_j / (1-alpha))],
+            // f_j = L_j / m_{j-1}.  The budget test n_p - n_0 >= 2|E| ln(gamma/wmass)/ln(1/(1-alpha))
+            // becomes (2|E| k - used) <= 2|E| sum_j log1p(...) / ln(1/(1-alpha)): a comparison of
+            // two small quantities that fp32 residues resolve as well as fp64 ones.
+            const double fj = sl.mass_prev > 0.0 ? red.left / sl.mass_prev : 0.0;
+            if (fj > 0.0) sl.defsum += log1p(alpha * fj / (1.0 - alpha));
+            sl.mass_prev = wsum;
+            if (!any) {
+                sl.term_f = BH_TERM_THRESHOLD;
+                sl.pi_t = 0;
+                fin = true;
+                slot_finish(sl, f, false);
+            } else if (wsum <= 0.0) {
+                sl.term_f = BH_TERM_DRAINED;
+                sl.pi_t = 0;
+                fin = true;
+                slot_finish(sl, f, false);
+            } else {
+                bool brk;
+                const int64_t used = sl.n_p - sl.n_p_entry;
+                const int64_t limit = (int64_t)budget_scale * sl.sel_f;  // 2|E| k
+                if (sl.defsum == 0.0) {
+                    // Every positive residue was pushed in every forward round: the
+                    // budget is exactly 2|E| k.  Equality (A = U in every round) is the
+                    // exact tie of SURVEY.md sec. 0 fact 11, which the reference resolves
+                    // by rounding: break, unless replaying a reference run (tie_skip).
+                    if (used >= limit) {
+                        sl.tie_checks++;
+                        brk = sl.tie_checks > sl.tie_skip;
+                        if (brk) sl.tie_broke = 1;
+                    } else {
+                        brk = false;
+                    }
+                } else {
+                    brk = (double)(limit - used) <= budget_scale * sl.defsum / log_decay;
+                }
+                if (brk) {
+                    sl.term_f = BH_TERM_BUDGET;
+                    sl.pi_t = required_iterations_dev(alpha, sl.eps_f, wsum);
+                    sl.pi_done = 0;
+                    sl.phase = PH_PI;
+                    sl.op = sl.pi_t > 0 ? OP_PIENTRY : OP_PIENTRY0;
+                } else {
+                    sl.op = OP_FSEL;
+                }
+            }
+        }
+        if (end_backward) {
+            sl.n_p_b = sl.n_p;
+            if (sl.job == BH_JOB_SS_PUSH || sl.job == BH_JOB_SELECTIVE) {
+                fin = true;
+                slot_finish(sl, f, false);
+            } else {
+                sl.phase = PH_FWD;
+                sl.op = OP_FENTRY;
+                sl.gamma = wsum;  // gamma at PI-Push entry (push_engine.py:222)
+                sl.mass_prev = wsum;
+                sl.defsum = 0.0;
+                sl.n_p_entry = sl.n_p;
+                sl.tie_checks = 0;
+            }
+        }
+    } else if (op == OP_PIENTRY0) {
+        sl.last_phase = -1;
+        fin = true;
+        slot_finish(sl, f, true);
+    } else if (op == OP_PIENTRY || op == OP_PI) {
+        sl.last_phase = -1;
+        sl.pi_done++;
+        if (sl.pi_done >= sl.pi_t) {
+            fin = true;
+            slot_finish(sl, f, true);
+        } else {
+            sl.op = OP_PI;
+        }
+    }
+    return fin;
+}
+
 constexpr int CONTROL_THREADS = 256;
 
 // One block per slot: deterministic reduction of the slot's partial rows, the
@@ -229,137 +378,15 @@ __global__ void __launch_bounds__(CONTROL_THREADS) k_control(ControlArgs a) {
         }
     }
     if (tid == 0) {
-        bool fin = false;
+        RoundRed red;
+        red.cnt = w_cnt[0];
+        red.np = w_np[0];
+        red.sum = w_sum[0];
+        red.wsum = w_wsum[0];
+        red.left = w_left[0];
+        red.any = w_any[0];
         const int op = a.first ? OP_IDLE : sl.op;
-        const int64_t cnt = w_cnt[0];
-        const int32_t any = w_any[0];
-        const double sum = w_sum[0], wsum = w_wsum[0];
-        if (op == OP_MEASURE) {  // pi_push entry: gamma of the uploaded ledger (push_engine.py:222)
-            sl.gamma = wsum;
-            sl.mass_prev = wsum;
-            sl.defsum = 0.0;
-            sl.op = OP_FENTRY;
-        } else if (op_is_push(op)) {
-            sl.push_seq++;
-            const int64_t worked = cnt > 0;
-            sl.n_p += w_np[0];
-            bool end_backward = false;
-            if (op == OP_BSEL_INIT || op == OP_BSEL) {
-                sl.sel_b += worked;
-                sl.last_phase = BH_PHASE_SELECTIVE;
-                sl.last_rounds = sl.sel_b;
-                if (!any) {
-                    sl.term_b = BH_TERM_THRESHOLD;
-                    end_backward = true;
-                } else if (!sl.budget) {
-                    sl.op = OP_BSEL;
-                } else if (sum <= 0.0) {
-                    sl.term_b = BH_TERM_DRAINED;
-                    end_backward = true;
-                } else if ((double)sl.n_p >= a.budget_scale * (log(1.0 / sum) / a.log_decay)) {
-                    if (sum > sl.eps_b) {  // any is true here
-                        sl.op = OP_SEQ;
-                        sl.phase = PH_SEQ;
-                    } else {
-                        sl.term_b = BH_TERM_BUDGET;
-                        end_backward = true;
-                    }
-                } else {
-                    sl.op = OP_BSEL;
-                }
-            } else if (op == OP_SEQ) {
-                sl.seq_b += worked;
-                sl.last_phase = BH_PHASE_SEQUENTIAL;
-                sl.last_rounds = sl.seq_b;
-                if (any && sum > sl.eps_b) {
-                    sl.op = OP_SEQ;
-                } else {
-                    sl.term_b = BH_TERM_BUDGET;
-                    end_backward = true;
-                }
-            } else {  // forward round
-                sl.sel_f += worked;
-                sl.last_phase = BH_PHASE_FORWARD;
-                sl.last_rounds = sl.sel_f;
-                // Eq. 12 in exact (telescoped) form.  By detailed balance a forward
-                // round maps the weighted residue mass m = P + L (P pushed, L left
-                // below threshold) to (1-alpha) P + L, so
-                //   ln(gamma / wmass_k) = sum_j [ln(1/(1-alpha)) - log1p(alpha f_j / (1-alpha))],
-                // f_j = L_j / m_{j-1}.  The budget test n_p - n_0 >= 2|E| ln(gamma/wmass)/ln(1/(1-alpha))
-                // becomes (2|E| k - used) <= 2|E| sum_j log1p(...) / ln(1/(1-alpha)): a comparison of
-                // two small quantities that fp32 residues resolve as well as fp64 ones.
-                const double fj = sl.mass_prev > 0.0 ? w_left[0] / sl.mass_prev : 0.0;
-                if (fj > 0.0) sl.defsum += log1p(a.alpha * fj / (1.0 - a.alpha));
-                sl.mass_prev = wsum;
-                if (!any) {
-                    sl.term_f = BH_TERM_THRESHOLD;
-                    sl.pi_t = 0;
-                    fin = true;
-                    slot_finish(sl, a.fin[s], false);
-                } else if (wsum <= 0.0) {
-                    sl.term_f = BH_TERM_DRAINED;
-                    sl.pi_t = 0;
-                    fin = true;
-                    slot_finish(sl, a.fin[s], false);
-                } else {
-                    bool brk;
-                    const int64_t used = sl.n_p - sl.n_p_entry;
-                    const int64_t limit = (int64_t)a.budget_scale * sl.sel_f;  // 2|E| k
-                    if (sl.defsum == 0.0) {
-                        // Every positive residue was pushed in every forward round: the
-                        // budget is exactly 2|E| k.  Equality (A = U in every round) is the
-                        // exact tie of SURVEY.md sec. 0 fact 11, which the reference resolves
-                        // by rounding: break, unless replaying a reference run (tie_skip).
-                        if (used >= limit) {
-                            sl.tie_checks++;
-                            brk = sl.tie_checks > sl.tie_skip;
-                            if (brk) sl.tie_broke = 1;
-                        } else {
-                            brk = false;
-                        }
-                    } else {
-                        brk = (double)(limit - used) <= a.budget_scale * sl.defsum / a.log_decay;
-                    }
-                    if (brk) {
-                        sl.term_f = BH_TERM_BUDGET;
-                        sl.pi_t = required_iterations_dev(a.alpha, sl.eps_f, wsum);
-                        sl.pi_done = 0;
-                        sl.phase = PH_PI;
-                        sl.op = sl.pi_t > 0 ? OP_PIENTRY : OP_PIENTRY0;
-                    } else {
-                        sl.op = OP_FSEL;
-                    }
-                }
-            }
-            if (end_backward) {
-                sl.n_p_b = sl.n_p;
-                if (sl.job == BH_JOB_SS_PUSH || sl.job == BH_JOB_SELECTIVE) {
-                    fin = true;
-                    slot_finish(sl, a.fin[s], false);
-                } else {
-                    sl.phase = PH_FWD;
-                    sl.op = OP_FENTRY;
-                    sl.gamma = wsum;  // gamma at PI-Push entry (push_engine.py:222)
-                    sl.mass_prev = wsum;
-                    sl.defsum = 0.0;
-                    sl.n_p_entry = sl.n_p;
-                    sl.tie_checks = 0;
-                }
-            }
-        } else if (op == OP_PIENTRY0) {
-            sl.last_phase = -1;
-            fin = true;
-            slot_finish(sl, a.fin[s], true);
-        } else if (op == OP_PIENTRY || op == OP_PI) {
-            sl.last_phase = -1;
-            sl.pi_done++;
-            if (sl.pi_done >= sl.pi_t) {
-                fin = true;
-                slot_finish(sl, a.fin[s], true);
-            } else {
-                sl.op = OP_PI;
-            }
-        }
+        const bool fin = slot_transition(sl, op, red, a.alpha, a.budget_scale, a.log_decay, a.fin[s]);
         const bool free_now = fin || sl.op == OP_IDLE;
         if (free_now) sl.qidx = fin ? sl.qidx : -1;
         a.slots[s] = sl;

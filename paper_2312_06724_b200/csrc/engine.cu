@@ -19,6 +19,7 @@
 #include "control.cuh"
 #include "kernels.cuh"
 #include "topk.cuh"
+#include "small.cuh"
 
 namespace bh {
 // BH_TRACE_E2E diagnostics: host timestamps (us) of the stages of a host-pointer batch
@@ -741,8 +742,184 @@ struct Engine final : EngineBase {
 };
 
 // ---------------------------------------------------------------------------
+// Small-graph path (small.cuh): one CTA per query, the whole state machine in
+// one launch.  Used for BHPP jobs without a round hook when the per-query
+// state fits in shared memory.
+static bool small_disabled() {
+    static const bool off = getenv("BH_NO_SMALL") != nullptr && atoi(getenv("BH_NO_SMALL")) != 0;
+    return off;
+}
+
+template <typename T>
+struct SmallEngine final : EngineBase {
+    bh_graph *g;
+    SmallPlan plan;
+    double *led_r = nullptr, *led_est = nullptr;  // single-query ledger (caller order)
+    cudaStream_t pending = nullptr;
+    int32_t *h_err = nullptr;
+
+    // Work items of one side: rows in chunks of <= SMALL_CHUNK edges, longest first.
+    static void build_items(const Side &sd, SmallItem *&d_items, int32_t &n_items, SmallSplit *&d_split,
+                            int32_t &n_split, int32_t &n_parts) {
+        std::vector<SmallItem> items;
+        std::vector<SmallSplit> split;
+        int32_t parts = 0;
+        for (int64_t r = 0; r < sd.n_rows; r++) {
+            const int64_t e0 = sd.h_indptr[r], d = sd.h_indptr[r + 1] - e0;
+            if (d <= SMALL_CHUNK) {
+                items.push_back({(int32_t)r, (int32_t)d, e0, -1, 0});
+                continue;
+            }
+            const int32_t np = (int32_t)((d + SMALL_CHUNK - 1) / SMALL_CHUNK);
+            split.push_back({(int32_t)r, parts, np, 0});
+            for (int32_t c = 0; c < np; c++)
+                items.push_back({(int32_t)r, (int32_t)std::min<int64_t>(SMALL_CHUNK, d - (int64_t)c * SMALL_CHUNK),
+                                 e0 + (int64_t)c * SMALL_CHUNK, parts + c, 0});
+            parts += np;
+        }
+        std::stable_sort(items.begin(), items.end(), [](const SmallItem &x, const SmallItem &y) { return x.len > y.len; });
+        n_items = (int32_t)items.size();
+        n_split = (int32_t)split.size();
+        n_parts = parts;
+        d_items = dalloc<SmallItem>(std::max<size_t>(1, items.size()));
+        d_split = dalloc<SmallSplit>(std::max<size_t>(1, split.size()));
+        if (!items.empty())
+            BH_CUDA(cudaMemcpy(d_items, items.data(), items.size() * sizeof(SmallItem), cudaMemcpyHostToDevice));
+        if (!split.empty())
+            BH_CUDA(cudaMemcpy(d_split, split.data(), split.size() * sizeof(SmallSplit), cudaMemcpyHostToDevice));
+    }
+
+    static size_t smem_for(const bh_graph *g, int32_t parts) {
+        return SmallSmem<T>::bytes(g->n_u, g->n_v, parts);
+    }
+
+    explicit SmallEngine(bh_graph *graph) : g(graph) {
+        this->nslots = 1;
+        build_items(g->V, plan.items_v, plan.n_items_v, plan.split_v, plan.n_split_v, plan.n_parts_v);
+        build_items(g->U, plan.items_u, plan.n_items_u, plan.split_u, plan.n_split_u, plan.n_parts_u);
+        plan.smem = smem_for(g, std::max(plan.n_parts_v, plan.n_parts_u));
+        BH_CUDA(cudaFuncSetAttribute(k_small_query<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem));
+        int occ = 0, sms = 148;
+        BH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_small_query<T>, SMALL_THREADS, plan.smem));
+        BH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
+        if (occ < 1) throw CudaError("small path: no resident CTA");
+        plan.grid_cap = occ * sms;
+        plan.error = dalloc<int32_t>(1);
+        plan.ctl = dalloc<Control>(1);
+        led_r = dalloc<double>(g->n_u);
+        led_est = dalloc<double>(g->n_u);
+        BH_CUDA(cudaMallocHost(&h_err, 2 * sizeof(int32_t)));
+    }
+    ~SmallEngine() override {
+        plan.free_all();
+        cudaFree(led_r);
+        cudaFree(led_est);
+        if (h_err) cudaFreeHost(h_err);
+    }
+
+    // Eligible graphs: the state of one query fits in a CTA's shared memory.
+    static bool fits(const bh_graph *g) {
+        if (small_disabled() || g->n_e > 4000000) return false;
+        int64_t parts = 0;
+        for (const Side *sd : {&g->U, &g->V}) {
+            int64_t p = 0;
+            for (int64_t r = 0; r < sd->n_rows; r++) {
+                const int64_t d = sd->h_indptr[r + 1] - sd->h_indptr[r];
+                if (d > SMALL_CHUNK) p += (d + SMALL_CHUNK - 1) / SMALL_CHUNK;
+            }
+            parts = std::max(parts, p);
+        }
+        const size_t static_smem = sizeof(SelectSmem) + TOPK_MAX * 16 + 1024 + sizeof(Slot) + sizeof(Finish);
+        return smem_for(g, (int32_t)parts) + static_smem <= 200 * 1024;
+    }
+
+    void run(const RunSpec &rs, cudaStream_t st) override {
+        if (rs.k > TOPK_MAX) throw InvalidArg("k exceeds the device top-k limit (1024) of bh_query_batch");
+        SmallArgs<T> a{};
+        a.n_u = g->n_u;
+        a.n_v = g->n_v;
+        a.n_e = g->n_e;
+        a.u_ptr = g->U.indptr;
+        a.v_ptr = g->V.indptr;
+        a.u_col = g->U.indices;
+        a.v_col = g->V.indices;
+        a.u_val = (const T *)g->U.vals;
+        a.v_val = (const T *)g->V.vals;
+        a.deg_u = g->U.deg;
+        a.ws_u = g->ws_u;
+        a.inv_ws_u = g->inv_ws_u;
+        a.perm_u = g->U.perm;
+        a.items_v = plan.items_v;
+        a.items_u = plan.items_u;
+        a.split_v = plan.split_v;
+        a.split_u = plan.split_u;
+        a.n_items_v = plan.n_items_v;
+        a.n_items_u = plan.n_items_u;
+        a.n_split_v = plan.n_split_v;
+        a.n_split_u = plan.n_split_u;
+        a.n_parts_v = plan.n_parts_v;
+        a.n_parts_u = plan.n_parts_u;
+        ControlArgs &ca = a.ca;
+        ca.ctl = plan.ctl;
+        ca.sources = rs.sources;
+        ca.inv_u = g->U.inv;
+        ca.trace = rs.trace;
+        ca.tie_skip = rs.tie;
+        ca.ws_u = g->ws_u;
+        ca.n_u = g->n_u;
+        ca.alpha = rs.alpha;
+        ca.lam = rs.lam;
+        ca.eps_b = rs.eps_b;
+        ca.eps_f = rs.eps_f;
+        ca.budget_scale = 2.0 * (double)g->n_e;
+        ca.log_decay = std::log(1.0 / (1.0 - rs.alpha));
+        ca.job = rs.job;
+        a.n_q = (int32_t)rs.n_q;
+        a.k = rs.k;
+        a.exclude = rs.exclude;
+        a.want_scores = rs.want_scores;
+        a.topk_idx = rs.topk_idx;
+        a.topk_score = rs.topk_score;
+        a.trace = rs.trace;
+        a.scores = rs.want_scores ? rs.scores : nullptr;
+        a.ledger_r = rs.n_q == 1 ? led_r : nullptr;
+        a.ledger_est = rs.n_q == 1 ? led_est : nullptr;
+        a.max_rounds = 100000000;
+        a.error = plan.error;
+        BH_CUDA(cudaMemsetAsync(plan.error, 0, sizeof(int32_t), st));
+        BH_CUDA(cudaMemsetAsync(plan.ctl, 0, sizeof(Control), st));
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(rs.n_q, plan.grid_cap));
+        k_small_query<T><<<grid, SMALL_THREADS, plan.smem, st>>>(a);
+        count_launch();
+        BH_CUDA(cudaGetLastError());
+        BH_CUDA(cudaMemcpyAsync(h_err, plan.error, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        BH_CUDA(cudaMemcpyAsync(h_err + 1, &plan.ctl->error, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        stats = bh_run_stats{};
+        stats.slots = 1;
+        stats.launches = 1;
+        pending = st;
+        if (!rs.async) finish();
+    }
+    void finish() override {
+        if (!pending) return;
+        cudaStream_t st = pending;
+        pending = nullptr;
+        BH_CUDA(cudaStreamSynchronize(st));
+        if (h_err[1] == 2) throw InvalidArg("node index out of range");
+        if (h_err[0]) throw CudaError("query batch did not terminate");
+    }
+    void read_ledger(int, double *r_dev, double *est_dev, cudaStream_t st) override {
+        BH_CUDA(cudaMemcpyAsync(r_dev, led_r, g->n_u * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        BH_CUDA(cudaMemcpyAsync(est_dev, led_est, g->n_u * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    }
+    void slot_state(int, Slot *, cudaStream_t) override { throw CudaError("small path has no round hook"); }
+};
+
+// ---------------------------------------------------------------------------
 struct EngineCache {
     std::map<int, std::unique_ptr<EngineBase>> by_b;
+    std::unique_ptr<EngineBase> small;  // small-graph path (one CTA per query), when eligible
+    int small_ok = -1;                  // -1 unknown, 0 not eligible, 1 eligible
     EngineBase *last = nullptr;
     EngineBase *pending = nullptr;  // engine of an un-finished BH_QUERY_ASYNC batch
     cudaStream_t stream = nullptr;
@@ -762,6 +939,7 @@ struct EngineCache {
     size_t cap_stage = 0;
     ~EngineCache() {
         by_b.clear();
+        small.reset();
         if (h_stage) cudaFreeHost(h_stage);
         cudaFree(d_src); cudaFree(d_tie); cudaFree(d_tk_idx); cudaFree(d_tk_sc);
         cudaFree(d_trace); cudaFree(d_scores); cudaFree(d_vec_a); cudaFree(d_vec_b);
@@ -829,6 +1007,21 @@ static EngineBase &engine_for(bh_graph *g, int B) {
     EngineBase *e = g->dtype == BH_DTYPE_F32 ? make_engine<float>(g, B) : make_engine<double>(g, B);
     c.by_b[B].reset(e);
     return *e;
+}
+
+// The small-graph engine of g, or null when g's state does not fit a CTA.
+static EngineBase *small_engine(bh_graph *g) {
+    EngineCache &c = cache_of(g);
+    if (c.small_ok < 0) {
+        const bool ok = g->dtype == BH_DTYPE_F32 ? SmallEngine<float>::fits(g) : SmallEngine<double>::fits(g);
+        c.small_ok = ok ? 1 : 0;
+    }
+    if (!c.small_ok || small_disabled()) return nullptr;
+    if (!c.small) {
+        if (g->dtype == BH_DTYPE_F32) c.small.reset(new SmallEngine<float>(g));
+        else c.small.reset(new SmallEngine<double>(g));
+    }
+    return c.small.get();
 }
 
 static void check_params(double alpha, double eps_b, double eps_f, double lam) {
@@ -1094,8 +1287,9 @@ int bh_query_batch(bh_graph *g, const bh_query_params *p, const int32_t *sources
             e0->finish();
         }
         cudaStream_t st = stream ? (cudaStream_t)stream : c.stream;
-        const int B = p->slots > 0 ? p->slots : auto_slots(g, n_q);
-        EngineBase &e = engine_for(g, B);
+        EngineBase *sm = p->slots > 0 ? nullptr : small_engine(g);
+        const int B = sm ? 1 : p->slots > 0 ? p->slots : auto_slots(g, n_q);
+        EngineBase &e = sm ? *sm : engine_for(g, B);
         c.last = &e;
         RunSpec rs{};
         rs.job = BH_JOB_BHPP;
@@ -1222,7 +1416,9 @@ int bh_push_run(bh_graph *g, int32_t job, int32_t source, double alpha, double l
         EngineCache &c = cache_of(g);
         g_tstamp[0] = host_us();
         cudaStream_t st = c.stream;
-        EngineBase &e = engine_for(g, 1);
+        EngineBase *sm = job == BH_JOB_BHPP && !hook ? small_engine(g) : nullptr;
+        EngineBase &e = sm ? *sm : engine_for(g, 1);
+        c.last = &e;
         const int64_t nu = g->n_u;
         grow(c.d_src, c.cap_q, 1);
         grow(c.d_trace, c.cap_tr, 1);

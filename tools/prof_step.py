@@ -23,7 +23,7 @@ ap.add_argument("--slots", type=int, default=0)
 ap.add_argument("--n", type=int, default=0)
 a = ap.parse_args()
 cfg = CONFIGS[a.config]
-g = make_graph(cfg)
+g = make_graph(cfg, device=0)
 meta = bh.build_index_meta(g, cfg.alpha)
 src = bench_sources(cfg.u_count, a.n or cfg.n_sources or 64)
 eps = cfg.epsilons[0]
