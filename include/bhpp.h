@@ -81,6 +81,10 @@ typedef struct bh_trace {
     int32_t source;      /* U index of the query                          */
     int32_t status;      /* 0 ok, BH_EINVAL: source out of range (device  */
                          /* pointer batches; the batch returns BH_EINVAL) */
+    int32_t near_ties;   /* budget checks (Eq. 10 / Eq. 12) decided with a */
+                         /* relative margin below 1e-12   */
+    int32_t pad;
+    double min_margin;   /* smallest relative margin of any budget check   */
 } bh_trace;
 
 typedef struct bh_query_params {

@@ -45,13 +45,15 @@ class Trace(C.Structure):
         ("term_b", C.c_int32), ("term_f", C.c_int32),
         ("tie_checks", C.c_int32), ("tie_broke", C.c_int32),
         ("source", C.c_int32), ("status", C.c_int32),
+        ("near_ties", C.c_int32), ("pad", C.c_int32), ("min_margin", C.c_double),
     ]
 
 
 TRACE_DTYPE = np.dtype([
     ("sel_b", "<i8"), ("seq_b", "<i8"), ("n_p_b", "<i8"), ("sel_f", "<i8"), ("pi_iters", "<i8"),
     ("n_p_f", "<i8"), ("gamma", "<f8"), ("term_b", "<i4"), ("term_f", "<i4"), ("tie_checks", "<i4"),
-    ("tie_broke", "<i4"), ("source", "<i4"), ("status", "<i4"),
+    ("tie_broke", "<i4"), ("source", "<i4"), ("status", "<i4"), ("near_ties", "<i4"), ("pad", "<i4"),
+    ("min_margin", "<f8"),
 ])
 assert TRACE_DTYPE.itemsize == C.sizeof(Trace)
 
@@ -288,5 +290,6 @@ def trace_dicts(tr) -> tuple[dict, dict, dict]:
         "gamma": float(tr["gamma"]),
         "terminated_by": TERMINATIONS[int(tr["term_f"])],
     }
-    extra = {"tie_checks": int(tr["tie_checks"]), "tie_broke": int(tr["tie_broke"])}
+    extra = {"tie_checks": int(tr["tie_checks"]), "tie_broke": int(tr["tie_broke"]),
+             "near_ties": int(tr["near_ties"]), "min_budget_margin": float(tr["min_margin"])}
     return back, fwd, extra

@@ -182,6 +182,8 @@ struct Slot {
     double ysc;             // y0 = residue * ysc in power iteration
     double theta_c;         // eps_f / lam
     double eps_b, eps_f;
+    int32_t near_ties;      // budget checks with relative margin < 1e-12
+    double min_margin;      // smallest relative budget margin seen
 };
 
 // Finished-query record written by K4 for the finalize kernels.

@@ -70,6 +70,7 @@ __device__ bool slot_start(Slot &sl, const ControlArgs &a, int32_t q) {
     sl.eps_b = a.eps_b;
     sl.eps_f = a.eps_f;
     sl.theta_c = a.eps_f / a.lam;
+    sl.min_margin = 1.0 / 0.0;
     sl.ysc = sl.inv_ws_q;
     sl.last_phase = -1;
     sl.budget = a.job != BH_JOB_SELECTIVE;
@@ -114,8 +115,19 @@ __device__ void slot_finish(Slot &sl, Finish &f, bool has_pi) {
     t.tie_broke = sl.tie_broke;
     t.source = sl.src_orig;
     t.status = 0;
+    t.near_ties = sl.near_ties;
+    t.min_margin = sl.min_margin;
     sl.phase = PH_DONE;
     sl.op = OP_IDLE;
+}
+
+// Near-tie log (SURVEY.md section 7 hard part 1(d)): every budget comparison
+// lhs >=/<= rhs records its margin relative to `scale`; those below 1e-12 are
+// counted in the trace (a rounding-order change could flip them).
+__device__ __forceinline__ void note_margin(Slot &sl, double lhs, double rhs, double scale) {
+    const double m = fabs(lhs - rhs) / fmax(fabs(scale), 1.0);
+    if (m < sl.min_margin) sl.min_margin = m;
+    if (m < 1e-12) sl.near_ties++;
 }
 
 // Reductions of one slot's round (K1 push statistics, K2 n_p, K1a exit tests).
@@ -160,16 +172,20 @@ __device__ bool slot_transition(Slot &sl, int op, const RoundRed &red, double al
             } else if (sum <= 0.0) {
                 sl.term_b = BH_TERM_DRAINED;
                 end_backward = true;
-            } else if ((double)sl.n_p >= budget_scale * (log(1.0 / sum) / log_decay)) {
-                if (sum > sl.eps_b) {  // any is true here
-                    sl.op = OP_SEQ;
-                    sl.phase = PH_SEQ;
-                } else {
-                    sl.term_b = BH_TERM_BUDGET;
-                    end_backward = true;
-                }
             } else {
-                sl.op = OP_BSEL;
+                const double rhs = budget_scale * (log(1.0 / sum) / log_decay);  // Eq. 10
+                note_margin(sl, (double)sl.n_p, rhs, rhs);
+                if ((double)sl.n_p >= rhs) {
+                    if (sum > sl.eps_b) {  // any is true here
+                        sl.op = OP_SEQ;
+                        sl.phase = PH_SEQ;
+                    } else {
+                        sl.term_b = BH_TERM_BUDGET;
+                        end_backward = true;
+                    }
+                } else {
+                    sl.op = OP_BSEL;
+                }
             }
         } else if (op == OP_SEQ) {
             sl.seq_b += worked;
@@ -222,7 +238,9 @@ __device__ bool slot_transition(Slot &sl, int op, const RoundRed &red, double al
                         brk = false;
                     }
                 } else {
-                    brk = (double)(limit - used) <= budget_scale * sl.defsum / log_decay;
+                    const double rhs = budget_scale * sl.defsum / log_decay;
+                    note_margin(sl, (double)(limit - used), rhs, (double)limit);
+                    brk = (double)(limit - used) <= rhs;
                 }
                 if (brk) {
                     sl.term_f = BH_TERM_BUDGET;

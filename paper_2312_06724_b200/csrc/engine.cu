@@ -1075,7 +1075,8 @@ __global__ void k_gate(const int32_t *flag) {
 extern "C" {
 
 const char *bh_last_error(void) { return t_err.c_str(); }
-int bh_version(void) { return 1; }
+static_assert(sizeof(bh_trace) == 96, "bh_trace layout (include/bhpp.h)");
+int bh_version(void) { return 2; }
 int64_t bh_kernel_launches(void) { return g_launches.load(); }
 
 int bh_csr_build(int64_t n_u, int64_t n_v, int64_t n_e, const int64_t *edge_u, const int64_t *edge_v,

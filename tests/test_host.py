@@ -31,13 +31,13 @@ def test_library_exports_every_header_symbol():
     for name in names:
         assert hasattr(lib, name), f"libbhpp.so does not export {name}"
     assert set(_capi.EXPORTS) == set(names)
-    assert lib.bh_version() == 1
+    assert lib.bh_version() == 2
 
 
 def test_struct_layouts_match_header():
     import ctypes as C
 
-    assert C.sizeof(_capi.Trace) == 80
+    assert C.sizeof(_capi.Trace) == 96
     assert C.sizeof(_capi.QueryParams) == 56
     assert C.sizeof(_capi.GraphInfo) == 56
     assert C.sizeof(_capi.RunStats) == 64
