@@ -295,7 +295,22 @@ struct Engine final : EngineBase {
             return k_pull_sw<B, T, SIDE>;
         }
     }
-    static PullFn pull_kernel(int side) { return side == SIDE_V ? sw_kernel<SIDE_V>() : sw_kernel<SIDE_U>(); }
+    // A/B of the pull geometry for 64 fp32 slots (BH_PULL_CFG = "S,MINB", both sides)
+    template <int SIDE>
+    static PullFn ab_kernel(const char *m) {
+        if constexpr (B == 64 && sizeof(T) == 4) {
+            const std::string v(m);
+            if (v == "10,3") return k_pull_sw<B, T, SIDE, 10, 3>;
+            if (v == "12,3") return k_pull_sw<B, T, SIDE, 12, 3>;
+            if (v == "16,2") return k_pull_sw<B, T, SIDE, 16, 2>;
+            if (v == "8,4") return k_pull_sw<B, T, SIDE, 8, 4>;
+        }
+        return sw_kernel<SIDE>();
+    }
+    static PullFn pull_kernel(int side) {
+        if (const char *m = getenv("BH_PULL_CFG")) return side == SIDE_V ? ab_kernel<SIDE_V>(m) : ab_kernel<SIDE_U>(m);
+        return side == SIDE_V ? sw_kernel<SIDE_V>() : sw_kernel<SIDE_U>();
+    }
 
     explicit Engine(bh_graph *graph) : g(graph) {
         this->nslots = B;
@@ -798,7 +813,15 @@ struct SmallEngine final : EngineBase {
         build_items(g->V, plan.items_v, plan.n_items_v, plan.split_v, plan.n_split_v, plan.n_parts_v);
         build_items(g->U, plan.items_u, plan.n_items_u, plan.split_u, plan.n_split_u, plan.n_parts_u);
         plan.smem = smem_for(g, std::max(plan.n_parts_v, plan.n_parts_u));
-        BH_CUDA(cudaFuncSetAttribute(k_small_query<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem));
+        // one process-wide ceiling for the kernel (a per-graph value would break the
+        // launches of other graphs' engines): everything the opt-in limit leaves
+        cudaFuncAttributes fa{};
+        BH_CUDA(cudaFuncGetAttributes(&fa, k_small_query<T>));
+        int optin = 0;
+        BH_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
+        const int ceiling = optin - (int)fa.sharedSizeBytes;
+        if ((int64_t)plan.smem > ceiling) throw CudaError("small path: shared memory plan exceeds the device limit");
+        BH_CUDA(cudaFuncSetAttribute(k_small_query<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, ceiling));
         int occ = 0, sms = 148;
         BH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_small_query<T>, SMALL_THREADS, plan.smem));
         BH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));

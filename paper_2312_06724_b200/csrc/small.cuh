@@ -98,20 +98,43 @@ struct SmallSmem {
     }
 };
 
-__device__ __forceinline__ void small_block_sum(double &x, double *buf) {
+// Block sums of N values at once (fixed shuffle tree, then warp partials in
+// warp order): two barriers for all N.  buf: N * (warps + 1) doubles.
+template <int N>
+__device__ __forceinline__ void small_block_sums(double (&x)[N], double *buf) {
+    constexpr int NW = SMALL_THREADS / 32;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
-    if (lane == 0) buf[w] = x;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int i = 0; i < SMALL_THREADS / 32; i++) t += buf[i];
-        buf[SMALL_THREADS / 32] = t;
+    for (int i = 0; i < N; i++) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x[i] += __shfl_down_sync(0xffffffffu, x[i], o);
+        if (lane == 0) buf[i * (NW + 1) + w] = x[i];
     }
     __syncthreads();
-    x = buf[SMALL_THREADS / 32];
+    if (threadIdx.x < N) {
+        double t = 0.0;
+        for (int j = 0; j < NW; j++) t += buf[threadIdx.x * (NW + 1) + j];
+        buf[threadIdx.x * (NW + 1) + NW] = t;
+    }
     __syncthreads();
+#pragma unroll
+    for (int i = 0; i < N; i++) x[i] = buf[i * (NW + 1) + NW];
+}
+
+// Marks the other-side endpoints of the edges of every active row (bitmap
+// `act_rows`) in `act_cols`, walking the side's chunked item list so a hub row's
+// edges are spread over many threads.
+__device__ __forceinline__ void small_mark(const SmallItem *__restrict__ items, int n_items,
+                                           const int32_t *__restrict__ col, const uint32_t *act_rows,
+                                           uint32_t *act_cols) {
+    for (int it = threadIdx.x; it < n_items; it += SMALL_THREADS) {
+        const SmallItem w = items[it];
+        if (!((act_rows[w.row >> 5] >> (w.row & 31)) & 1u)) continue;
+        for (int64_t e = w.e0; e < w.e0 + w.len; e++) {
+            const int32_t c = __ldg(col + e);
+            atomicOr(&act_cols[c >> 5], 1u << (c & 31));
+        }
+    }
 }
 
 template <typename T>
@@ -120,7 +143,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_query(SmallArgs<T> a) {
     __shared__ SelectSmem sel;
     __shared__ uint64_t skey[TOPK_MAX];
     __shared__ int64_t sidx[TOPK_MAX];
-    __shared__ double red_d[SMALL_THREADS / 32 + 1];
+    __shared__ double red_d[3 * (SMALL_THREADS / 32 + 1)];
     __shared__ Slot s_slot;
     __shared__ Finish s_done;
     __shared__ int32_t s_fin, s_sparse_v, s_sparse_u;
@@ -163,11 +186,12 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_query(SmallArgs<T> a) {
             const double thDp = fwdlike || o == OP_SEQ ? 0.0 : sl.eps_b;
             const double thDa = fwdlike ? 0.0 : sl.eps_b;
             // ---- K1: push decision, pushed vector, |A|, sum deg(A), left-behind mass
-            for (int i = tid; i < nwu; i += SMALL_THREADS) act_u[i] = 0u;
             for (int i = tid; i < nwv; i += SMALL_THREADS) act_v[i] = 0u;
-            __syncthreads();
             double cnt = 0.0, npu = 0.0, left = 0.0;
-            for (int64_t u = tid; u < nu; u += SMALL_THREADS) {
+            for (int64_t ub = 0; ub < nu; ub += SMALL_THREADS) {  // warp-uniform trip count: ballots below
+                const int64_t u = ub + tid;
+                bool nz = false;
+                if (u < nu) {
                 const double iws = a.inv_ws_u[u];
                 const double r = init ? (u == sl.src ? 1.0 : 0.0) : (double)R[u];
                 const double th = fma(thA * iws, thC, thDp);
@@ -182,23 +206,24 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_query(SmallArgs<T> a) {
                     R[u] = pushed ? (T)0 : (T)r;
                     EST[u] = (T)(pushed ? 0.0 + alpha * r : 0.0);
                 }
-                if ((double)P[u] != 0.0) atomicOr(&act_u[u >> 5], 1u << (u & 31));
+                nz = (double)P[u] != 0.0;
+                }
+                const uint32_t bal = __ballot_sync(0xffffffffu, nz);  // 32 consecutive nodes per warp
+                if ((tid & 31) == 0 && u < nu) act_u[u >> 5] = bal;
             }
-            small_block_sum(cnt, red_d);
-            small_block_sum(npu, red_d);
-            small_block_sum(left, red_d);
+            {
+                double x[3] = {cnt, npu, left};
+                small_block_sums<3>(x, red_d);
+                cnt = x[0];
+                npu = x[1];
+                left = x[2];
+            }
             // frontier form when the pushed rows are light (push_engine.py:44, 297)
             if (tid == 0) s_sparse_v = npu <= 0.25 * (double)a.n_e && !(o == OP_PI || o == OP_PIENTRY);
             __syncthreads();
             const bool sparse = s_sparse_v;
             if (sparse) {  // N(A): walk the pushed rows' U-CSR edges
-                for (int64_t u = tid; u < nu; u += SMALL_THREADS) {
-                    if (!((act_u[u >> 5] >> (u & 31)) & 1u)) continue;
-                    for (int64_t e = a.u_ptr[u]; e < a.u_ptr[u + 1]; e++) {
-                        const int32_t v = a.u_col[e];
-                        atomicOr(&act_v[v >> 5], 1u << (v & 31));
-                    }
-                }
+                small_mark(a.items_u, a.n_items_u, a.u_col, act_u, act_v);
                 __syncthreads();
             }
             // ---- K2: V pull  XV[v] = (1 - alpha) sum_u (w / ws_v) P[u];  n_p += deg(v) for XV > 0
@@ -237,22 +262,25 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_query(SmallArgs<T> a) {
                 }
                 __syncthreads();
             }
-            small_block_sum(npv, red_d);
-            small_block_sum(xdeg, red_d);
+            {
+                double x[2] = {npv, xdeg};
+                small_block_sums<2>(x, red_d);
+                npv = x[0];
+                xdeg = x[1];
+            }
             // U rows to visit: neighbours of the non-zero V rows (walk cost xdeg)
             if (tid == 0) s_sparse_u = sparse && xdeg <= 0.25 * (double)a.n_e;
             __syncthreads();
             const bool sparse_u = s_sparse_u;
-            if (sparse_u) {
+            if (sparse_u) {  // rows of the non-zero V rows (bitmap by ballot), then their U neighbours
                 for (int i = tid; i < nwu; i += SMALL_THREADS) act_u[i] = 0u;
-                __syncthreads();
-                for (int64_t v = tid; v < nv; v += SMALL_THREADS) {
-                    if ((double)XV[v] == 0.0) continue;
-                    for (int64_t e = a.v_ptr[v]; e < a.v_ptr[v + 1]; e++) {
-                        const int32_t u = a.v_col[e];
-                        atomicOr(&act_u[u >> 5], 1u << (u & 31));
-                    }
+                for (int64_t vb = 0; vb < nv; vb += SMALL_THREADS) {
+                    const int64_t v = vb + tid;
+                    const uint32_t bal = __ballot_sync(0xffffffffu, v < nv && (double)XV[v] != 0.0);
+                    if ((tid & 31) == 0 && v < nv) act_v[v >> 5] = bal;
                 }
+                __syncthreads();
+                small_mark(a.items_v, a.n_items_v, a.v_col, act_v, act_u);
             }
             __syncthreads();
             // ---- K3: U pull  Y[u] = sum_v (w / ws_u) XV[v]
@@ -298,9 +326,13 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_query(SmallArgs<T> a) {
                     if (r > fma(tA, thC, thDa)) anyd = 1.0;
                 }
             }
-            small_block_sum(sum, red_d);
-            small_block_sum(wsum, red_d);
-            small_block_sum(anyd, red_d);
+            {
+                double x[3] = {sum, wsum, anyd};
+                small_block_sums<3>(x, red_d);
+                sum = x[0];
+                wsum = x[1];
+                anyd = x[2];
+            }
             // ---- K4: the query's state transition (thread 0)
             if (tid == 0) {
                 RoundRed red;
