@@ -218,10 +218,20 @@ typedef struct bh_run_stats {
     double ms_vpull;       /* sum of K2 + K2b (V pull) durations                 */
     double ms_upull;       /* sum of K3 + K3b (U pull) durations                 */
     double ms_control;     /* sum of K4..K6 (control, finalize, top-k)           */
+    int64_t frontier_rounds;   /* rounds whose V half ran in frontier form (K-F) */
+    int64_t frontier_u_rounds; /* rounds whose U half ran in frontier form       */
 } bh_run_stats;
 /* on != 0: bracket every round's kernels with CUDA events on the launch stream
  * (process-wide switch; costs one event record per kernel group). */
 int bh_set_profiling(int32_t on);
+/* Frontier rounds (K-F), process-wide: a round pulls only the rows reachable
+ * from its pushed set when the pushed rows (summed over the block's slots)
+ * touch at most fraction * |E| edges; its U half likewise on the V rows it
+ * reached.  Mirrors push_engine._SCATTER_LIMIT (push_engine.py:44, 297, 315;
+ * default 0.25).  fraction < 0: never; >= 1: whenever no slot is in power
+ * iteration.  Results do not depend on it (every visited row is summed in
+ * full); it only changes which rows a round visits. */
+int bh_set_scatter_limit(double fraction);
 /* Measurement gate: enqueue on `stream` a one-thread kernel that spins until
  * *flag (host-mapped pinned memory) becomes nonzero, so a batch can be fully
  * enqueued before the device starts it and device timing excludes host

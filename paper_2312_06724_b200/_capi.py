@@ -32,7 +32,7 @@ EXPORTS = (
     "bh_power_iteration", "bh_topk", "bh_last_error", "bh_version", "bh_kernel_launches",
     "bh_set_profiling", "bh_last_run_stats", "bh_csr_build", "bh_query_wait", "bh_stream_gate",
     "bh_edge_list_parse", "bh_edge_list_sizes", "bh_edge_list_export", "bh_edge_list_free",
-    "bh_alias_create", "bh_monte_carlo", "bh_alias_destroy", "bh_alias_build",
+    "bh_alias_create", "bh_monte_carlo", "bh_alias_destroy", "bh_alias_build", "bh_set_scatter_limit",
 )
 QUERY_ASYNC = 1
 
@@ -78,6 +78,7 @@ class RunStats(C.Structure):
     _fields_ = [
         ("rounds", C.c_int64), ("launches", C.c_int64), ("slots", C.c_int64), ("profiled", C.c_int64),
         ("ms_prep", C.c_double), ("ms_vpull", C.c_double), ("ms_upull", C.c_double), ("ms_control", C.c_double),
+        ("frontier_rounds", C.c_int64), ("frontier_u_rounds", C.c_int64),
     ]
 
 
@@ -123,6 +124,8 @@ def lib():
         L.bh_kernel_launches.restype = C.c_int64
         L.bh_set_profiling.restype = C.c_int
         L.bh_set_profiling.argtypes = [C.c_int32]
+        L.bh_set_scatter_limit.restype = C.c_int
+        L.bh_set_scatter_limit.argtypes = [C.c_double]
         L.bh_last_run_stats.restype = C.c_int
         L.bh_last_run_stats.argtypes = [P, C.POINTER(RunStats)]
         L.bh_edge_list_parse.restype = C.c_int
@@ -231,6 +234,23 @@ class DeviceGraph:
 
 def set_profiling(on: bool) -> None:
     check(lib().bh_set_profiling(1 if on else 0))
+
+
+_applied_limit = None
+
+
+def apply_scatter_limit() -> None:
+    """Hand ``push_engine._SCATTER_LIMIT`` (the reference's module constant,
+    push_engine.py:44, which its tests monkeypatch) to the engine before a run:
+    rounds whose pushed rows touch at most that fraction of |E| run in frontier
+    form (include/bhpp.h bh_set_scatter_limit)."""
+    global _applied_limit
+    from . import push_engine
+
+    lim = float(push_engine._SCATTER_LIMIT)
+    if lim != _applied_limit:
+        check(lib().bh_set_scatter_limit(lim))
+        _applied_limit = lim
 
 
 _graph_cache: dict = {}

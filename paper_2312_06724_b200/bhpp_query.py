@@ -239,6 +239,7 @@ def bhpp_query_batch(g, meta: IndexMeta, sources, epsilon: float, k: int | None 
     import ctypes as C
 
     t0 = time.perf_counter()
+    _capi.apply_scatter_limit()
     _capi.check(_capi.lib().bh_query_batch(
         dg.h, C.byref(prm), _capi.ptr(src), n_q, _capi.ptr(ties), _capi.ptr(tk_idx) if kk else None,
         _capi.ptr(tk_sc) if kk else None, _capi.ptr(traces), _capi.ptr(scores),
@@ -264,6 +265,7 @@ def query_batch_device(dg, meta: IndexMeta, eps_b: float, eps_f: float, sources_
                             exclude_query=int(bool(exclude_query)), want_scores=int(bool(scores_ptr)),
                             slots=int(slots or 0), on_device=1, flags=_capi.QUERY_ASYNC if async_ else 0)
     vp = lambda x: C.c_void_p(x) if x else None  # noqa: E731
+    _capi.apply_scatter_limit()
     _capi.check(_capi.lib().bh_query_batch(dg.h, C.byref(prm), vp(sources_ptr), int(n_q), vp(tie_ptr),
                                            vp(topk_idx_ptr), vp(topk_score_ptr), vp(trace_ptr), vp(scores_ptr),
                                            vp(stream)))

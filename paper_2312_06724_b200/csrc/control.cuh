@@ -116,6 +116,7 @@ __device__ void slot_finish(Slot &sl, Finish &f, bool has_pi) {
     t.source = sl.src_orig;
     t.status = 0;
     t.near_ties = sl.near_ties;
+    t.pad = 0;
     t.min_margin = sl.min_margin;
     sl.phase = PH_DONE;
     sl.op = OP_IDLE;

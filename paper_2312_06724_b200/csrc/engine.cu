@@ -20,6 +20,7 @@
 #include "kernels.cuh"
 #include "topk.cuh"
 #include "small.cuh"
+#include "frontier.cuh"
 
 namespace bh {
 // BH_TRACE_E2E diagnostics: host timestamps (us) of the stages of a host-pointer batch
@@ -131,6 +132,10 @@ struct RunSpec {
 };
 
 static std::atomic<int> g_profiling{0};
+// push_engine._SCATTER_LIMIT (push_engine.py:44): a round runs in frontier form when
+// the pushed rows touch at most this fraction of |E| (bh_set_scatter_limit)
+static std::atomic<double> g_scatter_limit{0.25};
+static double scatter_limit() { return g_scatter_limit.load(); }
 
 struct EngineBase {
     virtual ~EngineBase() = default;
@@ -234,6 +239,25 @@ struct Engine final : EngineBase {
     int32_t *chunk_done = nullptr;
     std::vector<cudaEvent_t> evpool;
     SidePlan plan_v, plan_u;
+    // K-F frontier rounds (frontier.cuh): control block, K1's pushed-node flags,
+    // row bitmaps, work items and split-row partials per side
+    FrontCtl *front = nullptr;
+    FrontCtl *h_front = nullptr;
+    uint8_t *flag_u = nullptr;
+    uint32_t *bits_v = nullptr, *bits_u = nullptr;
+    FrontItem *items_v = nullptr, *items_u = nullptr;
+    double *fscr_v = nullptr, *fscr_u = nullptr;
+    int32_t *pcnt_v = nullptr, *pcnt_u = nullptr;
+    int grid_front = 1;
+    cudaGraphConditionalHandle fcond{};
+    int use_fcond = 0;  // K1 sets the graph's IF/ELSE condition (capture of the batch graph)
+    // Frontier rounds are compiled into a run when the scatter limit allows them
+    // and the block is narrow (B <= FRONT_MAX_B) or the limit forces them (>= 1):
+    // for 32+ slots in mixed phases the union frontier is dense in practically
+    // every round (a slot in power iteration makes it all of U), and the per-round
+    // decision (K1's flags + ticket, the IF/ELSE node) costs ~8 % at c2.
+    static constexpr int FRONT_MAX_B = 16;
+    bool front_on = false;
     // L2 residency of the gathered operands' hub slabs (store rows [0, h) of P for
     // the V pull, of XV for the U pull; degree-ordered store): empty windows
     // unless the operands outgrow L2 (BH_L2_PERSIST_MB overrides the carve-out)
@@ -249,29 +273,19 @@ struct Engine final : EngineBase {
     // Elementwise K1 / K1a geometry (nodes in flight per thread, blocks per SM),
     // measured at c2 on B200 (profiles/r01_pull_variants.md): fp32 K1 one node
     // per thread at 4 blocks/SM, K1a software-pipelined at 3 blocks/SM; fp64 two
-    // nodes per thread at 2 blocks/SM.
-    // When the state outgrows L2 (HBM regime, c3/c4) the same kernels need more
-    // bytes in flight per SM to cover DRAM latency: several nodes per thread.
+    // nodes per thread at 2 blocks/SM.  The same geometry is at least as fast in
+    // the HBM regime (c3: 4-8 nodes per thread measured equal or slower,
+    // profiles/r02_elem_geometry.md), so there is one geometry per dtype.
     using ElemFn = void (*)(ElemArgs<T>);
-    bool hbm = false;   // set in the constructor from the state size vs L2
-    int elem_var = -1;  // BH_ELEM_VAR (A/B): -1 regime default
     ElemFn push_kernel() const {
-        if constexpr (B >= 32) {
-            const int v = elem_var >= 0 ? elem_var : (hbm ? 1 : 0);
-            if (v == 1) return k_push<B, T, 4, 2>;
-            if (v == 2) return k_push<B, T, 2, 4>;
-            if (v == 3) return k_push<B, T, 8, 1>;
+        if (front_on) {
+            if constexpr (sizeof(T) == 4 && B >= 32) return k_push<B, T, 1, 4, false, true>;
+            else return k_push<B, T, 2, 2, false, true>;
         }
         if constexpr (sizeof(T) == 4 && B >= 32) return k_push<B, T, 1, 4>;
         else return k_push<B, T, 2, 2>;
     }
-    ElemFn combine_kernel() const {
-        if constexpr (B >= 32) {
-            const int v = elem_var >= 0 ? elem_var : (hbm ? 1 : 0);
-            if (v == 1) return k_combine<B, T, 4, 2>;
-            if (v == 2) return k_combine<B, T, 2, 4>;
-            if (v == 3) return k_combine<B, T, 8, 1>;
-        }
+    static ElemFn combine_kernel() {
         if constexpr (sizeof(T) == 4 && B >= 32) return k_combine<B, T, 1, 3, true>;
         else return k_combine<B, T, 2, 2>;
     }
@@ -295,22 +309,7 @@ struct Engine final : EngineBase {
             return k_pull_sw<B, T, SIDE>;
         }
     }
-    // A/B of the pull geometry for 64 fp32 slots (BH_PULL_CFG = "S,MINB", both sides)
-    template <int SIDE>
-    static PullFn ab_kernel(const char *m) {
-        if constexpr (B == 64 && sizeof(T) == 4) {
-            const std::string v(m);
-            if (v == "10,3") return k_pull_sw<B, T, SIDE, 10, 3>;
-            if (v == "12,3") return k_pull_sw<B, T, SIDE, 12, 3>;
-            if (v == "16,2") return k_pull_sw<B, T, SIDE, 16, 2>;
-            if (v == "8,4") return k_pull_sw<B, T, SIDE, 8, 4>;
-        }
-        return sw_kernel<SIDE>();
-    }
-    static PullFn pull_kernel(int side) {
-        if (const char *m = getenv("BH_PULL_CFG")) return side == SIDE_V ? ab_kernel<SIDE_V>(m) : ab_kernel<SIDE_U>(m);
-        return side == SIDE_V ? sw_kernel<SIDE_V>() : sw_kernel<SIDE_U>();
-    }
+    static PullFn pull_kernel(int side) { return side == SIDE_V ? sw_kernel<SIDE_V>() : sw_kernel<SIDE_U>(); }
 
     explicit Engine(bh_graph *graph) : g(graph) {
         this->nslots = B;
@@ -333,12 +332,6 @@ struct Engine final : EngineBase {
         BH_CUDA(cudaMemset(ctl, 0, sizeof(Control)));
         int sms = 148;
         BH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
-        {
-            int l2 = 0;
-            BH_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, g->device));
-            hbm = (double)B * sizeof(T) * (4.0 * (double)nu + (double)nv) > (double)l2;
-            if (const char *m = getenv("BH_ELEM_VAR")) elem_var = atoi(m);
-        }
         setup_l2_windows(nu, nv);
         for (int side = 0; side < 2; side++) {
             PullFn fn = pull_kernel(side);
@@ -383,6 +376,27 @@ struct Engine final : EngineBase {
         hook_est = dalloc<double>(nu);
         chunk_done = dalloc<int32_t>(MAX_B);
         BH_CUDA(cudaMemset(chunk_done, 0, MAX_B * sizeof(int32_t)));
+        {  // frontier buffers (FRONT_CHUNK-edge items; a split row of d edges has <= 2 d / CHUNK parts)
+            const int64_t ne = g->n_e, chunks = ne / FRONT_CHUNK + 2, parts = 2 * chunks;
+            front = dalloc<FrontCtl>(1);
+            BH_CUDA(cudaMallocHost(&h_front, sizeof(FrontCtl)));
+            BH_CUDA(cudaMemset(front, 0, sizeof(FrontCtl)));
+            flag_u = dalloc<uint8_t>(nu);
+            BH_CUDA(cudaMemset(flag_u, 0, nu));
+            bits_v = dalloc<uint32_t>((nv + 31) / 32);
+            bits_u = dalloc<uint32_t>((nu + 31) / 32);
+            BH_CUDA(cudaMemset(bits_v, 0, ((nv + 31) / 32) * 4));
+            BH_CUDA(cudaMemset(bits_u, 0, ((nu + 31) / 32) * 4));
+            items_v = dalloc<FrontItem>(nv + chunks);
+            items_u = dalloc<FrontItem>(nu + chunks);
+            fscr_v = dalloc<double>((size_t)parts * B);
+            fscr_u = dalloc<double>((size_t)parts * B);
+            pcnt_v = dalloc<int32_t>(parts);
+            pcnt_u = dalloc<int32_t>(parts);
+            BH_CUDA(cudaMemset(pcnt_v, 0, parts * 4));
+            BH_CUDA(cudaMemset(pcnt_u, 0, parts * 4));
+            grid_front = 4 * sms;
+        }
     }
 
     void setup_l2_windows(int64_t nu, int64_t nv) {
@@ -392,7 +406,11 @@ struct Engine final : EngineBase {
         BH_CUDA(cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, g->device));
         const double row = (double)B * sizeof(T);
         const double operands = row * (double)(nu + nv);
-        double mb = operands > 0.5 * l2 ? 0.5 * l2 / 1048576.0 : 0.0;  // default: half of L2 when outgrown
+        // Off by default: at c3 the carve-out slowed K1 / K1a by 35 % and gained
+        // the pulls 2-5 %, a net loss (profiles/r02_c3_store_ab.md); opt-in with
+        // BH_L2_PERSIST_MB (a carve-out of that size, shared by the two windows)
+        double mb = 0.0;
+        (void)operands;
         if (const char *m = getenv("BH_L2_PERSIST_MB")) mb = atof(m);
         if (!g->relabeled || mb <= 0 || maxp <= 0 || maxwin <= 0) return;
         const size_t carve = std::min<size_t>((size_t)maxp, (size_t)(mb * 1048576.0));
@@ -424,6 +442,8 @@ struct Engine final : EngineBase {
         cudaFree(part.any); cudaFree(part.sum); cudaFree(part.wsum);
         cudaFree(scratch); cudaFree(cand_key); cudaFree(cand_idx);
         cudaFree(hook_r); cudaFree(hook_est); cudaFree(chunk_done);
+        cudaFree(front); cudaFreeHost(h_front); cudaFree(flag_u); cudaFree(bits_v); cudaFree(bits_u);
+        cudaFree(items_v); cudaFree(items_u); cudaFree(fscr_v); cudaFree(fscr_u); cudaFree(pcnt_v); cudaFree(pcnt_u);
         plan_u.free_all();
         plan_v.free_all();
         for (auto e : evpool) cudaEventDestroy(e);
@@ -478,12 +498,7 @@ struct Engine final : EngineBase {
                        side == SIDE_V ? &win_v : &win_u, a);
     }
 
-    // One round: K5 (the slots K4 finished last round) | K1 K2 K3 K1a | K4.  In the
-    // batch graph K5 sits under an IF node on a branch parallel to K1..K1a (a finished
-    // slot is refilled one round later, so nothing else touches its columns meanwhile).
-    void launch_round(const RunSpec &rs, const ControlArgs &ca, const FinalArgs<T> &fa, cudaStream_t st,
-                      int64_t round, bool prof, bool with_k5 = true, bool with_k4 = true) {
-        const size_t e0 = (size_t)round * 7;
+    ElemArgs<T> elem_args(const RunSpec &rs) {
         ElemArgs<T> ea{};
         ea.n_u = g->n_u;
         ea.R = R;
@@ -499,26 +514,118 @@ struct Engine final : EngineBase {
         ea.active = &ctl->active;
         ea.part = part;
         ea.alpha = rs.alpha;
+        ea.front = front_on ? front : nullptr;
+        ea.flag_u = front_on ? flag_u : nullptr;
+        ea.fcond = fcond;
+        ea.use_fcond = use_fcond;
+        return ea;
+    }
+
+    FrontArgs front_args() const {
+        FrontArgs fa{};
+        fa.f = front;
+        fa.active = &ctl->active;
+        fa.B = B;
+        fa.elem_bytes = (int)sizeof(T);
+        fa.n_u = g->n_u;
+        fa.n_v = g->n_v;
+        fa.n_e = g->n_e;
+        fa.u_ptr = g->U.indptr;
+        fa.v_ptr = g->V.indptr;
+        fa.u_col = g->U.indices;
+        fa.v_col = g->V.indices;
+        fa.flag_u = flag_u;
+        fa.bits_v = bits_v;
+        fa.bits_u = bits_u;
+        fa.items_v = items_v;
+        fa.items_u = items_u;
+        fa.XV = XV;
+        fa.Y = Y;
+        return fa;
+    }
+
+    FrontPullArgs<T> front_pull_args(int side, double alpha) const {
+        FrontPullArgs<T> a{};
+        const Side &sd = side == SIDE_V ? g->V : g->U;
+        a.f = front;
+        a.active = &ctl->active;
+        a.indptr = sd.indptr;
+        a.indices = sd.indices;
+        a.vals = (const T *)sd.vals;
+        a.items = side == SIDE_V ? items_v : items_u;
+        a.X = side == SIDE_V ? P : XV;
+        a.Y = side == SIDE_V ? XV : Y;
+        a.scratch = side == SIDE_V ? fscr_v : fscr_u;
+        a.pcnt = side == SIDE_V ? pcnt_v : pcnt_u;
+        a.slots = slots;
+        a.np_v = part.np_v;
+        a.n_warps = plan_v.n_warps;
+        a.scale = side == SIDE_V ? 1.0 - alpha : 1.0;
+        return a;
+    }
+
+    // The V / U halves of a frontier round (Fa Fb Fc | Fd Fe + the dense U pull
+    // when the U half is dense), each kernel gated on FrontCtl.
+    void launch_front_v(double alpha, cudaStream_t st) {
+        const FrontArgs fa = front_args();
+        launch_pdl(k_front_reset, grid_front, 256, 0, st, fa);
+        launch_pdl(k_front_mark<SIDE_V>, grid_front, 256, 0, st, fa);
+        launch_pdl(k_front_pull<B, T, SIDE_V>, plan_v.grid, PULL_THREADS, 0, st, front_pull_args(SIDE_V, alpha));
+        count_launch(3);
+        stats.launches += 3;
+    }
+    void launch_front_u(double alpha, cudaStream_t st) {
+        const FrontArgs fa = front_args();
+        launch_pdl(k_front_mark<SIDE_U>, grid_front, 256, 0, st, fa);
+        launch_pdl(k_front_pull<B, T, SIDE_U>, plan_u.grid, PULL_THREADS, 0, st, front_pull_args(SIDE_U, alpha));
+        PullArgs<T> pu = pull_args(SIDE_U, alpha);
+        pu.active = &front->gate_udense;
+        launch_pull(SIDE_U, pu, st);
+        count_launch(3);
+        stats.launches += 3;
+    }
+    void launch_dense(int side, double alpha, cudaStream_t st) {
+        PullArgs<T> pa = pull_args(side, alpha);
+        if (front_on) pa.active = &front->gate_dense;
+        launch_pull(side, pa, st);
+        count_launch(1);
+        stats.launches += 1;
+    }
+
+    // One round: K5 (the slots K4 finished last round) | K1 K2 K3 K1a | K4.  In the
+    // batch graph K5 sits under an IF node on a branch parallel to K1..K1a (a finished
+    // slot is refilled one round later, so nothing else touches its columns meanwhile),
+    // and the pulls under an IF/ELSE node set by K1 (frontier / dense).  Eagerly, both
+    // forms are launched and gate themselves.
+    void launch_round(const RunSpec &rs, const ControlArgs &ca, const FinalArgs<T> &fa, cudaStream_t st,
+                      int64_t round, bool prof, bool with_k5 = true, bool with_k4 = true) {
+        const size_t e0 = (size_t)round * 7;
+        const ElemArgs<T> ea = elem_args(rs);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0), st));
-        if (with_k5) launch_pdl(k_finalize<T>, grid_k5, TOPK_THREADS, 0, st, fa);
+        if (with_k5) {
+            launch_pdl(k_finalize<T>, grid_k5, TOPK_THREADS, 0, st, fa);
+            count_launch(1);
+            stats.launches += 1;
+        }
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 1), st));
         launch_pdl(push_kernel(), grid_elem, ELEM_THREADS, 0, st, ea);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 2), st));
-        launch_pull(SIDE_V, pull_args(SIDE_V, rs.alpha), st);
+        if (front_on) launch_front_v(rs.alpha, st);
+        launch_dense(SIDE_V, rs.alpha, st);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 3), st));
-        launch_pull(SIDE_U, pull_args(SIDE_U, rs.alpha), st);
+        if (front_on) launch_front_u(rs.alpha, st);
+        launch_dense(SIDE_U, rs.alpha, st);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 4), st));
         launch_pdl(combine_kernel(), grid_comb, ELEM_THREADS, 0, st, ea);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 5), st));
         if (with_k4) launch_pdl(k_control, B, CONTROL_THREADS, 0, st, ca);
         if (prof) BH_CUDA(cudaEventRecord(ev(e0 + 6), st));
-        const int launches = launches_per_round() - (with_k5 ? 0 : 1) - (with_k4 ? 0 : 1);
-        count_launch(launches);
-        stats.launches += launches;
+        const int n = 2 + (with_k4 ? 1 : 0);
+        count_launch(n);
+        stats.launches += n;
         BH_CUDA(cudaGetLastError());
     }
 
-    int launches_per_round() const { return 6; }
 
     void collect_profile(int64_t rounds) {
         // events per round: K5 | K1 | K2 | K3 | K1a | K4
@@ -550,7 +657,7 @@ struct Engine final : EngineBase {
         put(rs.k); put(rs.exclude); put(rs.want_scores); put(rs.topk_idx); put(rs.topk_score); put(rs.trace);
         put(rs.scores);
         put(ca.budget_scale); put(ca.log_decay); put(ca.max_rounds); put(ca.sources); put(ca.tie_skip);
-        put(fa.cand_key); put(fa.cand_idx); put(fa.out_scores); put(fa.chunk_done);
+        put(fa.cand_key); put(fa.cand_idx); put(fa.out_scores); put(fa.chunk_done); put(front_on);
         if (graph_exec && key == graph_key) return;
         if (graph_exec) cudaGraphExecDestroy(graph_exec);
         if (graph) cudaGraphDestroy(graph);
@@ -589,20 +696,65 @@ struct Engine final : EngineBase {
         k_finalize<T><<<grid_k5, TOPK_THREADS, 0, cap_stream>>>(fa);
         BH_CUDA(cudaGetLastError());
         BH_CUDA(cudaStreamEndCapture(cap_stream, &captured));
-        const int64_t launches0 = stats.launches;
-        BH_CUDA(cudaStreamBeginCaptureToGraph(cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-        launch_round(rs, ca, fa, cap_stream, 0, false, /*with_k5=*/false, /*with_k4=*/false);
-        BH_CUDA(cudaStreamUpdateCaptureDependencies(cap_stream, &if_node, 1, cudaStreamAddCaptureDependencies));
-        launch_pdl(k_control, B, CONTROL_THREADS, 0, cap_stream, ca);
-        BH_CUDA(cudaGetLastError());
-        BH_CUDA(cudaStreamEndCapture(cap_stream, &captured));
+        const int64_t launches0 = stats.launches, counted0 = g_launches.load();
+        if (!front_on) {  // body: K1 -> K2 -> K3 -> K1a -> K4 (PDL chain; K4 also waits for the K5 branch)
+            BH_CUDA(cudaStreamBeginCaptureToGraph(cap_stream, body, nullptr, nullptr, 0,
+                                                  cudaStreamCaptureModeThreadLocal));
+            launch_round(rs, ca, fa, cap_stream, 0, false, /*with_k5=*/false, /*with_k4=*/false);
+            BH_CUDA(cudaStreamUpdateCaptureDependencies(cap_stream, &if_node, 1, cudaStreamAddCaptureDependencies));
+            launch_pdl(k_control, B, CONTROL_THREADS, 0, cap_stream, ca);
+            BH_CUDA(cudaGetLastError());
+            BH_CUDA(cudaStreamEndCapture(cap_stream, &captured));
+        } else {
+            // body: K1 -> IF/ELSE (frontier pulls | dense pulls, condition set by K1's last
+            // block) -> K1a -> K4 (K4 also waits for the K5 branch)
+            BH_CUDA(cudaGraphConditionalHandleCreate(&fcond, body, 0, cudaGraphCondAssignDefault));
+            use_fcond = 1;
+            const ElemArgs<T> ea = elem_args(rs);
+            use_fcond = 0;
+            BH_CUDA(cudaStreamBeginCaptureToGraph(cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+            launch_pdl(push_kernel(), grid_elem, ELEM_THREADS, 0, cap_stream, ea);
+            BH_CUDA(cudaGetLastError());
+            cudaStreamCaptureStatus cst;
+            const cudaGraphNode_t *deps = nullptr;
+            size_t n_deps = 0;
+            BH_CUDA(cudaStreamGetCaptureInfo(cap_stream, &cst, nullptr, nullptr, &deps, &n_deps));
+            if (n_deps != 1) throw CudaError("batch graph: K1 capture has no single node");
+            const cudaGraphNode_t k1_node = deps[0];
+            BH_CUDA(cudaStreamEndCapture(cap_stream, &captured));
+            cudaGraphNodeParams pp = {};
+            pp.type = cudaGraphNodeTypeConditional;
+            pp.conditional.handle = fcond;
+            pp.conditional.type = cudaGraphCondTypeIf;
+            pp.conditional.size = 2;  // [0] frontier (condition 1), [1] dense (else)
+            cudaGraphNode_t pull_node;
+            BH_CUDA(cudaGraphAddNode(&pull_node, body, &k1_node, 1, &pp));
+            BH_CUDA(cudaStreamBeginCaptureToGraph(cap_stream, pp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                                  cudaStreamCaptureModeThreadLocal));
+            launch_front_v(rs.alpha, cap_stream);
+            launch_front_u(rs.alpha, cap_stream);
+            BH_CUDA(cudaGetLastError());
+            BH_CUDA(cudaStreamEndCapture(cap_stream, &captured));
+            BH_CUDA(cudaStreamBeginCaptureToGraph(cap_stream, pp.conditional.phGraph_out[1], nullptr, nullptr, 0,
+                                                  cudaStreamCaptureModeThreadLocal));
+            launch_dense(SIDE_V, rs.alpha, cap_stream);
+            launch_dense(SIDE_U, rs.alpha, cap_stream);
+            BH_CUDA(cudaGetLastError());
+            BH_CUDA(cudaStreamEndCapture(cap_stream, &captured));
+            BH_CUDA(cudaStreamBeginCaptureToGraph(cap_stream, body, &pull_node, nullptr, 1, cudaStreamCaptureModeThreadLocal));
+            combine_kernel()<<<grid_comb, ELEM_THREADS, 0, cap_stream>>>(ea);  // after a conditional node: plain edge
+            BH_CUDA(cudaStreamUpdateCaptureDependencies(cap_stream, &if_node, 1, cudaStreamAddCaptureDependencies));
+            launch_pdl(k_control, B, CONTROL_THREADS, 0, cap_stream, ca);
+            BH_CUDA(cudaGetLastError());
+            BH_CUDA(cudaStreamEndCapture(cap_stream, &captured));
+        }
         // after the loop: K5 for the slots the last round finished
         BH_CUDA(cudaStreamBeginCaptureToGraph(cap_stream, graph, &node, nullptr, 1, cudaStreamCaptureModeThreadLocal));
         k_finalize<T><<<grid_k5, TOPK_THREADS, 0, cap_stream>>>(fa);
         BH_CUDA(cudaGetLastError());
         BH_CUDA(cudaStreamEndCapture(cap_stream, &captured));
         stats.launches = launches0;
-        count_launch(-(launches_per_round() - 2));  // launch_round counted K1..K1a: captured, not launched
+        count_launch((int)(counted0 - g_launches.load()));  // captured, not launched (finish() counts them)
         BH_CUDA(cudaGraphInstantiate(&graph_exec, graph, 0));
         graph_key = key;
     }
@@ -616,6 +768,15 @@ struct Engine final : EngineBase {
         c0.n_q = (int32_t)rs.n_q;
         *h_ctl = c0;
         BH_CUDA(cudaMemcpyAsync(ctl, h_ctl, sizeof(Control), cudaMemcpyHostToDevice, st));
+        {  // frontier control: every XV / Y row is stale, the scatter limit of this run
+            const double lim = scatter_limit();
+            front_on = lim >= 0.0 && (B <= FRONT_MAX_B || lim >= 1.0);
+            const int64_t li =
+                lim < 0.0 ? -1 : (lim * (double)g->n_e >= 9.0e18 ? INT64_MAX : (int64_t)(lim * (double)g->n_e));
+            k_front_begin<<<1, 1, 0, st>>>(front, li);
+            count_launch();
+            BH_CUDA(cudaGetLastError());
+        }
 
         ControlArgs ca{};
         ca.slots = slots;
@@ -686,6 +847,7 @@ struct Engine final : EngineBase {
             BH_CUDA(cudaGraphLaunch(graph_exec, st));
             g_tstamp[5] = host_us();
             BH_CUDA(cudaMemcpyAsync(h_ctl, ctl, sizeof(Control), cudaMemcpyDeviceToHost, st));
+            BH_CUDA(cudaMemcpyAsync(h_front, front, sizeof(FrontCtl), cudaMemcpyDeviceToHost, st));
             pending = st;
             if (!rs.async) finish();
             return;
@@ -716,6 +878,9 @@ struct Engine final : EngineBase {
             if (!h_ctl->active && h_ctl->n_fin == 0) {
                 check_error();
                 stats.rounds = h_ctl->rounds_active;
+                BH_CUDA(cudaMemcpy(h_front, front, sizeof(FrontCtl), cudaMemcpyDeviceToHost));
+                stats.frontier_rounds = h_front->rounds_front;
+                stats.frontier_u_rounds = h_front->rounds_ufront;
                 if (prof) collect_profile(round);
                 return;
             }
@@ -738,8 +903,12 @@ struct Engine final : EngineBase {
         check_error();
         stats.rounds = h_ctl->rounds_active;
         // graph path: K5 only in the rounds where a slot finished (IF node)
-        const int64_t n_launch = (launches_per_round() - 1) * (int64_t)h_ctl->rounds_active + h_ctl->fin_rounds;
+        // K1 K1a K4 every round, the two dense pulls or the six frontier kernels
+        const int64_t rounds = h_ctl->rounds_active, fr = front_on ? h_front->rounds_front : 0;
+        const int64_t n_launch = 3 * rounds + 2 * (rounds - fr) + 6 * fr + h_ctl->fin_rounds;
         stats.launches += n_launch;
+        stats.frontier_rounds = fr;
+        stats.frontier_u_rounds = h_front->rounds_ufront;
         count_launch((int)n_launch);
     }
 
@@ -908,6 +1077,7 @@ struct SmallEngine final : EngineBase {
         a.ledger_r = rs.n_q == 1 ? led_r : nullptr;
         a.ledger_est = rs.n_q == 1 ? led_est : nullptr;
         a.max_rounds = 100000000;
+        a.scatter_limit = scatter_limit() * (double)g->n_e;
         a.error = plan.error;
         BH_CUDA(cudaMemsetAsync(plan.error, 0, sizeof(int32_t), st));
         BH_CUDA(cudaMemsetAsync(plan.ctl, 0, sizeof(Control), st));
@@ -1099,7 +1269,8 @@ extern "C" {
 
 const char *bh_last_error(void) { return t_err.c_str(); }
 static_assert(sizeof(bh_trace) == 96, "bh_trace layout (include/bhpp.h)");
-int bh_version(void) { return 2; }
+static_assert(sizeof(bh_run_stats) == 80, "bh_run_stats layout (include/bhpp.h)");
+int bh_version(void) { return 3; }
 int64_t bh_kernel_launches(void) { return g_launches.load(); }
 
 int bh_csr_build(int64_t n_u, int64_t n_v, int64_t n_e, const int64_t *edge_u, const int64_t *edge_v,
@@ -1241,6 +1412,12 @@ int bh_stream_gate(void *stream, const int32_t *flag) {
 
 int bh_set_profiling(int32_t on) {
     g_profiling = on ? 1 : 0;
+    return BH_OK;
+}
+
+int bh_set_scatter_limit(double fraction) {
+    if (std::isnan(fraction)) return BH_EINVAL;
+    g_scatter_limit = fraction;
     return BH_OK;
 }
 

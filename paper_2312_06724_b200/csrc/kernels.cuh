@@ -139,6 +139,52 @@ struct ElemGeo {
     static constexpr int TPN = B / EV;          // threads per node
 };
 
+// Frontier-round control (frontier.cuh): K1's decision and the K-F kernels' gates.
+struct FrontCtl {
+    unsigned long long deg_acc;   // sum over blocks and slots of sum deg(A_s) (K1)
+    unsigned long long edges_v;   // sum deg over the V list (Fb)
+    unsigned long long edges_u;   // sum deg over the U list (Fd)
+    int64_t limit;                // frontier iff deg_acc <= limit; < 0: never
+    int64_t rounds_front;         // rounds whose V half ran frontier
+    int64_t rounds_ufront;        // rounds whose U half ran frontier
+    int32_t ticket;               // K1 block arrival counter
+    int32_t mode;                 // 1: this round is a frontier round
+    int32_t gate_dense, gate_front, gate_ufront, gate_udense;
+    int32_t zero_all_v, zero_all_u;  // XV / Y may be non-zero outside the item lists
+    int32_t n_items_v, n_items_u, n_parts_v, n_parts_u;
+    int32_t old_items_v, old_items_u;  // lists of the previous frontier round (Fa)
+};
+
+// K1's last block: the round's mode, gates and graph condition.
+__device__ __forceinline__ void front_decide(FrontCtl *f, const int32_t *ops, int B, bool use_cond,
+                                             cudaGraphConditionalHandle cond) {
+    bool push = false, dense_op = false;
+    for (int s = 0; s < B; s++) {
+        const int o = ops[s];
+        push |= op_is_push(o);
+        dense_op |= !(o == OP_IDLE || o == OP_MEASURE || op_is_push(o));
+    }
+    const unsigned long long d = atomicAdd(&f->deg_acc, 0ull);
+    const bool front = push && !dense_op && f->limit >= 0 && d <= (unsigned long long)f->limit;
+    f->deg_acc = 0;
+    f->ticket = 0;
+    f->mode = front;
+    f->gate_front = front;
+    f->gate_dense = !front;
+    f->gate_ufront = 0;
+    f->gate_udense = 0;
+    if (front) {
+        f->rounds_front++;
+        f->old_items_v = f->n_items_v;
+        f->old_items_u = f->n_items_u;
+        f->n_items_v = f->n_items_u = f->n_parts_v = f->n_parts_u = 0;
+        f->edges_v = 0;
+    } else {
+        f->zero_all_v = f->zero_all_u = 1;
+    }
+    if (use_cond) cudaGraphSetConditional(cond, front ? 1u : 0u);
+}
+
 template <typename T>
 struct ElemArgs {
     int64_t n_u;
@@ -155,6 +201,11 @@ struct ElemArgs {
     const int32_t *active;
     Partials part;
     double alpha;
+    // frontier rounds (frontier.cuh; k_push<..., FRONT = true> only)
+    FrontCtl *front;
+    uint8_t *flag_u;  // [n_u] some slot pushed u this round
+    cudaGraphConditionalHandle fcond;
+    int32_t use_fcond;
 };
 
 // Per-slot constants of K1 / K1a in shared memory, element-major: the v-th slot
@@ -196,16 +247,24 @@ __device__ __forceinline__ void load_elem_consts(ElemSlotC &c, const Slot *__res
 // which re-takes the same decision on the same r; only the ledger-initialising
 // round writes r and est here.  Per element the work is predicated (the slots
 // of one warp are in different phases), loads of UNR nodes are in flight.
-template <int B, typename T, int ELEM_UNR = 4, int MINB = 1, bool PIPE = false>
+template <int B, typename T, int ELEM_UNR = 4, int MINB = 1, bool PIPE = false, bool FRONT = false>
 __global__ void __launch_bounds__(ELEM_THREADS, MINB) k_push(ElemArgs<T> a) {
     pdl_begin();
-    if (*a.active == 0) return;
+    if (*a.active == 0) {
+        if (FRONT && blockIdx.x == 0 && threadIdx.x == 0) {  // batch over: close every gate
+            a.front->gate_front = a.front->gate_dense = 0;
+            a.front->gate_ufront = a.front->gate_udense = 0;
+        }
+        return;
+    }
     using EG = ElemGeo<B>;
     constexpr int EV = EG::EV, TPN = EG::TPN;
     __shared__ ElemSlotC sc;
     __shared__ int64_t red_cnt[ELEM_THREADS * EV];
     __shared__ int64_t red_np[ELEM_THREADS * EV];
     __shared__ double red_left[ELEM_THREADS * EV];
+    __shared__ unsigned long long blk_deg;
+    if (threadIdx.x == 0) blk_deg = 0;
     load_elem_consts<B>(sc, a.slots);
     __syncthreads();
     const int grp = threadIdx.x % TPN;
@@ -235,7 +294,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, MINB) k_push(ElemArgs<T> a) {
     // thread's group (one round per query); the common body has neither
     auto run = [&](auto rare_tag) {
         constexpr bool RARE = decltype(rare_tag)::value;
-        auto node = [&](int64_t u, T (&rv)[EV], double iwsv, double wsv, int32_t degv) {
+        auto node = [&](int64_t u, T (&rv)[EV], double iwsv, double wsv, int32_t degv, unsigned live) {
             const int64_t i = u * B + j0;
             const double iws = iwsv;
             T pv[EV];
@@ -267,6 +326,19 @@ __global__ void __launch_bounds__(ELEM_THREADS, MINB) k_push(ElemArgs<T> a) {
                 }
                 if (init) rv[v] = pushed ? (T)0 : (T)r;
                 pv[v] = p;
+            }
+            if constexpr (FRONT) {  // frontier flag: some slot pushed u (the node's TPN lanes combined)
+                bool anyp = false;
+#pragma unroll
+                for (int v = 0; v < EV; v++) anyp |= act[v];
+                if constexpr (TPN == 1) {
+                    a.flag_u[u] = anyp;
+                } else {
+                    const unsigned bal = __ballot_sync(live, anyp);
+                    const int lane = threadIdx.x & 31;
+                    const unsigned gm = (TPN == 32 ? 0xffffffffu : ((1u << (TPN % 32)) - 1u)) << ((lane / TPN) * TPN % 32);
+                    if ((lane % TPN) == 0) a.flag_u[u] = (bal & gm) != 0u;
+                }
             }
             if (m_keep) {  // slots whose P is kept (iterate / idle) are not written
 #pragma unroll
@@ -301,17 +373,19 @@ __global__ void __launch_bounds__(ELEM_THREADS, MINB) k_push(ElemArgs<T> a) {
             double in = 0.0, wn = 0.0;
             int32_t dn = 0;
             if (first < total) load(first / TPN, rn, in, wn, dn);
-            for (int64_t t = first; t < total; t += stride) {
+            for (int64_t t = first; FRONT ? __any_sync(0xffffffffu, t < total) : t < total; t += stride) {
+                const unsigned live = FRONT ? __ballot_sync(0xffffffffu, t < total) : 0u;
+                if (t >= total) continue;
                 T rv[EV];
 #pragma unroll
                 for (int v = 0; v < EV; v++) rv[v] = rn[v];
                 const double iwsv = in, wsv = wn;
                 const int32_t degv = dn;
                 if (t + stride < total) load((t + stride) / TPN, rn, in, wn, dn);
-                node(t / TPN, rv, iwsv, wsv, degv);
+                node(t / TPN, rv, iwsv, wsv, degv, live);
             }
         } else {
-            for (int64_t t0 = first; t0 < total; t0 += ELEM_UNR * stride) {
+            for (int64_t t0 = first; FRONT ? __any_sync(0xffffffffu, t0 < total) : t0 < total; t0 += ELEM_UNR * stride) {
                 T rv[ELEM_UNR][EV];
                 double iwsk[ELEM_UNR], wsk[ELEM_UNR];
                 int32_t degk[ELEM_UNR];
@@ -323,14 +397,22 @@ __global__ void __launch_bounds__(ELEM_THREADS, MINB) k_push(ElemArgs<T> a) {
 #pragma unroll
                 for (int k = 0; k < ELEM_UNR; k++) {
                     const int64_t t = t0 + k * stride;
-                    if (t >= total) break;
-                    node(t / TPN, rv[k], iwsk[k], wsk[k], degk[k]);
+                    const unsigned live = FRONT ? __ballot_sync(0xffffffffu, t < total) : 0u;
+                    if (FRONT ? !live : t >= total) break;
+                    if (t < total) node(t / TPN, rv[k], iwsk[k], wsk[k], degk[k], live);
                 }
             }
         }
     };
-    if (m_init | m_x0) run(std::true_type{});
-    else if (m_push | m_entry) run(std::false_type{});
+    // warp-uniform choice (the frontier flag combines the lanes of a node by ballot):
+    // lanes whose own slots have no work run the loop with empty masks
+    if constexpr (FRONT) {
+        if (__any_sync(0xffffffffu, (m_init | m_x0) != 0u)) run(std::true_type{});
+        else if (__any_sync(0xffffffffu, (m_push | m_entry) != 0u)) run(std::false_type{});
+    } else {
+        if (m_init | m_x0) run(std::true_type{});
+        else if (m_push | m_entry) run(std::false_type{});
+    }
 #pragma unroll
     for (int v = 0; v < EV; v++) {
         red_cnt[threadIdx.x * EV + v] = cnt[v];
@@ -350,6 +432,21 @@ __global__ void __launch_bounds__(ELEM_THREADS, MINB) k_push(ElemArgs<T> a) {
         a.part.cnt[(int64_t)s * gridDim.x + blockIdx.x] = c;
         a.part.np_u[(int64_t)s * gridDim.x + blockIdx.x] = n;
         a.part.lmass[(int64_t)s * gridDim.x + blockIdx.x] = l;
+        if constexpr (FRONT) atomicAdd(&blk_deg, (unsigned long long)n);
+    }
+    if constexpr (FRONT) {  // frontier decision: the last block to arrive (frontier.cuh)
+        __shared__ int last;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            atomicAdd(&a.front->deg_acc, blk_deg);
+            __threadfence();
+            last = atomicAdd(&a.front->ticket, 1) == (int)gridDim.x - 1;
+        }
+        __syncthreads();
+        if (last && threadIdx.x == 0) {
+            __threadfence();
+            front_decide(a.front, sc.op, B, a.use_fcond != 0, a.fcond);
+        }
     }
 }
 

@@ -18,7 +18,7 @@
 // its V neighbours is non-zero.  Rows outside the frontier are zero, exactly
 // as in a full pull; every visited row is summed sequentially in CSR order.
 // A round switches to the frontier form when the pushed rows' degree sum is at
-// most a quarter of |E| (the reference's _SCATTER_LIMIT, push_engine.py:44).
+// most _SCATTER_LIMIT * |E| (push_engine.py:44; bh_set_scatter_limit, default 0.25).
 //
 // Work split inside the CTA: rows are cut into chunks of at most SMALL_CHUNK
 // edges (host-built item lists, longest first, dealt round-robin to threads);
@@ -68,6 +68,7 @@ struct SmallArgs {
     double *scores;         // [n_q][n_u] caller order, or null
     double *ledger_r, *ledger_est;  // [n_u] caller order (single-query ledger out), or null
     int64_t max_rounds;
+    double scatter_limit;   // _SCATTER_LIMIT * |E| (bh_set_scatter_limit); < 0: dense rounds only
     int32_t *error;         // set to 1 on the runaway guard
 };
 
@@ -219,7 +220,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_query(SmallArgs<T> a) {
                 left = x[2];
             }
             // frontier form when the pushed rows are light (push_engine.py:44, 297)
-            if (tid == 0) s_sparse_v = npu <= 0.25 * (double)a.n_e && !(o == OP_PI || o == OP_PIENTRY);
+            if (tid == 0) s_sparse_v = (double)npu <= a.scatter_limit && !(o == OP_PI || o == OP_PIENTRY);
             __syncthreads();
             const bool sparse = s_sparse_v;
             if (sparse) {  // N(A): walk the pushed rows' U-CSR edges
@@ -269,7 +270,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_query(SmallArgs<T> a) {
                 xdeg = x[1];
             }
             // U rows to visit: neighbours of the non-zero V rows (walk cost xdeg)
-            if (tid == 0) s_sparse_u = sparse && xdeg <= 0.25 * (double)a.n_e;
+            if (tid == 0) s_sparse_u = sparse && (double)xdeg <= a.scatter_limit;
             __syncthreads();
             const bool sparse_u = s_sparse_u;
             if (sparse_u) {  // rows of the non-zero V rows (bitmap by ballot), then their U neighbours

@@ -22,6 +22,12 @@ import numpy as np
 
 from . import _capi
 
+# Frontier ("scatter") rounds when the pushed rows touch at most this fraction of
+# |E| (push_engine.py:44); the engine reads it at every run (_capi.apply_scatter_limit).
+# Results do not depend on it; tests monkeypatch it like the reference's own
+# (pkg/tests/test_push_engine.py:188-202): -1 forces dense rounds, >= 1 frontier.
+_SCATTER_LIMIT = 0.25
+
 
 @dataclass
 class ResidueLedger:
@@ -130,6 +136,7 @@ def run_job(g, job: int, source: int, alpha: float, lam: float, eps_b: float, ep
     scores = np.empty(n_u)
     tr = _capi.Trace()
     hook = _hook_adapter(g, round_hook)
+    _capi.apply_scatter_limit()
     _capi.check(_capi.lib().bh_push_run(dg.h, job, int(source), float(alpha), float(lam), float(eps_b),
                                         float(eps_f), int(tie_skip), _capi.ptr(r_u), _capi.ptr(est),
                                         _capi.ptr(n_p), _capi.ptr(scores), C.byref(tr), hook, None))

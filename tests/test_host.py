@@ -31,7 +31,7 @@ def test_library_exports_every_header_symbol():
     for name in names:
         assert hasattr(lib, name), f"libbhpp.so does not export {name}"
     assert set(_capi.EXPORTS) == set(names)
-    assert lib.bh_version() == 2
+    assert lib.bh_version() == 3
 
 
 def test_struct_layouts_match_header():
@@ -40,7 +40,7 @@ def test_struct_layouts_match_header():
     assert C.sizeof(_capi.Trace) == 96
     assert C.sizeof(_capi.QueryParams) == 56
     assert C.sizeof(_capi.GraphInfo) == 56
-    assert C.sizeof(_capi.RunStats) == 64
+    assert C.sizeof(_capi.RunStats) == 80
     assert _capi.TRACE_DTYPE.itemsize == C.sizeof(_capi.Trace)
 
 
@@ -252,3 +252,19 @@ def test_batch_source_list_keeps_each_elements_type():
     assert _source_list(np.array([[1, 2], [3, 4]])) == [1, 2, 3, 4]
     assert _source_list(np.array(["a", "b"])) == ["a", "b"]
     assert _source_list((x for x in (1, 2))) == [1, 2]
+
+
+def test_scatter_limit_switch_mirrors_reference_constant(monkeypatch):
+    """push_engine._SCATTER_LIMIT (push_engine.py:44) is handed to the engine
+    before every run; NaN is rejected by the C ABI (no GPU needed)."""
+    from paper_2312_06724_b200 import push_engine as pe
+
+    assert pe._SCATTER_LIMIT == 0.25
+    lib = _capi.lib()
+    assert lib.bh_set_scatter_limit(float("nan")) != 0
+    monkeypatch.setattr(pe, "_SCATTER_LIMIT", -1.0)
+    _capi.apply_scatter_limit()
+    assert _capi._applied_limit == -1.0
+    monkeypatch.setattr(pe, "_SCATTER_LIMIT", 0.25)
+    _capi.apply_scatter_limit()
+    assert _capi._applied_limit == 0.25

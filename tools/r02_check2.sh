@@ -1,0 +1,8 @@
+set -u
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_frontier.py -x -q > gpurun_out/pytest_front.txt 2>&1; tail -15 gpurun_out/pytest_front.txt
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu2.txt 2>&1; tail -4 gpurun_out/pytest_gpu2.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke2.txt 2>&1; tail -2 gpurun_out/smoke2.txt
+timeout 900 python bench.py --no-cpu --no-c3 > gpurun_out/bench2.json 2> gpurun_out/bench2.err; python -c "
+import json; d=json.load(open('gpurun_out/bench2.json')); r=d['roofline']
+print('value', round(d['value'],1), 'e2e', round(d['e2e']['value'],1), {k: round(v,3) for k,v in r['breakdown_ms_per_step'].items()}, r['timed_step_ms'], 'fp64', d['fp64'] and round(d['fp64']['value'],1))" || tail -5 gpurun_out/bench2.err
