@@ -942,46 +942,92 @@ struct SmallEngine final : EngineBase {
     cudaStream_t pending = nullptr;
     int32_t *h_err = nullptr;
 
-    // Work items of one side: rows in chunks of <= SMALL_CHUNK edges, longest first.
-    static void build_items(const Side &sd, SmallItem *&d_items, int32_t &n_items, SmallSplit *&d_split,
-                            int32_t &n_split, int32_t &n_parts) {
-        std::vector<SmallItem> items;
-        std::vector<SmallSplit> split;
-        int32_t parts = 0;
-        for (int64_t r = 0; r < sd.n_rows; r++) {
-            const int64_t e0 = sd.h_indptr[r], d = sd.h_indptr[r + 1] - e0;
-            if (d <= SMALL_CHUNK) {
-                items.push_back({(int32_t)r, (int32_t)d, e0, -1, 0});
-                continue;
+    // Row slices of one side for CL ranks, balanced on edges + rows; then each
+    // rank's work items (rows in chunks of <= SMALL_CHUNK edges, longest first).
+    static void build_side(const Side &sd, int cl, std::vector<int32_t> &slice, std::vector<SmallItem> &items,
+                           std::vector<int32_t> &ioff, std::vector<SmallSplit> &split, std::vector<int32_t> &soff,
+                           int32_t &n_parts) {
+        const int64_t n = sd.n_rows, E = sd.h_indptr[n];
+        const int64_t total = E + 2 * n;
+        slice.assign(cl + 1, 0);
+        slice[cl] = (int32_t)n;
+        for (int r = 1; r < cl; r++) {
+            const int64_t target = total * r / cl;
+            int64_t lo = slice[r - 1], hi = n;
+            while (lo < hi) {  // first row whose cost prefix reaches the target
+                const int64_t mid = (lo + hi) / 2;
+                if (sd.h_indptr[mid] + 2 * mid < target) lo = mid + 1; else hi = mid;
             }
-            const int32_t np = (int32_t)((d + SMALL_CHUNK - 1) / SMALL_CHUNK);
-            split.push_back({(int32_t)r, parts, np, 0});
-            for (int32_t c = 0; c < np; c++)
-                items.push_back({(int32_t)r, (int32_t)std::min<int64_t>(SMALL_CHUNK, d - (int64_t)c * SMALL_CHUNK),
-                                 e0 + (int64_t)c * SMALL_CHUNK, parts + c, 0});
-            parts += np;
+            slice[r] = (int32_t)lo;
         }
-        std::stable_sort(items.begin(), items.end(), [](const SmallItem &x, const SmallItem &y) { return x.len > y.len; });
-        n_items = (int32_t)items.size();
-        n_split = (int32_t)split.size();
+        items.clear();
+        split.clear();
+        ioff.assign(cl + 1, 0);
+        soff.assign(cl + 1, 0);
+        int32_t parts = 0;
+        for (int r = 0; r < cl; r++) {
+            const size_t first = items.size();
+            for (int64_t row = slice[r]; row < slice[r + 1]; row++) {
+                const int64_t e0 = sd.h_indptr[row], d = sd.h_indptr[row + 1] - e0;
+                if (d <= SMALL_CHUNK) {
+                    items.push_back({(int32_t)row, (int32_t)d, e0, -1, 0});
+                    continue;
+                }
+                const int32_t np = (int32_t)((d + SMALL_CHUNK - 1) / SMALL_CHUNK);
+                split.push_back({(int32_t)row, parts, np, 0});
+                for (int32_t c = 0; c < np; c++)
+                    items.push_back({(int32_t)row, (int32_t)std::min<int64_t>(SMALL_CHUNK, d - (int64_t)c * SMALL_CHUNK),
+                                     e0 + (int64_t)c * SMALL_CHUNK, parts + c, 0});
+                parts += np;
+            }
+            std::stable_sort(items.begin() + first, items.end(),
+                             [](const SmallItem &x, const SmallItem &y) { return x.len > y.len; });
+            ioff[r + 1] = (int32_t)items.size();
+            soff[r + 1] = (int32_t)split.size();
+        }
         n_parts = parts;
-        d_items = dalloc<SmallItem>(std::max<size_t>(1, items.size()));
-        d_split = dalloc<SmallSplit>(std::max<size_t>(1, split.size()));
-        if (!items.empty())
-            BH_CUDA(cudaMemcpy(d_items, items.data(), items.size() * sizeof(SmallItem), cudaMemcpyHostToDevice));
-        if (!split.empty())
-            BH_CUDA(cudaMemcpy(d_split, split.data(), split.size() * sizeof(SmallSplit), cudaMemcpyHostToDevice));
+    }
+
+    template <class X>
+    static X *upload(const std::vector<X> &v) {
+        X *d = dalloc<X>(std::max<size_t>(1, v.size()));
+        if (!v.empty()) BH_CUDA(cudaMemcpy(d, v.data(), v.size() * sizeof(X), cudaMemcpyHostToDevice));
+        return d;
     }
 
     static size_t smem_for(const bh_graph *g, int32_t parts) {
         return SmallSmem<T>::bytes(g->n_u, g->n_v, parts);
     }
 
+    // cluster size: BH_SMALL_CL (1, 2, 4, 8, 16), default 8 (portable)
+    static int cluster_size() {
+        const char *m = getenv("BH_SMALL_CL");
+        const int v = m ? atoi(m) : 8;
+        return (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) ? v : 8;
+    }
+
     explicit SmallEngine(bh_graph *graph) : g(graph) {
         this->nslots = 1;
-        build_items(g->V, plan.items_v, plan.n_items_v, plan.split_v, plan.n_split_v, plan.n_parts_v);
-        build_items(g->U, plan.items_u, plan.n_items_u, plan.split_u, plan.n_split_u, plan.n_parts_u);
+        plan.cl = cluster_size();
+        std::vector<int32_t> us, vs, iu, iv, su, sv;
+        std::vector<SmallItem> itu, itv;
+        std::vector<SmallSplit> spu, spv;
+        build_side(g->V, plan.cl, vs, itv, iv, spv, sv, plan.n_parts_v);
+        build_side(g->U, plan.cl, us, itu, iu, spu, su, plan.n_parts_u);
+        plan.items_v = upload(itv);
+        plan.items_u = upload(itu);
+        plan.split_v = upload(spv);
+        plan.split_u = upload(spu);
+        std::vector<int32_t> offs;
+        for (auto *v : {&us, &vs, &iu, &iv, &su, &sv}) offs.insert(offs.end(), v->begin(), v->end());
+        plan.offs = upload(offs);
         plan.smem = smem_for(g, std::max(plan.n_parts_v, plan.n_parts_u));
+        for (int r = 0; r < plan.cl; r++) {
+            plan.cap_ev = std::max<int32_t>(plan.cap_ev, (int32_t)(g->V.h_indptr[vs[r + 1]] - g->V.h_indptr[vs[r]]));
+            plan.cap_eu = std::max<int32_t>(plan.cap_eu, (int32_t)(g->U.h_indptr[us[r + 1]] - g->U.h_indptr[us[r]]));
+            plan.cap_iv = std::max<int32_t>(plan.cap_iv, iv[r + 1] - iv[r]);
+            plan.cap_iu = std::max<int32_t>(plan.cap_iu, iu[r + 1] - iu[r]);
+        }
         // one process-wide ceiling for the kernel (a per-graph value would break the
         // launches of other graphs' engines): everything the opt-in limit leaves
         cudaFuncAttributes fa{};
@@ -990,12 +1036,30 @@ struct SmallEngine final : EngineBase {
         BH_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
         const int ceiling = optin - (int)fa.sharedSizeBytes;
         if ((int64_t)plan.smem > ceiling) throw CudaError("small path: shared memory plan exceeds the device limit");
+        {  // stage each rank's graph slice in shared memory when it fits beside the state
+            const size_t st = SmallSmem<T>::staged(plan.cap_ev, plan.cap_eu, plan.cap_iv, plan.cap_iu);
+            if (plan.smem + st <= (size_t)ceiling && !getenv("BH_SMALL_NOSTAGE")) {
+                plan.stage = 1;
+                plan.smem += st;
+            }
+        }
         BH_CUDA(cudaFuncSetAttribute(k_small_query<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, ceiling));
-        int occ = 0, sms = 148;
-        BH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_small_query<T>, SMALL_THREADS, plan.smem));
-        BH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
-        if (occ < 1) throw CudaError("small path: no resident CTA");
-        plan.grid_cap = occ * sms;
+        if (plan.cl > 8) BH_CUDA(cudaFuncSetAttribute(k_small_query<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)plan.cl;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3((unsigned)plan.cl);
+        cfg.blockDim = dim3(SMALL_THREADS);
+        cfg.dynamicSmemBytes = plan.smem;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int clusters = 0;
+        BH_CUDA(cudaOccupancyMaxActiveClusters(&clusters, k_small_query<T>, &cfg));
+        if (clusters < 1) throw CudaError("small path: no resident cluster");
+        plan.cluster_cap = clusters;
         plan.error = dalloc<int32_t>(1);
         plan.ctl = dalloc<Control>(1);
         led_r = dalloc<double>(g->n_u);
@@ -1041,16 +1105,24 @@ struct SmallEngine final : EngineBase {
         a.ws_u = g->ws_u;
         a.inv_ws_u = g->inv_ws_u;
         a.perm_u = g->U.perm;
+        const int cl = plan.cl;
+        a.u_slice = plan.offs;
+        a.v_slice = plan.offs + (cl + 1);
+        a.iu_off = plan.offs + 2 * (cl + 1);
+        a.iv_off = plan.offs + 3 * (cl + 1);
+        a.su_off = plan.offs + 4 * (cl + 1);
+        a.sv_off = plan.offs + 5 * (cl + 1);
         a.items_v = plan.items_v;
         a.items_u = plan.items_u;
         a.split_v = plan.split_v;
         a.split_u = plan.split_u;
-        a.n_items_v = plan.n_items_v;
-        a.n_items_u = plan.n_items_u;
-        a.n_split_v = plan.n_split_v;
-        a.n_split_u = plan.n_split_u;
         a.n_parts_v = plan.n_parts_v;
         a.n_parts_u = plan.n_parts_u;
+        a.stage = plan.stage;
+        a.cap_ev = plan.cap_ev;
+        a.cap_eu = plan.cap_eu;
+        a.cap_iv = plan.cap_iv;
+        a.cap_iu = plan.cap_iu;
         ControlArgs &ca = a.ca;
         ca.ctl = plan.ctl;
         ca.sources = rs.sources;
@@ -1077,12 +1149,39 @@ struct SmallEngine final : EngineBase {
         a.ledger_r = rs.n_q == 1 ? led_r : nullptr;
         a.ledger_est = rs.n_q == 1 ? led_est : nullptr;
         a.max_rounds = 100000000;
-        a.scatter_limit = scatter_limit() * (double)g->n_e;
         a.error = plan.error;
         BH_CUDA(cudaMemsetAsync(plan.error, 0, sizeof(int32_t), st));
         BH_CUDA(cudaMemsetAsync(plan.ctl, 0, sizeof(Control), st));
-        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(rs.n_q, plan.grid_cap));
-        k_small_query<T><<<grid, SMALL_THREADS, plan.smem, st>>>(a);
+        const int n_clusters = (int)std::max<int64_t>(1, std::min<int64_t>(rs.n_q, plan.cluster_cap));
+        unsigned long long *prof = nullptr;
+        if (getenv("BH_SMALL_PROF")) {
+            prof = dalloc<unsigned long long>(8);
+            BH_CUDA(cudaMemsetAsync(prof, 0, 64, st));
+        }
+        a.prof = prof;
+        {
+            cudaLaunchConfig_t cfg = {};
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = (unsigned)cl;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.gridDim = dim3((unsigned)(n_clusters * cl));
+            cfg.blockDim = dim3(SMALL_THREADS);
+            cfg.dynamicSmemBytes = plan.smem;
+            cfg.stream = st;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            BH_CUDA(cudaLaunchKernelEx(&cfg, k_small_query<T>, a));
+        }
+        if (prof) {
+            unsigned long long h[8];
+            BH_CUDA(cudaMemcpyAsync(h, prof, 64, cudaMemcpyDeviceToHost, st));
+            BH_CUDA(cudaStreamSynchronize(st));
+            fprintf(stderr, "small-path cycles: K1 %llu sync1 %llu Vpull %llu sync2 %llu Upull %llu K1a+sums %llu sync3+K4 %llu\n",
+                    h[0], h[1], h[2], h[3], h[4], h[5], h[6]);
+            cudaFree(prof);
+        }
         count_launch();
         BH_CUDA(cudaGetLastError());
         BH_CUDA(cudaMemcpyAsync(h_err, plan.error, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
