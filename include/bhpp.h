@@ -227,10 +227,11 @@ int bh_set_profiling(int32_t on);
 /* Frontier rounds (K-F), process-wide: a round pulls only the rows reachable
  * from its pushed set when the pushed rows (summed over the block's slots)
  * touch at most fraction * |E| edges; its U half likewise on the V rows it
- * reached.  Mirrors push_engine._SCATTER_LIMIT (push_engine.py:44, 297, 315;
- * default 0.25).  fraction < 0: never; >= 1: whenever no slot is in power
- * iteration.  Results do not depend on it (every visited row is summed in
- * full); it only changes which rows a round visits. */
+ * reached.  Mirrors push_engine._SCATTER_LIMIT (push_engine.py:44, 297,
+ * 315).  fraction < 0: never; >= 1: whenever no slot is in power iteration.
+ * Blocks of more than 16 slots run dense rounds unless fraction >= 1.  Results do not depend on it (every visited row is summed in
+ * full); it only changes which rows a round visits.  Default 0.01 (the
+ * reference's 0.25 is a CPU tuning). */
 int bh_set_scatter_limit(double fraction);
 /* Measurement gate: enqueue on `stream` a one-thread kernel that spins until
  * *flag (host-mapped pinned memory) becomes nonzero, so a batch can be fully

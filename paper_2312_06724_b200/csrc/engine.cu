@@ -134,7 +134,7 @@ struct RunSpec {
 static std::atomic<int> g_profiling{0};
 // push_engine._SCATTER_LIMIT (push_engine.py:44): a round runs in frontier form when
 // the pushed rows touch at most this fraction of |E| (bh_set_scatter_limit)
-static std::atomic<double> g_scatter_limit{0.25};
+static std::atomic<double> g_scatter_limit{0.01};
 static double scatter_limit() { return g_scatter_limit.load(); }
 
 struct EngineBase {

@@ -23,10 +23,14 @@ import numpy as np
 from . import _capi
 
 # Frontier ("scatter") rounds when the pushed rows touch at most this fraction of
-# |E| (push_engine.py:44); the engine reads it at every run (_capi.apply_scatter_limit).
-# Results do not depend on it; tests monkeypatch it like the reference's own
-# (pkg/tests/test_push_engine.py:188-202): -1 forces dense rounds, >= 1 frontier.
-_SCATTER_LIMIT = 0.25
+# |E| (the reference's constant of the same name, push_engine.py:44, is 0.25 --
+# tuned for numpy scatter against scipy matvec on a CPU; on the GPU a frontier
+# round pays below a few % of |E|: single c3 queries 729 ms dense, 731 at 0.25,
+# 673 at 0.05, 646 at 0.01, profiles/r02_latency.md).  The engine reads it at
+# every run (_capi.apply_scatter_limit).  Results do not depend on it; tests
+# monkeypatch it like the reference's own (pkg/tests/test_push_engine.py:188-202):
+# -1 forces dense rounds, >= 1 frontier rounds.
+_SCATTER_LIMIT = 0.01
 
 
 @dataclass

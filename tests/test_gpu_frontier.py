@@ -6,7 +6,7 @@ dense matvec otherwise (pkg/src/bipush/push_engine.py:44, 269-277, 294-324);
 its own test forces either path by monkeypatching the constant and checks they
 agree (pkg/tests/test_push_engine.py:187-202).  The engine mirrors the
 constant (``push_engine._SCATTER_LIMIT``): -1 forces dense rounds, >= 1 forces
-frontier rounds whenever no slot is in power iteration; the default 0.25
+frontier rounds whenever no slot is in power iteration; the default (0.01)
 applies to blocks of up to 16 slots (wider blocks run dense rounds, see
 frontier.cuh).  Every mode must meet
 the same bar against the reference fixtures: fp64 scores within 1e-9 and
@@ -24,7 +24,7 @@ from test_gpu_parity import ATOL64, RTOL32, assert_traces, tie_skip_from, topk_e
 
 pytestmark = pytest.mark.gpu
 
-FORCE_DENSE, DEFAULT, FORCE_FRONTIER = -1.0, 0.25, 10.0
+FORCE_DENSE, DEFAULT, FORCE_FRONTIER = -1.0, pe._SCATTER_LIMIT, 10.0
 
 
 def _stats(g, dtype):

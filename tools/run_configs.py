@@ -93,7 +93,7 @@ def main():
             ties = np.array([O.tie_skip_for(t["forward"]) for _, t in ref], dtype=np.int32)
             r64 = bh.bhpp_query_batch(g, meta, src[:P], eps, k=cfg.k, dtype="fp64", return_scores=True,
                                       tie_skip=ties)
-            worst64, traces_ok, topk32_rel, sets32 = 0.0, True, 0.0, True
+            worst64, traces_ok, topk32_rel, sets32, topk32_abs = 0.0, True, 0.0, True, 0.0
             for i, (scores, t) in enumerate(ref):
                 worst64 = max(worst64, float(np.abs(r64.scores[i] - scores).max()))
                 got = r64.trace_dicts(i)
@@ -103,12 +103,14 @@ def main():
                 top = O.topk_indices(scores, cfg.k)
                 rel = np.abs(res.topk_score[i] - scores[top]) / np.maximum(np.abs(scores[top]), 1e-300)
                 topk32_rel = max(topk32_rel, float(rel.max()))
+                topk32_abs = max(topk32_abs, float(np.abs(res.topk_score[i] - scores[top]).max()))
                 diff = res.topk_index[i] != top
                 if diff.any():
                     gap = np.abs(scores[res.topk_index[i][diff]] - scores[top[diff]]).max()
                     sets32 &= bool(gap <= 1e-5 * scores[top[-1]] + eps)
             run["parity"] = {"sources": P, "fp64_max_abs_err": worst64, "fp64_traces_identical": bool(traces_ok),
                              f"{a.dtype}_topk_max_rel_err": topk32_rel, f"{a.dtype}_topk_sets_equal_up_to_ties": sets32,
+                             f"{a.dtype}_topk_max_abs_err": topk32_abs, f"{a.dtype}_topk_abs_err_over_eps": topk32_abs / eps,
                              "pass": bool(worst64 <= 1e-9 and traces_ok and topk32_rel <= 1e-5 and sets32)}
         out["runs"].append(run)
         print(json.dumps(run), file=sys.stderr, flush=True)
