@@ -293,7 +293,7 @@ struct Engine final : EngineBase {
     // Pull geometry per side and lane width (rows in flight per warp, 256-thread
     // blocks per SM), measured at c2 / c5 on B200 (profiles/r01_pull_variants.md):
     //   8-byte lanes (64 fp32 slots): V 7 rows at 4 blocks/SM, U 8 rows at 4
-    //   16-byte lanes: fp32 (128 slots) V 8 at 2, U 6 at 3; fp64 (64 slots) 6 at 3 both
+    //   16-byte lanes: fp32 (128 slots) V 8 at 2, U 8 at 3 (round 2); fp64 (64 slots) 6 at 3 both
     //   otherwise SwPipe's defaults (U side at 4 blocks/SM when the default is 3)
     using PullFn = void (*)(PullArgs<T>);
     template <int SIDE>
@@ -304,12 +304,35 @@ struct Engine final : EngineBase {
             constexpr int LB = SwPipe<B, T>::LANE_BYTES;
             if constexpr (sizeof(T) == 8 && B == 64) return k_pull_sw<B, T, SIDE, 6, 3>;
             if constexpr (SIDE == SIDE_V && LB == 8) return k_pull_sw<B, T, SIDE_V, 7, 4>;
-            if constexpr (SIDE == SIDE_U && LB == 16 && sizeof(T) == 4) return k_pull_sw<B, T, SIDE_U, 6, 3>;
+            // 16-byte fp32 lanes (128 slots), U side: 8 rows at 3 blocks/SM (c5 slice: U pull
+            // 145 -> 110 us per round against 6 rows at 3, profiles/r02_pull_geometry.md)
+            if constexpr (SIDE == SIDE_U && LB == 16 && sizeof(T) == 4) return k_pull_sw<B, T, SIDE_U, 8, 3>;
             if constexpr (SIDE == SIDE_U && SwPipe<B, T>::MINB == 3) return k_pull_sw<B, T, SIDE_U, SwPipe<B, T>::S, 4>;
             return k_pull_sw<B, T, SIDE>;
         }
     }
-    static PullFn pull_kernel(int side) { return side == SIDE_V ? sw_kernel<SIDE_V>() : sw_kernel<SIDE_U>(); }
+    // A/B of the pull geometry (BH_PULL_CFG_V / BH_PULL_CFG_U = "S,MINB")
+    template <int SIDE>
+    static PullFn ab_kernel(const char *m) {
+        if constexpr (WIDE) {
+            const std::string v(m);
+            if (v == "8,2") return k_pull_sw<B, T, SIDE, 8, 2>;
+            if (v == "6,3") return k_pull_sw<B, T, SIDE, 6, 3>;
+            if (v == "5,3") return k_pull_sw<B, T, SIDE, 5, 3>;
+            if (v == "8,3") return k_pull_sw<B, T, SIDE, 8, 3>;
+            if (v == "4,4") return k_pull_sw<B, T, SIDE, 4, 4>;
+            if (v == "6,4") return k_pull_sw<B, T, SIDE, 6, 4>;
+        }
+        return sw_kernel<SIDE>();
+    }
+    static PullFn pull_kernel(int side) {
+        if (side == SIDE_V) {
+            const char *m = getenv("BH_PULL_CFG_V");
+            return m ? ab_kernel<SIDE_V>(m) : sw_kernel<SIDE_V>();
+        }
+        const char *m = getenv("BH_PULL_CFG_U");
+        return m ? ab_kernel<SIDE_U>(m) : sw_kernel<SIDE_U>();
+    }
 
     explicit Engine(bh_graph *graph) : g(graph) {
         this->nslots = B;
