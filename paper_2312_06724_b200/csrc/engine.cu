@@ -291,9 +291,11 @@ struct Engine final : EngineBase {
     }
 
     // Pull geometry per side and lane width (rows in flight per warp, 256-thread
-    // blocks per SM), measured at c2 / c5 on B200 (profiles/r01_pull_variants.md):
-    //   8-byte lanes (64 fp32 slots): V 7 rows at 4 blocks/SM, U 8 rows at 4
-    //   16-byte lanes: fp32 (128 slots) V 8 at 2, U 8 at 3 (round 2); fp64 (64 slots) 6 at 3 both
+    // blocks per SM), measured at c2 / c5 on B200 (profiles/r01_pull_variants.md,
+    // profiles/r02_pull_geometry.md):
+    //   64 fp32 slots (8-byte lanes): V 7 at 4, U 7 at 4
+    //   64 fp64 slots (16-byte lanes): V 6 at 3, U 5 at 4
+    //   128 fp32 slots (16-byte lanes): V 10 at 2, U 8 at 3
     //   otherwise SwPipe's defaults (U side at 4 blocks/SM when the default is 3)
     using PullFn = void (*)(PullArgs<T>);
     template <int SIDE>
@@ -301,12 +303,21 @@ struct Engine final : EngineBase {
         if constexpr (!WIDE) {
             return k_pull_small<B, T, SIDE>;
         } else {
+            // (rows in flight per warp, 256-thread blocks per SM) per side and lane width,
+            // swept on one box in round 2 (profiles/r02_pull_geometry.md)
             constexpr int LB = SwPipe<B, T>::LANE_BYTES;
-            if constexpr (sizeof(T) == 8 && B == 64) return k_pull_sw<B, T, SIDE, 6, 3>;
-            if constexpr (SIDE == SIDE_V && LB == 8) return k_pull_sw<B, T, SIDE_V, 7, 4>;
-            // 16-byte fp32 lanes (128 slots), U side: 8 rows at 3 blocks/SM (c5 slice: U pull
-            // 145 -> 110 us per round against 6 rows at 3, profiles/r02_pull_geometry.md)
-            if constexpr (SIDE == SIDE_U && LB == 16 && sizeof(T) == 4) return k_pull_sw<B, T, SIDE_U, 8, 3>;
+            if constexpr (sizeof(T) == 8 && B == 64) {  // 16-byte fp64 lanes (c2 fp64)
+                if constexpr (SIDE == SIDE_V) return k_pull_sw<B, T, SIDE_V, 6, 3>;
+                else return k_pull_sw<B, T, SIDE_U, 5, 4>;
+            }
+            if constexpr (LB == 8) {  // 64 fp32 slots (c2)
+                if constexpr (SIDE == SIDE_V) return k_pull_sw<B, T, SIDE_V, 7, 4>;
+                else return k_pull_sw<B, T, SIDE_U, 7, 4>;
+            }
+            if constexpr (LB == 16 && sizeof(T) == 4) {  // 128 fp32 slots (c3, c4, c5)
+                if constexpr (SIDE == SIDE_V) return k_pull_sw<B, T, SIDE_V, 10, 2>;
+                else return k_pull_sw<B, T, SIDE_U, 8, 3>;
+            }
             if constexpr (SIDE == SIDE_U && SwPipe<B, T>::MINB == 3) return k_pull_sw<B, T, SIDE_U, SwPipe<B, T>::S, 4>;
             return k_pull_sw<B, T, SIDE>;
         }
@@ -322,6 +333,11 @@ struct Engine final : EngineBase {
             if (v == "8,3") return k_pull_sw<B, T, SIDE, 8, 3>;
             if (v == "4,4") return k_pull_sw<B, T, SIDE, 4, 4>;
             if (v == "6,4") return k_pull_sw<B, T, SIDE, 6, 4>;
+            if (v == "7,4") return k_pull_sw<B, T, SIDE, 7, 4>;
+            if (v == "8,4") return k_pull_sw<B, T, SIDE, 8, 4>;
+            if (v == "5,4") return k_pull_sw<B, T, SIDE, 5, 4>;
+            if (v == "10,3") return k_pull_sw<B, T, SIDE, 10, 3>;
+            if (v == "10,2") return k_pull_sw<B, T, SIDE, 10, 2>;
         }
         return sw_kernel<SIDE>();
     }
