@@ -31,6 +31,8 @@ roofline: the dominant kernel (K2 V pull): SURVEY.md 8(d) algorithmic bytes
           traffic from the committed ncu capture.
 hbm_regime: the same measurement at config c3 (|E|=1e8, operands far larger
           than L2), N=1 only (--no-c3 skips it).
+latency_c1: config c1 (configs[0]) single-query latency through the public
+          API (the cluster small path) beside the C port on one host core.
 cpu_baseline / --impl reference: the bit-exact C port of the reference
           (oracle/) on all host cores, the reference's thread-pool pattern.
 """
@@ -542,6 +544,43 @@ def c3_leg(n_sources, dev, stream, flush_buf, peak, peak_src):
     return out
 
 
+def c1_leg(n_queries: int = 16):
+    """Config c1 (configs[0], the reference's CPU-runnable case): single-query
+    latency through the public API (one source per call, fp64, the cluster
+    small path), beside the bit-exact C port on ONE host core for the same
+    sources."""
+    import torch
+
+    import paper_2312_06724_b200 as bh
+    from oracle import cpu_oracle as O
+    from paper_2312_06724_b200.synth import CONFIGS, bench_sources, make_graph
+
+    cfg = CONFIGS["c1"]
+    g = make_graph(cfg, device=torch.cuda.current_device())
+    meta = bh.build_index_meta(g, cfg.alpha)
+    eps = cfg.epsilons[0]
+    src = bench_sources(cfg.u_count, n_queries)
+    bh.bhpp_query_batch(g, meta, src[:1], eps, k=cfg.k, dtype="fp64")  # warm
+    ts = []
+    for s in src:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        bh.bhpp_query_batch(g, meta, [int(s)], eps, k=cfg.k, dtype="fp64")
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+    og = O.OracleGraph(g)
+    eb = float(meta.eps_split_policy(eps))
+    t0 = time.perf_counter()
+    for s in src[:4]:
+        og.bhpp_query(int(s), cfg.alpha, meta.lam, eb, eps - eb)
+    cpu_ms = (time.perf_counter() - t0) / 4 * 1e3
+    med = float(np.median(ts)) * 1e3
+    return {"config": "c1: |U|=1000, |V|=1500, |E|=10000, alpha=0.15, eps=1e-6, fp64, one source per call",
+            "ms_per_query": med, "queries_per_s": 1e3 / med, "queries": len(src),
+            "path": "bhpp_query_batch with one source (thread-block-cluster small path)",
+            "cpu_one_core_ms_per_query": cpu_ms, "cpu_kind": "port (oracle/bhpp_oracle.c, 1 thread)"}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -603,6 +642,10 @@ def run_ours(args):
         eb = float(meta.eps_split_policy(eps))
         cpu = cpu_leg(g, src, cfg.alpha, eb, eps - eb, meta.lam, args.cpu_seconds)
 
+    c1 = None
+    if rank == 0 and world == 1 and args.config == "c2":
+        c1 = c1_leg()
+
     hbm = None
     if world == 1 and not args.no_c3 and args.config == "c2":
         hbm = c3_leg(args.c3_sources, dev, stream, flush_buf, peak, peak_src)
@@ -628,6 +671,7 @@ def run_ours(args):
             "clocks": clk,
             "fp64": fp64,
             "hbm_regime": hbm,
+            "latency_c1": c1,
             "trace_sample": {"sel_b": int(t0["sel_b"][0]), "seq_b": int(t0["seq_b"][0]), "sel_f": int(t0["sel_f"][0]),
                              "pi_iters": int(t0["pi_iters"][0]), "n_p_f": int(t0["n_p_f"][0])} if len(t0) else None,
         }

@@ -19,6 +19,8 @@
 #include "control.cuh"
 #include "kernels.cuh"
 #include "topk.cuh"
+#include <nvtx3/nvToolsExt.h>
+
 #include "small.cuh"
 #include "frontier.cuh"
 
@@ -1608,6 +1610,10 @@ int bh_graph_get_info(const bh_graph *g, bh_graph_info *out) {
 int bh_query_batch(bh_graph *g, const bh_query_params *p, const int32_t *sources, int64_t n_q,
                    const int32_t *tie_skip, int32_t *topk_idx, double *topk_score, bh_trace *trace,
                    double *scores, void *stream) {
+    struct NvtxRange {  // one NVTX range per batch (nsys / ncu --nvtx)
+        NvtxRange() { nvtxRangePushA("bh_query_batch"); }
+        ~NvtxRange() { nvtxRangePop(); }
+    } nvtx_range;
     const double t_entry =
         std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
     return guarded([&] {
@@ -1742,6 +1748,10 @@ int bh_query_batch(bh_graph *g, const bh_query_params *p, const int32_t *sources
 int bh_push_run(bh_graph *g, int32_t job, int32_t source, double alpha, double lam, double eps_b, double eps_f,
                 int32_t tie_skip, double *residue_u, double *estimate, int64_t *n_p, double *scores,
                 bh_trace *trace, bh_round_hook hook, void *user) {
+    struct NvtxRange {
+        NvtxRange() { nvtxRangePushA("bh_push_run"); }
+        ~NvtxRange() { nvtxRangePop(); }
+    } nvtx_range;
     return guarded([&] {
         if (!g || !trace) throw InvalidArg("null argument");
         if (job < BH_JOB_BHPP || job > BH_JOB_PI_PUSH) throw InvalidArg("bad job");
