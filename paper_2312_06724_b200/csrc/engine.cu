@@ -246,6 +246,8 @@ struct Engine final : EngineBase {
     FrontCtl *front = nullptr;
     FrontCtl *h_front = nullptr;
     uint8_t *flag_u = nullptr;
+    FrontPiece *hub_pieces = nullptr;
+    int64_t n_hub_pieces = 0;
     uint32_t *bits_v = nullptr, *bits_u = nullptr;
     FrontItem *items_v = nullptr, *items_u = nullptr;
     double *fscr_v = nullptr, *fscr_u = nullptr;
@@ -424,19 +426,33 @@ struct Engine final : EngineBase {
             BH_CUDA(cudaMemset(front, 0, sizeof(FrontCtl)));
             flag_u = dalloc<uint8_t>(nu);
             BH_CUDA(cudaMemset(flag_u, 0, nu));
+            std::vector<FrontPiece> pcs;  // hub U rows cut into FRONT_WALK-edge claim pieces
+            for (int64_t r = 0; r < nu; r++) {
+                const int64_t e0 = g->U.h_indptr[r], e1 = g->U.h_indptr[r + 1];
+                if (e1 - e0 <= FRONT_WALK) continue;
+                for (int64_t e = e0; e < e1; e += FRONT_WALK) pcs.push_back({e, std::min(e1, e + FRONT_WALK), (int32_t)r, 0});
+            }
+            n_hub_pieces = (int64_t)pcs.size();
+            hub_pieces = dalloc<FrontPiece>(std::max<size_t>(1, pcs.size()));
+            if (!pcs.empty())
+                BH_CUDA(cudaMemcpy(hub_pieces, pcs.data(), pcs.size() * sizeof(FrontPiece), cudaMemcpyHostToDevice));
             bits_v = dalloc<uint32_t>((nv + 31) / 32);
             bits_u = dalloc<uint32_t>((nu + 31) / 32);
             BH_CUDA(cudaMemset(bits_v, 0, ((nv + 31) / 32) * 4));
             BH_CUDA(cudaMemset(bits_u, 0, ((nu + 31) / 32) * 4));
-            items_v = dalloc<FrontItem>(nv + chunks);
-            items_u = dalloc<FrontItem>(nu + chunks);
+            // item slots: rows + hub chunks, at most doubled by the per-warp allocation
+            // chunks (an abandoned chunk is at least half used), plus one open chunk per
+            // warp of the claim kernels
+            grid_front = 4 * sms;
+            const int64_t open = (int64_t)FRONT_ITEM_CHUNK * grid_front * 8 + FRONT_ITEM_CHUNK;
+            items_v = dalloc<FrontItem>(2 * (nv + chunks) + open);
+            items_u = dalloc<FrontItem>(2 * (nu + chunks) + open);
             fscr_v = dalloc<double>((size_t)parts * B);
             fscr_u = dalloc<double>((size_t)parts * B);
             pcnt_v = dalloc<int32_t>(parts);
             pcnt_u = dalloc<int32_t>(parts);
             BH_CUDA(cudaMemset(pcnt_v, 0, parts * 4));
             BH_CUDA(cudaMemset(pcnt_u, 0, parts * 4));
-            grid_front = 4 * sms;
         }
     }
 
@@ -483,7 +499,7 @@ struct Engine final : EngineBase {
         cudaFree(part.any); cudaFree(part.sum); cudaFree(part.wsum);
         cudaFree(scratch); cudaFree(cand_key); cudaFree(cand_idx);
         cudaFree(hook_r); cudaFree(hook_est); cudaFree(chunk_done);
-        cudaFree(front); cudaFreeHost(h_front); cudaFree(flag_u); cudaFree(bits_v); cudaFree(bits_u);
+        cudaFree(front); cudaFreeHost(h_front); cudaFree(flag_u); cudaFree(hub_pieces); cudaFree(bits_v); cudaFree(bits_u);
         cudaFree(items_v); cudaFree(items_u); cudaFree(fscr_v); cudaFree(fscr_u); cudaFree(pcnt_v); cudaFree(pcnt_u);
         plan_u.free_all();
         plan_v.free_all();
@@ -576,6 +592,8 @@ struct Engine final : EngineBase {
         fa.u_col = g->U.indices;
         fa.v_col = g->V.indices;
         fa.flag_u = flag_u;
+        fa.hub_pieces = hub_pieces;
+        fa.n_hub_pieces = n_hub_pieces;
         fa.bits_v = bits_v;
         fa.bits_u = bits_u;
         fa.items_v = items_v;

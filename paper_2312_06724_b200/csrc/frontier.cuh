@@ -22,19 +22,23 @@
 //   Fa   k_front_reset: XV / Y rows written non-zero by the previous frontier
 //        round (its item lists) -- or every row, after dense rounds -- are
 //        zeroed, and the row bitmaps cleared.
-//   Fb   k_front_mark<SIDE_V>: one warp per 32 flag bytes; for every pushed
-//        u the warp walks u's edges 32 at a time, claims each neighbour v in
-//        the V bitmap (atomicOr: exactly one claimant per row) and appends the
-//        claimed rows as work items with warp-aggregated atomics (one
-//        atomicAdd per 32 edges for items, partial slots and edge count).
-//        Degree binning: a row of d edges becomes ceil(d / FRONT_CHUNK) items;
-//        split rows publish fp64 partials and the last item to arrive adds
-//        them in chunk order (deterministic), so hub rows do not serialise.
+//   Fb   k_front_mark<SIDE_V>: the pushed U rows' edges are walked 32 at a
+//        time by one warp each -- rows of more than FRONT_WALK edges as
+//        host-cut pieces shared by several warps, the others one warp per row
+//        from the flag bytes -- claiming each neighbour v in the V bitmap
+//        (a test, then atomicOr: exactly one claimant per row) and appending
+//        the claimed rows as work items.  Warp-aggregated allocation: each warp
+//        reserves item slots in chunks of FRONT_ITEM_CHUNK (one atomicAdd per
+//        chunk; unused slots become empty items), partial slots with one
+//        atomicAdd per 32 edges, edge counts once per warp.  Degree binning on
+//        the output side: a row of d edges becomes ceil(d / FRONT_CHUNK) items;
+//        split rows publish fp64 partials and the last item to arrive adds them
+//        in chunk order (deterministic), so hub rows do not serialise.
 //   Fc   k_front_pull<SIDE_V>: XV rows of the V items, n_p partials per warp
 //        (the dense pull's layout).  It also takes the U half's decision:
 //        frontier iff sum deg(V list) <= limit (the reference's _flush_v test).
-//   Fd   k_front_mark<SIDE_U>: walks the V items' edge ranges into the U
-//        bitmap / U items.
+//   Fd   k_front_mark<SIDE_U>: walks the V items' edge ranges (in FRONT_WALK-
+//        edge pieces) into the U bitmap / U items.
 //   Fe   k_front_pull<SIDE_U>: Y rows of the U items.  When the U half is
 //        dense, the dense U pull runs instead (gate_udense): XV is exact on
 //        every row (zero outside the V list), so the dense pull is too.
@@ -61,6 +65,13 @@
 namespace bh {
 
 constexpr int FRONT_CHUNK = 2048;  // edges per work item (longer rows are split)
+constexpr int FRONT_WALK = 256;    // edges per claim walk (hub rows walked by several warps)
+
+// A piece of a hub row's edges for the claim walk (host plan, static per graph).
+struct FrontPiece {
+    int64_t e0, e1;
+    int32_t row, pad;
+};
 
 struct FrontItem {
     int64_t e0;          // first edge (CSR slot of the row's side)
@@ -94,6 +105,8 @@ struct FrontArgs {
     const int64_t *u_ptr, *v_ptr;
     const int32_t *u_col, *v_col;
     const uint8_t *flag_u;  // [n_u] K1: some slot pushed u
+    const FrontPiece *hub_pieces;  // U rows of more than FRONT_WALK edges, cut into pieces
+    int64_t n_hub_pieces;
     uint32_t *bits_v, *bits_u;
     FrontItem *items_v, *items_u;
     void *XV, *Y;           // [n][B] elements of elem_bytes
@@ -121,7 +134,7 @@ __global__ void k_front_reset(FrontArgs a) {
     auto zero_listed = [&](uint32_t *base, uint32_t *bits, const FrontItem *items, int n_items, bool rows) {
         for (int64_t it = gw; it < n_items; it += nw) {
             const FrontItem w = items[it];
-            if (w.part >= 0 && w.part != w.first_part) continue;  // one item per row
+            if (w.row < 0 || (w.part >= 0 && w.part != w.first_part)) continue;  // empty / one item per row
             if (rows)
                 for (int64_t j = lane; j < row_words; j += 32) base[(int64_t)w.row * row_words + j] = 0u;
             if (lane == 0) atomicAnd(&bits[w.row >> 5], ~(1u << (w.row & 31)));
@@ -134,11 +147,38 @@ __global__ void k_front_reset(FrontArgs a) {
     zero_listed(reinterpret_cast<uint32_t *>(a.Y), a.bits_u, a.items_u, f->old_items_u, !all_u);
 }
 
+// Per-warp item allocator: item slots are reserved from the global counter in
+// chunks (one atomicAdd per FRONT_ITEM_CHUNK items instead of one per 32
+// edges -- every warp of the grid otherwise hammers one address: a forced c2
+// round spent 5-7 ms in the V mark).  Unused slots of a chunk are written as
+// empty items (row = -1), which the readers skip.  Values are warp-uniform.
+constexpr int FRONT_ITEM_CHUNK = 64;
+struct WarpAlloc {
+    int32_t next = 0, end = 0;
+    unsigned long long edges = 0;  // lane 31: edges of the rows this warp claimed
+};
+
+__device__ __forceinline__ void front_pad_empty(FrontItem *items, int32_t from, int32_t to) {
+    const int lane = threadIdx.x & 31;
+    for (int32_t i = from + lane; i < to; i += 32) {
+        FrontItem w{};
+        w.row = -1;
+        items[i] = w;
+    }
+}
+
+__device__ __forceinline__ void front_flush(WarpAlloc &al, FrontItem *items, unsigned long long *edges) {
+    front_pad_empty(items, al.next, al.end);
+    al.next = al.end;
+    if ((threadIdx.x & 31) == 31 && al.edges) atomicAdd(edges, al.edges);
+    al.edges = 0;
+}
+
 // Claims the other-side rows of edges [e0, e1) (one warp, all lanes) and
 // appends the newly claimed rows as work items.
 __device__ __forceinline__ void front_claim(int64_t e0, int64_t e1, const int32_t *__restrict__ col,
                                             const int64_t *__restrict__ dst_ptr, uint32_t *bits, FrontItem *items,
-                                            int32_t *n_items, int32_t *n_parts, unsigned long long *edges) {
+                                            int32_t *n_items, int32_t *n_parts, WarpAlloc &al) {
     const int lane = threadIdx.x & 31;
     for (int64_t base = e0; base < e1; base += 32) {
         const int64_t e = base + lane;
@@ -147,7 +187,8 @@ __device__ __forceinline__ void front_claim(int64_t e0, int64_t e1, const int32_
         if (e < e1) {
             c = __ldg(col + e);
             const uint32_t bit = 1u << (c & 31);
-            fresh = !(atomicOr(&bits[c >> 5], bit) & bit);
+            // test before the atomic: a claimed hub row is met by many walks at once
+            if (!(__ldcg(&bits[c >> 5]) & bit)) fresh = !(atomicOr(&bits[c >> 5], bit) & bit);
         }
         const unsigned nb = __ballot_sync(0xffffffffu, fresh);
         if (!nb) continue;
@@ -171,16 +212,22 @@ __device__ __forceinline__ void front_claim(int64_t e0, int64_t e1, const int32_
             }
             s_d += __shfl_xor_sync(0xffffffffu, s_d, o);
         }
-        int b_it = 0, b_pt = 0;
-        if (lane == 31) {
-            b_it = atomicAdd(n_items, s_it);
-            b_pt = s_pt ? atomicAdd(n_parts, s_pt) : 0;
-            atomicAdd(edges, s_d);
+        const int tot_it = __shfl_sync(0xffffffffu, s_it, 31);
+        if (al.next + tot_it > al.end) {  // new chunk (the rest of the old one becomes empty items)
+            front_pad_empty(items, al.next, al.end);
+            const int want = tot_it > FRONT_ITEM_CHUNK ? tot_it : FRONT_ITEM_CHUNK;
+            int b = 0;
+            if (lane == 0) b = atomicAdd(n_items, want);
+            b = __shfl_sync(0xffffffffu, b, 0);
+            al.next = b;
+            al.end = b + want;
         }
-        b_it = __shfl_sync(0xffffffffu, b_it, 31);
+        int b_pt = 0;
+        if (lane == 31 && s_pt) b_pt = atomicAdd(n_parts, s_pt);
         b_pt = __shfl_sync(0xffffffffu, b_pt, 31);
+        if (lane == 31) al.edges += s_d;
         if (fresh) {
-            const int it0 = b_it + s_it - n_it;
+            const int it0 = al.next + s_it - n_it;
             const int pt0 = b_pt + s_pt - n_pt;
             for (int k = 0; k < n_it; k++) {
                 FrontItem w;
@@ -194,6 +241,7 @@ __device__ __forceinline__ void front_claim(int64_t e0, int64_t e1, const int32_
                 items[it0 + k] = w;
             }
         }
+        al.next += tot_it;
     }
 }
 
@@ -206,26 +254,43 @@ __global__ void __launch_bounds__(256) k_front_mark(FrontArgs a) {
     const int lane = threadIdx.x & 31;
     const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    WarpAlloc al;
     if constexpr (SIDE == SIDE_V) {
+        // hub rows (more than FRONT_WALK edges) as host-cut pieces, so several warps
+        // share a hub's walk (degree binning: a c2 hub of ~5e4 edges walked by one warp
+        // took 5-7 ms); then the other pushed rows, one warp per row
+        for (int64_t p = gw; p < a.n_hub_pieces; p += nw) {
+            const FrontPiece pc = a.hub_pieces[p];
+            if (!a.flag_u[pc.row]) continue;
+            front_claim(pc.e0, pc.e1, a.u_col, a.v_ptr, a.bits_v, a.items_v, &f->n_items_v, &f->n_parts_v, al);
+        }
         for (int64_t base = gw * 32; base < a.n_u; base += nw * 32) {
             const int64_t u = base + lane;
-            const bool pushed = u < a.n_u && a.flag_u[u];
+            bool pushed = false;
+            if (u < a.n_u && a.flag_u[u]) pushed = __ldg(a.u_ptr + u + 1) - __ldg(a.u_ptr + u) <= FRONT_WALK;
             unsigned m = __ballot_sync(0xffffffffu, pushed);
             while (m) {
                 const int j = __ffs(m) - 1;
                 m &= m - 1;
                 const int64_t uu = base + j;
                 front_claim(__ldg(a.u_ptr + uu), __ldg(a.u_ptr + uu + 1), a.u_col, a.v_ptr, a.bits_v, a.items_v,
-                            &f->n_items_v, &f->n_parts_v, &f->edges_v);
+                            &f->n_items_v, &f->n_parts_v, al);
             }
         }
+        front_flush(al, a.items_v, &f->edges_v);
     } else {
-        const int n = f->n_items_v;
+        // the V items' edge ranges in FRONT_WALK-edge pieces (an item holds up to
+        // FRONT_CHUNK edges)
+        constexpr int PER = FRONT_CHUNK / FRONT_WALK;
+        const int64_t n = (int64_t)f->n_items_v * PER;
         for (int64_t it = gw; it < n; it += nw) {
-            const FrontItem w = a.items_v[it];
-            front_claim(w.e0, w.e0 + w.len, a.v_col, a.u_ptr, a.bits_u, a.items_u, &f->n_items_u, &f->n_parts_u,
-                        &f->edges_u);
+            const FrontItem w = a.items_v[it / PER];
+            const int64_t b0 = w.e0 + (it % PER) * FRONT_WALK;
+            const int64_t b1 = w.e0 + w.len < b0 + FRONT_WALK ? w.e0 + w.len : b0 + FRONT_WALK;
+            if (w.row < 0 || b0 >= b1) continue;  // empty slot / past the item's end
+            front_claim(b0, b1, a.v_col, a.u_ptr, a.bits_u, a.items_u, &f->n_items_u, &f->n_parts_u, al);
         }
+        front_flush(al, a.items_u, &f->edges_u);
     }
 }
 
@@ -284,6 +349,7 @@ __global__ void __launch_bounds__(PULL_THREADS) k_front_pull(FrontPullArgs<T> a)
     for (int v = 0; v < VEC; v++) np[v] = 0;
     for (int it = gw; it < n_items; it += nw) {
         const FrontItem w = a.items[it];
+        if (w.row < 0) continue;  // empty slot of an allocation chunk (warp-uniform)
         const int64_t e_end = w.e0 + w.len;
         double acc[VEC];
 #pragma unroll
