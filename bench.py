@@ -589,9 +589,18 @@ def run_ours(args):
     from paper_2312_06724_b200 import _capi
 
     rank, world, local = dist_env()
+    # test hooks for the multi-rank path on a one-GPU box (never set by the driver):
+    # BH_BENCH_DEVICE pins every rank to one device, BH_DIST_BACKEND=gloo because
+    # NCCL refuses two ranks on one device
+    if os.environ.get("BH_BENCH_DEVICE"):
+        local = int(os.environ["BH_BENCH_DEVICE"])
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("BH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
 
     cfg, g, src, total = workload(args.config, rank, world, args.scaling, args.batch)
@@ -693,7 +702,7 @@ def main():
             have = torch.cuda.device_count()
         except Exception:  # noqa: BLE001
             have = 0
-        if have < args.gpus:
+        if have < args.gpus and not os.environ.get("BH_BENCH_DEVICE"):
             print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible CUDA devices, found {have}", file=sys.stderr)
             sys.exit(2)
         sys.exit(relaunch_under_torchrun(args))
