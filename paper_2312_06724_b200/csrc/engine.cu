@@ -326,33 +326,7 @@ struct Engine final : EngineBase {
             return k_pull_sw<B, T, SIDE>;
         }
     }
-    // A/B of the pull geometry (BH_PULL_CFG_V / BH_PULL_CFG_U = "S,MINB")
-    template <int SIDE>
-    static PullFn ab_kernel(const char *m) {
-        if constexpr (WIDE) {
-            const std::string v(m);
-            if (v == "8,2") return k_pull_sw<B, T, SIDE, 8, 2>;
-            if (v == "6,3") return k_pull_sw<B, T, SIDE, 6, 3>;
-            if (v == "5,3") return k_pull_sw<B, T, SIDE, 5, 3>;
-            if (v == "8,3") return k_pull_sw<B, T, SIDE, 8, 3>;
-            if (v == "4,4") return k_pull_sw<B, T, SIDE, 4, 4>;
-            if (v == "6,4") return k_pull_sw<B, T, SIDE, 6, 4>;
-            if (v == "7,4") return k_pull_sw<B, T, SIDE, 7, 4>;
-            if (v == "8,4") return k_pull_sw<B, T, SIDE, 8, 4>;
-            if (v == "5,4") return k_pull_sw<B, T, SIDE, 5, 4>;
-            if (v == "10,3") return k_pull_sw<B, T, SIDE, 10, 3>;
-            if (v == "10,2") return k_pull_sw<B, T, SIDE, 10, 2>;
-        }
-        return sw_kernel<SIDE>();
-    }
-    static PullFn pull_kernel(int side) {
-        if (side == SIDE_V) {
-            const char *m = getenv("BH_PULL_CFG_V");
-            return m ? ab_kernel<SIDE_V>(m) : sw_kernel<SIDE_V>();
-        }
-        const char *m = getenv("BH_PULL_CFG_U");
-        return m ? ab_kernel<SIDE_U>(m) : sw_kernel<SIDE_U>();
-    }
+    static PullFn pull_kernel(int side) { return side == SIDE_V ? sw_kernel<SIDE_V>() : sw_kernel<SIDE_U>(); }
 
     explicit Engine(bh_graph *graph) : g(graph) {
         this->nslots = B;
