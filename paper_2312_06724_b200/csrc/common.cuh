@@ -94,11 +94,22 @@ struct CutRow {
 // hub columns.  Each row keeps the caller's edge order, so every row sum adds
 // the same terms in the same order as without relabelling.  perm / inv map
 // store index -> caller index and back (null when the caller's order is kept).
+// One edge of the dense pulls' stream: column and prescaled value side by side,
+// so a lane fetches its edge with one load.  v < 0 marks the last edge of a row
+// (values are w / ws(row) > 0), which replaces the row-pointer walk in the pull.
+template <typename T>
+struct alignas(2 * sizeof(T)) EdgeRF {
+    int32_t c;
+    T v;
+};
+
 struct Side {
     int64_t n_rows = 0;
     int64_t *indptr = nullptr;   // [n_rows + 1]
     int32_t *indices = nullptr;  // [E] column (other side) index, store order
     void *vals = nullptr;        // [E] T, w / ws(row)
+    void *ecv = nullptr;         // [E] EdgeRF<T>: (column, value) pairs for the dense pulls, the value
+                                 // negated on the last edge of its row (null when some row is empty)
     int32_t *deg = nullptr;      // [n_rows]
     int32_t *perm = nullptr;     // [n_rows] store row -> caller row (null: identity)
     int32_t *inv = nullptr;      // [n_rows] caller row -> store row (null: identity)

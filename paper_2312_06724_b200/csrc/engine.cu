@@ -151,7 +151,8 @@ struct EngineBase {
 };
 
 // Merge-path partition of one pull side into n_warps contiguous edge ranges
-// balanced on (edges + ROWCOST * rows); rows cut by a boundary get one partial
+// balanced on (edges + ROWCOST * rows), boundaries snapped to row starts where
+// the row is short; rows cut by a boundary get one partial
 // slot per warp touching them (SURVEY.md sec. 7 hard part 3: hub rows of
 // ~1e6 edges must not serialise).
 struct SidePlan {
@@ -175,6 +176,7 @@ static void build_plan(const Side &sd, int64_t n_e, int n_warps, SidePlan &pl) {
     const std::vector<int64_t> &ip = sd.h_indptr;
     const int64_t n = sd.n_rows;
     const int64_t total = n_e + ROWCOST * n;
+    const int64_t snap = std::max<int64_t>(32, n_e / std::max(1, n_warps) / 8);
     std::vector<int64_t> eb((size_t)n_warps + 1);
     eb[0] = 0;
     eb[n_warps] = n_e;
@@ -186,6 +188,10 @@ static void build_plan(const Side &sd, int64_t n_e, int n_warps, SidePlan &pl) {
             if (ip[mid] + ROWCOST * mid <= d) lo = mid; else hi = mid - 1;
         }
         int64_t e = lo >= n ? n_e : std::min(std::max(d - ROWCOST * lo, ip[lo]), ip[lo + 1]);
+        // a boundary inside a short row moves to the nearer row start: only rows that are long
+        // against a warp's range (hubs) are cut, so most warps skip the cut protocol (two
+        // fences and an atomic per cut) at the cost of at most snap / 2 edges of imbalance
+        if (lo < n && ip[lo + 1] - ip[lo] <= snap) e = (e - ip[lo] < ip[lo + 1] - e) ? ip[lo] : ip[lo + 1];
         eb[w] = std::max(e, eb[w - 1]);
     }
     std::vector<WarpWork> work((size_t)n_warps);
@@ -326,7 +332,28 @@ struct Engine final : EngineBase {
             return k_pull_sw<B, T, SIDE>;
         }
     }
-    static PullFn pull_kernel(int side) { return side == SIDE_V ? sw_kernel<SIDE_V>() : sw_kernel<SIDE_U>(); }
+    // Row-flag pull geometries (rows in flight per warp, 256-thread blocks per SM);
+    // BH_RF_GEO="v,u" picks one per side for A/B runs.
+    static constexpr int RF_GEOS = 4;
+    template <int SIDE>
+    static PullFn rf_kernel(int geo) {
+        if constexpr (!WIDE) {
+            return nullptr;
+        } else {
+            switch (geo) {
+                case 0: return k_pull_rf<B, T, SIDE, 8, 3>;
+                case 1: return k_pull_rf<B, T, SIDE, 8, 2>;
+                case 2: return k_pull_rf<B, T, SIDE, 4, 4>;
+                default: return k_pull_rf<B, T, SIDE, 8, 4>;
+            }
+        }
+    }
+    bool use_rf = false;
+    int rf_geo[2] = {0, 0};
+    PullFn pull_kernel(int side) const {
+        if (use_rf) return side == SIDE_V ? rf_kernel<SIDE_V>(rf_geo[0]) : rf_kernel<SIDE_U>(rf_geo[1]);
+        return side == SIDE_V ? sw_kernel<SIDE_V>() : sw_kernel<SIDE_U>();
+    }
 
     explicit Engine(bh_graph *graph) : g(graph) {
         this->nslots = B;
@@ -350,13 +377,30 @@ struct Engine final : EngineBase {
         int sms = 148;
         BH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
         setup_l2_windows(nu, nv);
+        // dense pull selection: the row-flag pull when the store has the flagged edge
+        // stream (no empty row); BH_PULL=sw keeps the row-pointer pull (A/B)
+        use_rf = WIDE && g->U.ecv && g->V.ecv;
+        if (const char *m = getenv("BH_PULL")) use_rf = use_rf && strcmp(m, "sw") != 0;
+        if (use_rf) {
+            constexpr int LB = (B / 32) * (int)sizeof(T);
+            rf_geo[0] = rf_geo[1] = LB <= 8 ? 3 : 0;
+            if (const char *m = getenv("BH_RF_GEO")) {  // "v,u"
+                int gv = rf_geo[0], gu = rf_geo[1];
+                const int k = sscanf(m, "%d,%d", &gv, &gu);
+                if (k == 1) gu = gv;
+                if (k >= 1) {
+                    rf_geo[0] = std::min(std::max(gv, 0), RF_GEOS - 1);
+                    rf_geo[1] = std::min(std::max(gu, 0), RF_GEOS - 1);
+                }
+            }
+        }
         for (int side = 0; side < 2; side++) {
+            const Side &sd = side == SIDE_V ? g->V : g->U;
+            SidePlan &pl = side == SIDE_V ? plan_v : plan_u;
             PullFn fn = pull_kernel(side);
             int occ = 1;
             BH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, PULL_THREADS, 0));
             occ = std::max(1, occ);
-            const Side &sd = side == SIDE_V ? g->V : g->U;
-            SidePlan &pl = side == SIDE_V ? plan_v : plan_u;
             // one resident wave of warps, fewer if the side is tiny
             int64_t grid = (int64_t)occ * sms;
             const int64_t want = (g->n_e + 2 * sd.n_rows) / 64 / PULL_WARPS + 1;
@@ -521,6 +565,7 @@ struct Engine final : EngineBase {
         a.active = &ctl->active;
         a.np_v = part.np_v;
         a.one_minus_alpha = one_minus_alpha;
+        a.ecv = sd.ecv;
         return a;
     }
 

@@ -29,7 +29,7 @@ __global__ void k_build_rows(int64_t n_rows, const int64_t *__restrict__ old_ind
                              const double *__restrict__ w, const double *__restrict__ ws_old,
                              const int32_t *__restrict__ perm, const int32_t *__restrict__ inv_col,
                              const int64_t *__restrict__ new_indptr, int32_t *__restrict__ new_idx,
-                             T *__restrict__ vals) {
+                             T *__restrict__ vals, EdgeRF<T> *__restrict__ ecv) {
     const int lane = threadIdx.x & 31;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < n_rows; i += nw) {
@@ -37,9 +37,12 @@ __global__ void k_build_rows(int64_t n_rows, const int64_t *__restrict__ old_ind
         const int64_t o = old_indptr[r], deg = old_indptr[r + 1] - o, n = new_indptr[i];
         const double ws = ws_old[r];
         for (int64_t k = lane; k < deg; k += 32) {
-            const int32_t c = old_idx[o + k];
-            new_idx[n + k] = inv_col ? inv_col[c] : c;
-            vals[n + k] = (T)(w[o + k] / ws);
+            const int32_t c0 = old_idx[o + k];
+            const int32_t c = inv_col ? inv_col[c0] : c0;
+            const T v = (T)(w[o + k] / ws);
+            new_idx[n + k] = c;
+            vals[n + k] = v;
+            if (ecv) ecv[n + k] = EdgeRF<T>{c, k == deg - 1 ? -v : v};
         }
     }
 }
@@ -101,6 +104,9 @@ void upload_side(Side &s, int64_t n_rows, int64_t n_e, const int64_t *indptr, co
     s.indices = dmalloc<int32_t>(n_e, acc);
     s.vals = dmalloc<T>(n_e, acc);
     s.deg = dmalloc<int32_t>(n_rows, acc);
+    bool no_empty_row = true;
+    for (int64_t i = 0; i < n_rows && no_empty_row; i++) no_empty_row = indptr[i + 1] > indptr[i];
+    s.ecv = no_empty_row ? (void *)dmalloc<EdgeRF<T>>(n_e, acc) : nullptr;
     std::vector<int64_t> nip;
     const int64_t *new_ip = indptr;
     if (!perm.empty()) {
@@ -127,7 +133,7 @@ void upload_side(Side &s, int64_t n_rows, int64_t n_e, const int64_t *indptr, co
     BH_CUDA(cudaMemcpy(dws, ws_rows, n_rows * sizeof(double), cudaMemcpyHostToDevice));
     if (d_invc) BH_CUDA(cudaMemcpy(d_invc, inv_col.data(), inv_col.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     k_build_rows<T><<<grid_for(n_rows * 32), 256>>>(n_rows, d_oip, d_oidx, dw, dws, s.perm, d_invc, s.indptr,
-                                                     s.indices, (T *)s.vals);
+                                                     s.indices, (T *)s.vals, (EdgeRF<T> *)s.ecv);
     count_launch();
     BH_CUDA(cudaGetLastError());
     k_deg<<<grid_for(n_rows), 256>>>(n_rows, s.indptr, s.deg);
@@ -148,6 +154,7 @@ void free_side(Side &s) {
     cudaFree(s.indptr);
     cudaFree(s.indices);
     cudaFree(s.vals);
+    cudaFree(s.ecv);
     cudaFree(s.deg);
     s = Side{};
 }

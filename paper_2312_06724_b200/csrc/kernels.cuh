@@ -129,6 +129,19 @@ __device__ __forceinline__ bool op_is_fwd(int op) { return op == OP_FENTRY || op
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
+// cp.async of one element (8 or 16 bytes) into shared memory; !valid zero-fills.
+template <int BYTES>
+__device__ __forceinline__ void cp_async_zfill(uint32_t dst, const void *src, bool valid) {
+    static_assert(BYTES == 8 || BYTES == 16, "cp.async element size");
+    const int sz = valid ? BYTES : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(dst), "l"(src), "n"(BYTES), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // Elementwise kernels over [n_u x B]: one thread per (node, EV consecutive slots).
 constexpr int ELEM_THREADS = 256;
@@ -602,6 +615,7 @@ struct PullArgs {
     const int32_t *active;
     int64_t *np_v;         // [n_warps][B] (V pull)
     double one_minus_alpha;
+    const void *ecv;       // [E] EdgeRF<T> (k_pull_rf)
 };
 
 __device__ __forceinline__ uint64_t gtimer() {
@@ -760,6 +774,7 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) k_pull_sw(PullArgs<T> a) {
             };
             EdgeCV<T>(*win)[S] = s_win[warp];
             int32_t *re = s_re[warp];
+            auto fetch = [&](int c, T(&x)[VEC]) { ldg_vec<T, VEC>(X + (int64_t)c * B, x); };
             re[lane] = rend_at(lane);
             re[32 + lane] = rend_at(32 + lane);
             if (lane < 2 * S) win[lane / S][lane % S] = EdgeCV<T>{col_at(lane), val_at(lane)};
@@ -773,7 +788,7 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) k_pull_sw(PullArgs<T> a) {
             for (int t = 0; t < S; t++) {
                 const EdgeCV<T> e = win[0][t];
                 wsv[t] = e.v;
-                ldg_vec<T, VEC>(X + (int64_t)e.c * B, xs[t]);
+                fetch(e.c, xs[t]);
             }
             int rw = 0;       // row-end ring holds local rows [rw, rw + 64)
             int lr = 0;
@@ -830,7 +845,7 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) k_pull_sw(PullArgs<T> a) {
                     }
                     const EdgeCV<T> e = nxt[t];
                     wsv[t] = e.v;
-                    ldg_vec<T, VEC>(X + (int64_t)e.c * B, xs[t]);
+                    fetch(e.c, xs[t]);
                 }
                 if constexpr (sizeof(T) == 4) {
 #pragma unroll
@@ -876,6 +891,185 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) k_pull_sw(PullArgs<T> a) {
     }
 }
 
+
+// Row-flag pull (the default dense pull for B >= 32).  Same partition, cut-row
+// protocol, n_p layout and summation order within a row as k_pull_sw, with a
+// leaner edge path:
+//   - the edge stream is the store's packed EdgeRF array.  A 32-edge tile goes
+//     from global memory straight into a 128-entry shared ring with one cp.async
+//     per lane, three tiles ahead of its use: no staging registers, and the wait
+//     is on the copy group, not on a scoreboard shared with the operand gathers;
+//   - the per-edge work is one broadcast LDS of (column, value), the operand-row
+//     gather and VEC FMAs;
+//   - the last edge of a row carries a negated value, so the row end is a sign
+//     test on a register that is loaded anyway: no row-pointer ring, no per-edge
+//     offset compare, no reload of row ends;
+//   - S (a divisor of 32) operand rows are in flight per warp in registers; the
+//     S-edge body is unrolled, the bodies of a tile are a loop;
+//   - fp32: products accumulate in fp32 over one S-edge body at most and are
+//     folded into the row's fp64 accumulator after it (and at a row end).
+template <int B, typename T, int SIDE, int S, int MINB>
+__global__ void __launch_bounds__(PULL_THREADS, MINB) k_pull_rf(PullArgs<T> a) {
+    pdl_begin();
+    if (*a.active == 0) return;
+    constexpr int VEC = RegPipe<B, T>::VEC;
+    constexpr int RING = 128;  // four 32-edge tiles
+    static_assert(32 % S == 0, "the S-edge body must tile a 32-edge window");
+    __shared__ EdgeRF<T> s_ring[PULL_WARPS][RING];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int gw = blockIdx.x * PULL_WARPS + warp;
+    const int slot0 = lane * VEC;
+    uint32_t cmask = 0;
+    if constexpr (SIDE == SIDE_V) {
+#pragma unroll
+        for (int v = 0; v < VEC; v++) cmask |= (op_is_push(a.slots[slot0 + v].op) ? 1u : 0u) << v;
+    }
+    const double scale = SIDE == SIDE_V ? a.one_minus_alpha : 1.0;
+    int64_t npt[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; v++) npt[v] = 0;
+    if (gw < a.n_warps) {
+        // only what the edge loop needs stays in registers; the cut fields are read again after it
+        const int64_t e0 = a.work[gw].e0;
+        const int n = (int)(a.work[gw].e1 - e0);
+        if (n > 0) {
+            int32_t np[VEC];
+#pragma unroll
+            for (int v = 0; v < VEC; v++) np[v] = 0;
+            const EdgeRF<T> *ed = reinterpret_cast<const EdgeRF<T> *>(a.ecv) + e0;
+            const T *X = a.X + slot0;
+            T *yrow = a.Y + (int64_t)a.work[gw].r0 * B + slot0;
+            EdgeRF<T> *ring = s_ring[warp];
+            // tile k (edges 32 k + lane) into ring slot k & 3; past the range the copy zero-fills
+            // (column 0, value +0: gathers row 0, adds nothing, ends no row)
+            const uint32_t ring_lane = smem_u32(ring + lane);
+            auto stage = [&](int tile) {
+                const int o = tile * 32 + lane;
+                const EdgeRF<T> *src = ed + (o < n ? o : 0);
+                cp_async_zfill<(int)sizeof(EdgeRF<T>)>(ring_lane + (uint32_t)((tile & 3) * 32 * sizeof(EdgeRF<T>)), src,
+                                                      o < n);
+                cp_async_commit();
+            };
+            auto fetch = [&](int c, T(&x)[VEC]) { ldg_vec<T, VEC>(X + (int64_t)c * B, x); };
+            stage(0);
+            stage(1);
+            stage(2);
+            cp_async_wait<1>();  // tiles 0 and 1 have landed
+            __syncwarp();
+            T xs[S][VEC];
+            T wsv[S];
+#pragma unroll
+            for (int t = 0; t < S; t++) {
+                const EdgeRF<T> e = ring[t];
+                wsv[t] = e.v;
+                fetch(e.c, xs[t]);
+            }
+            double acc[VEC];
+            T accs[VEC];
+#pragma unroll
+            for (int v = 0; v < VEC; v++) {
+                acc[v] = 0.0;
+                accs[v] = (T)0;
+            }
+            const bool first_cut = a.work[gw].cut0 >= 0;
+            int rstart = 0;  // offset of the current row's first edge in the range (0: the range's first row)
+            for (int base = 0; base < n; base += 32) {
+#pragma unroll 1
+                for (int sub = 0; sub < 32; sub += S) {
+                    const EdgeRF<T> *nxt = ring + ((base + sub + S) & (RING - 1));
+#pragma unroll
+                    for (int t = 0; t < S; t++) {
+                        const T w = wsv[t];
+                        if constexpr (sizeof(T) == 8) {
+#pragma unroll
+                            for (int v = 0; v < VEC; v++) acc[v] = fma(fabs((double)w), (double)xs[t][v], acc[v]);
+                        } else {
+#pragma unroll
+                            for (int v = 0; v < VEC; v++) accs[v] = fmaf(fabsf(w), xs[t][v], accs[v]);
+                        }
+                        if (w < (T)0) {  // last edge of a row
+                            if constexpr (sizeof(T) == 4) {
+#pragma unroll
+                                for (int v = 0; v < VEC; v++) {
+                                    acc[v] += (double)accs[v];
+                                    accs[v] = (T)0;
+                                }
+                            }
+                            const int rend = base + sub + t + 1;
+                            if (rstart == 0 && first_cut) {
+                                double *dst = a.scratch + (int64_t)a.work[gw].part0 * B + slot0;
+#pragma unroll
+                                for (int v = 0; v < VEC; v++) dst[v] = acc[v];
+                            } else {
+                                T out[VEC];
+#pragma unroll
+                                for (int v = 0; v < VEC; v++) {
+                                    out[v] = (T)(scale * acc[v]);
+                                    if constexpr (SIDE == SIDE_V)
+                                        np[v] += (((cmask >> v) & 1u) && out[v] > (T)0) ? rend - rstart : 0;
+                                }
+                                VecIO<T, VEC>::st(yrow, out);
+                            }
+#pragma unroll
+                            for (int v = 0; v < VEC; v++) acc[v] = 0.0;
+                            yrow += B;
+                            rstart = rend;
+                        }
+                        const EdgeRF<T> e = nxt[t];
+                        wsv[t] = e.v;
+                        fetch(e.c, xs[t]);
+                    }
+                    if constexpr (sizeof(T) == 4) {
+#pragma unroll
+                        for (int v = 0; v < VEC; v++) {
+                            acc[v] += (double)accs[v];
+                            accs[v] = (T)0;
+                        }
+                    }
+                }
+                // tile base/32 is consumed and the gathers reached at most S edges into the next
+                // one.  Tile + 3 goes into the slot tile - 1 left (its last read was before the
+                // previous iteration's barrier); tile + 2 must have landed before the next
+                // iteration's last body looks S edges ahead.
+                stage((base >> 5) + 3);
+                cp_async_wait<1>();
+                __syncwarp();
+            }
+            cp_async_wait<0>();
+            const WarpWork wk = a.work[gw];
+            if (rstart < n) {  // the range ends inside a row: its partial goes to the cut protocol
+                double *dst = a.scratch + (int64_t)((rstart == 0 && first_cut) ? wk.part0 : wk.part1) * B + slot0;
+#pragma unroll
+                for (int v = 0; v < VEC; v++) dst[v] = acc[v];
+            }
+            const CutCtx<T> cx{a.scratch, a.cut_count, a.cuts, a.Y, a.indptr, scale};
+            if (wk.cut0 >= 0) {
+                DVec<VEC> av;
+#pragma unroll
+                for (int v = 0; v < VEC; v++) av.v[v] = a.scratch[(int64_t)wk.part0 * B + slot0 + v];
+                const IVec<VEC> inc = pull_cut<B, T, VEC>(cx, wk.cut0, wk.part0, slot0, cmask, av);
+#pragma unroll
+                for (int v = 0; v < VEC; v++) npt[v] += inc.v[v];
+            }
+#pragma unroll
+            for (int v = 0; v < VEC; v++) npt[v] += np[v];
+            if (wk.cut1 >= 0) {
+                DVec<VEC> av;
+#pragma unroll
+                for (int v = 0; v < VEC; v++) av.v[v] = a.scratch[(int64_t)wk.part1 * B + slot0 + v];
+                const IVec<VEC> inc = pull_cut<B, T, VEC>(cx, wk.cut1, wk.part1, slot0, cmask, av);
+#pragma unroll
+                for (int v = 0; v < VEC; v++) npt[v] += inc.v[v];
+            }
+        }
+    }
+    if constexpr (SIDE == SIDE_V) {
+        if (gw < a.n_warps)
+#pragma unroll
+            for (int v = 0; v < VEC; v++) a.np_v[(int64_t)(slot0 + v) * a.n_warps + gw] = npt[v];
+    }
+}
 
 // B < 32 (single-query and small blocks): G lanes per edge group, 32/G groups
 // split each row; plain loads.  Same partition, cut rows and epilogue.
