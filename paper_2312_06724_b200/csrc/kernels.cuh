@@ -975,9 +975,26 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) k_pull_rf(PullArgs<T> a) {
             const bool first_cut = a.work[gw].cut0 >= 0;
             int rstart = 0;  // offset of the current row's first edge in the range (0: the range's first row)
             for (int base = 0; base < n; base += 32) {
+                // row ends of this tile, one bit per edge: a body without one runs branch-free
+                const uint32_t tmask = __ballot_sync(0xffffffffu, ring[(base & (RING - 1)) + lane].v < (T)0);
 #pragma unroll 1
                 for (int sub = 0; sub < 32; sub += S) {
                     const EdgeRF<T> *nxt = ring + ((base + sub + S) & (RING - 1));
+                    if (((tmask >> sub) & (uint32_t)((1ull << S) - 1ull)) == 0u) {
+#pragma unroll
+                        for (int t = 0; t < S; t++) {
+                            if constexpr (sizeof(T) == 8) {
+#pragma unroll
+                                for (int v = 0; v < VEC; v++) acc[v] = fma((double)wsv[t], (double)xs[t][v], acc[v]);
+                            } else {
+#pragma unroll
+                                for (int v = 0; v < VEC; v++) accs[v] = fmaf(wsv[t], xs[t][v], accs[v]);
+                            }
+                            const EdgeRF<T> e = nxt[t];
+                            wsv[t] = e.v;
+                            fetch(e.c, xs[t]);
+                        }
+                    } else
 #pragma unroll
                     for (int t = 0; t < S; t++) {
                         const T w = wsv[t];
