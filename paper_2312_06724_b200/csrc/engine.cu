@@ -383,7 +383,7 @@ struct Engine final : EngineBase {
         if (const char *m = getenv("BH_PULL")) use_rf = use_rf && strcmp(m, "sw") != 0;
         if (use_rf) {
             constexpr int LB = (B / 32) * (int)sizeof(T);
-            rf_geo[0] = rf_geo[1] = 0;
+            rf_geo[0] = rf_geo[1] = LB <= 16 ? 0 : 1;  // 8 rows at 3 blocks/SM; 32-byte lanes at 2
             if (const char *m = getenv("BH_RF_GEO")) {  // "v,u"
                 int gv = rf_geo[0], gu = rf_geo[1];
                 const int k = sscanf(m, "%d,%d", &gv, &gu);

@@ -910,8 +910,7 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) k_pull_sw(PullArgs<T> a) {
 //     folded into the row's fp64 accumulator after it (and at a row end).
 template <int B, typename T, int SIDE, int S, int MINB>
 __global__ void __launch_bounds__(PULL_THREADS, MINB) k_pull_rf(PullArgs<T> a) {
-    pdl_begin();
-    if (*a.active == 0) return;
+    pdl_launch_dependents();
     constexpr int VEC = RegPipe<B, T>::VEC;
     constexpr int RING = 128;  // four 32-edge tiles
     static_assert(32 % S == 0, "the S-edge body must tile a 32-edge window");
@@ -920,6 +919,35 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) k_pull_rf(PullArgs<T> a) {
     const int warp = threadIdx.x >> 5;
     const int gw = blockIdx.x * PULL_WARPS + warp;
     const int slot0 = lane * VEC;
+    // The plan and the edge stream are immutable graph data: the first three edge tiles are
+    // put in flight under the predecessor's tail, before the wait for its memory.
+    int64_t e0 = 0;
+    int n = 0;
+    if (gw < a.n_warps) {
+        e0 = a.work[gw].e0;
+        n = (int)(a.work[gw].e1 - e0);
+    }
+    const EdgeRF<T> *ed = reinterpret_cast<const EdgeRF<T> *>(a.ecv) + e0;
+    EdgeRF<T> *ring = s_ring[warp];
+    // tile k (edges 32 k + lane) into ring slot k & 3; past the range the copy zero-fills
+    // (column 0, value +0: gathers row 0, adds nothing, ends no row)
+    const uint32_t ring_lane = smem_u32(ring + lane);
+    auto stage = [&](int tile) {
+        const int o = tile * 32 + lane;
+        const EdgeRF<T> *src = ed + (o < n ? o : 0);
+        cp_async_zfill<(int)sizeof(EdgeRF<T>)>(ring_lane + (uint32_t)((tile & 3) * 32 * sizeof(EdgeRF<T>)), src, o < n);
+        cp_async_commit();
+    };
+    if (n > 0) {
+        stage(0);
+        stage(1);
+        stage(2);
+    }
+    pdl_wait();
+    if (*a.active == 0) {
+        cp_async_wait<0>();
+        return;
+    }
     uint32_t cmask = 0;
     if constexpr (SIDE == SIDE_V) {
 #pragma unroll
@@ -930,31 +958,13 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) k_pull_rf(PullArgs<T> a) {
 #pragma unroll
     for (int v = 0; v < VEC; v++) npt[v] = 0;
     if (gw < a.n_warps) {
-        // only what the edge loop needs stays in registers; the cut fields are read again after it
-        const int64_t e0 = a.work[gw].e0;
-        const int n = (int)(a.work[gw].e1 - e0);
         if (n > 0) {
             int32_t np[VEC];
 #pragma unroll
             for (int v = 0; v < VEC; v++) np[v] = 0;
-            const EdgeRF<T> *ed = reinterpret_cast<const EdgeRF<T> *>(a.ecv) + e0;
             const T *X = a.X + slot0;
             T *yrow = a.Y + (int64_t)a.work[gw].r0 * B + slot0;
-            EdgeRF<T> *ring = s_ring[warp];
-            // tile k (edges 32 k + lane) into ring slot k & 3; past the range the copy zero-fills
-            // (column 0, value +0: gathers row 0, adds nothing, ends no row)
-            const uint32_t ring_lane = smem_u32(ring + lane);
-            auto stage = [&](int tile) {
-                const int o = tile * 32 + lane;
-                const EdgeRF<T> *src = ed + (o < n ? o : 0);
-                cp_async_zfill<(int)sizeof(EdgeRF<T>)>(ring_lane + (uint32_t)((tile & 3) * 32 * sizeof(EdgeRF<T>)), src,
-                                                      o < n);
-                cp_async_commit();
-            };
             auto fetch = [&](int c, T(&x)[VEC]) { ldg_vec<T, VEC>(X + (int64_t)c * B, x); };
-            stage(0);
-            stage(1);
-            stage(2);
             cp_async_wait<1>();  // tiles 0 and 1 have landed
             __syncwarp();
             T xs[S][VEC];
@@ -980,7 +990,8 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) k_pull_rf(PullArgs<T> a) {
 #pragma unroll 1
                 for (int sub = 0; sub < 32; sub += S) {
                     const EdgeRF<T> *nxt = ring + ((base + sub + S) & (RING - 1));
-                    if (((tmask >> sub) & (uint32_t)((1ull << S) - 1ull)) == 0u) {
+                    const uint32_t bm = (tmask >> sub) & (uint32_t)((1ull << S) - 1ull);
+                    if (bm == 0u) {
 #pragma unroll
                         for (int t = 0; t < S; t++) {
                             if constexpr (sizeof(T) == 8) {
@@ -1005,7 +1016,7 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) k_pull_rf(PullArgs<T> a) {
 #pragma unroll
                             for (int v = 0; v < VEC; v++) accs[v] = fmaf(fabsf(w), xs[t][v], accs[v]);
                         }
-                        if (w < (T)0) {  // last edge of a row
+                        if ((bm >> t) & 1u) {  // last edge of a row (w < 0)
                             if constexpr (sizeof(T) == 4) {
 #pragma unroll
                                 for (int v = 0; v < VEC; v++) {
