@@ -161,6 +161,8 @@ struct SidePlan {
     int32_t *cut_count = nullptr;
     int32_t n_warps = 0, n_cuts = 0, n_parts = 0;
     int grid = 1;
+    int threads = PULL_THREADS;  // block size of the dense pull
+    int front_grid = 1;          // 256-thread blocks covering the same n_warps (frontier pulls)
     void free_all() {
         cudaFree(work);
         cudaFree(cuts);
@@ -343,11 +345,12 @@ struct Engine final : EngineBase {
             switch (geo) {
                 case 0: return k_pull_rf<B, T, SIDE, 8, 3>;
                 case 1: return k_pull_rf<B, T, SIDE, 8, 2>;
-                case 2: return k_pull_rf<B, T, SIDE, 4, 4>;
+                case 2: return k_pull_rf<B, T, SIDE, 8, 4, 7>;
                 default: return k_pull_rf<B, T, SIDE, 8, 4>;
             }
         }
     }
+    static int rf_warps(int geo) { return geo == 2 ? 7 : PULL_WARPS; }
     bool use_rf = false;
     int rf_geo[2] = {0, 0};
     PullFn pull_kernel(int side) const {
@@ -383,7 +386,7 @@ struct Engine final : EngineBase {
         if (const char *m = getenv("BH_PULL")) use_rf = use_rf && strcmp(m, "sw") != 0;
         if (use_rf) {
             constexpr int LB = (B / 32) * (int)sizeof(T);
-            rf_geo[0] = rf_geo[1] = LB <= 16 ? 0 : 1;  // 8 rows at 3 blocks/SM; 32-byte lanes at 2
+            rf_geo[0] = rf_geo[1] = LB <= 8 ? 2 : (LB <= 16 ? 0 : 1);  // 8-byte lanes: 4 blocks of 7 warps; 16: 3 of 8; 32: 2 of 8
             if (const char *m = getenv("BH_RF_GEO")) {  // "v,u"
                 int gv = rf_geo[0], gu = rf_geo[1];
                 const int k = sscanf(m, "%d,%d", &gv, &gu);
@@ -398,15 +401,18 @@ struct Engine final : EngineBase {
             const Side &sd = side == SIDE_V ? g->V : g->U;
             SidePlan &pl = side == SIDE_V ? plan_v : plan_u;
             PullFn fn = pull_kernel(side);
+            const int wpb = use_rf ? rf_warps(rf_geo[side]) : PULL_WARPS;
+            pl.threads = wpb * 32;
             int occ = 1;
-            BH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, PULL_THREADS, 0));
+            BH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, pl.threads, 0));
             occ = std::max(1, occ);
             // one resident wave of warps, fewer if the side is tiny
             int64_t grid = (int64_t)occ * sms;
-            const int64_t want = (g->n_e + 2 * sd.n_rows) / 64 / PULL_WARPS + 1;
+            const int64_t want = (g->n_e + 2 * sd.n_rows) / 64 / wpb + 1;
             grid = std::max<int64_t>(1, std::min(grid, want));
             pl.grid = (int)grid;
-            build_plan(sd, g->n_e, (int)grid * PULL_WARPS, pl);
+            pl.front_grid = (int)((grid * wpb + PULL_WARPS - 1) / PULL_WARPS);
+            build_plan(sd, g->n_e, (int)grid * wpb, pl);
         }
         {  // one resident wave of the elementwise kernels
             int occ_p = 1, occ_c = 1;
@@ -570,8 +576,8 @@ struct Engine final : EngineBase {
     }
 
     void launch_pull(int side, const PullArgs<T> &a, cudaStream_t st) {
-        launch_pdl_win(pull_kernel(side), side == SIDE_V ? plan_v.grid : plan_u.grid, PULL_THREADS, 0, st,
-                       side == SIDE_V ? &win_v : &win_u, a);
+        const SidePlan &pl = side == SIDE_V ? plan_v : plan_u;
+        launch_pdl_win(pull_kernel(side), pl.grid, pl.threads, 0, st, side == SIDE_V ? &win_v : &win_u, a);
     }
 
     ElemArgs<T> elem_args(const RunSpec &rs) {
@@ -648,14 +654,14 @@ struct Engine final : EngineBase {
         const FrontArgs fa = front_args();
         launch_pdl(k_front_reset, grid_front, 256, 0, st, fa);
         launch_pdl(k_front_mark<SIDE_V>, grid_front, 256, 0, st, fa);
-        launch_pdl(k_front_pull<B, T, SIDE_V>, plan_v.grid, PULL_THREADS, 0, st, front_pull_args(SIDE_V, alpha));
+        launch_pdl(k_front_pull<B, T, SIDE_V>, plan_v.front_grid, PULL_THREADS, 0, st, front_pull_args(SIDE_V, alpha));
         count_launch(3);
         stats.launches += 3;
     }
     void launch_front_u(double alpha, cudaStream_t st) {
         const FrontArgs fa = front_args();
         launch_pdl(k_front_mark<SIDE_U>, grid_front, 256, 0, st, fa);
-        launch_pdl(k_front_pull<B, T, SIDE_U>, plan_u.grid, PULL_THREADS, 0, st, front_pull_args(SIDE_U, alpha));
+        launch_pdl(k_front_pull<B, T, SIDE_U>, plan_u.front_grid, PULL_THREADS, 0, st, front_pull_args(SIDE_U, alpha));
         PullArgs<T> pu = pull_args(SIDE_U, alpha);
         pu.active = &front->gate_udense;
         launch_pull(SIDE_U, pu, st);

@@ -332,8 +332,9 @@ __global__ void __launch_bounds__(PULL_THREADS) k_front_pull(FrontPullArgs<T> a)
     if (*a.active == 0 || !(SIDE == SIDE_V ? f->gate_front : f->gate_ufront)) return;
     const int lane = threadIdx.x & 31;
     const int gw = blockIdx.x * PULL_WARPS + (threadIdx.x >> 5);
-    const int nw = gridDim.x * PULL_WARPS;
-    const int n_items = SIDE == SIDE_V ? f->n_items_v : f->n_items_u;
+    // the grid covers the dense plan's n_warps n_p rows; warps past them take no item
+    const int nw = gridDim.x * PULL_WARPS < a.n_warps ? gridDim.x * PULL_WARPS : a.n_warps;
+    const int n_items = gw < nw ? (SIDE == SIDE_V ? f->n_items_v : f->n_items_u) : 0;
     constexpr bool WIDE = B >= 32;
     constexpr int VEC = WIDE ? B / 32 : 1;
     constexpr int G = WIDE ? 32 : B, EPW = WIDE ? 1 : 32 / B;

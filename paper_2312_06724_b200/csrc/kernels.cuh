@@ -905,19 +905,20 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) k_pull_sw(PullArgs<T> a) {
 //     test on a register that is loaded anyway: no row-pointer ring, no per-edge
 //     offset compare, no reload of row ends;
 //   - S (a divisor of 32) operand rows are in flight per warp in registers; the
-//     S-edge body is unrolled, the bodies of a tile are a loop;
+//     S-edge body is unrolled, the bodies of a tile are a loop; WARPS warps per
+//     block (7 lets four blocks of 72-register threads share an SM);
 //   - fp32: products accumulate in fp32 over one S-edge body at most and are
 //     folded into the row's fp64 accumulator after it (and at a row end).
-template <int B, typename T, int SIDE, int S, int MINB>
-__global__ void __launch_bounds__(PULL_THREADS, MINB) k_pull_rf(PullArgs<T> a) {
+template <int B, typename T, int SIDE, int S, int MINB, int WARPS = PULL_WARPS>
+__global__ void __launch_bounds__(WARPS * 32, MINB) k_pull_rf(PullArgs<T> a) {
     pdl_launch_dependents();
     constexpr int VEC = RegPipe<B, T>::VEC;
     constexpr int RING = 128;  // four 32-edge tiles
     static_assert(32 % S == 0, "the S-edge body must tile a 32-edge window");
-    __shared__ EdgeRF<T> s_ring[PULL_WARPS][RING];
+    __shared__ EdgeRF<T> s_ring[WARPS][RING];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int gw = blockIdx.x * PULL_WARPS + warp;
+    const int gw = blockIdx.x * WARPS + warp;
     const int slot0 = lane * VEC;
     // The plan and the edge stream are immutable graph data: the first three edge tiles are
     // put in flight under the predecessor's tail, before the wait for its memory.
