@@ -475,7 +475,7 @@ def roofline_block(g, prof, pms, steps, s_bytes, alg, peak, peak_src, traffic_na
     return {
         "bound": "hbm", "achieved": v_ach, "peak": peak, "unit": "GB/s",
         "frac": v_ach / peak if v_ach else None, "traffic": vp_t,
-        "kernel": "K2 V pull (k_pull_sw / k_pull_small, SIDE_V), the dominant kernel",
+        "kernel": "K2 V pull (k_pull_rf / k_pull_small, SIDE_V), the dominant kernel",
         "algorithmic_bytes_per_launch": v_bytes,
         "algorithmic_model": "E(i+s) + (|V|+1) o + B s (|U| + |V|), i = o = 4 (SURVEY 8(d), one SpMM half)",
         "launch_us": v_us, "launches": int(prof["rounds"]),

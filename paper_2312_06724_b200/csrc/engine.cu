@@ -302,41 +302,20 @@ struct Engine final : EngineBase {
         else return k_combine<B, T, 2, 2>;
     }
 
-    // Pull geometry per side and lane width (rows in flight per warp, 256-thread
-    // blocks per SM), measured at c2 / c5 on B200 (profiles/r01_pull_variants.md,
-    // profiles/r02_pull_geometry.md):
-    //   64 fp32 slots (8-byte lanes): V 7 at 4, U 7 at 4
-    //   64 fp64 slots (16-byte lanes): V 6 at 3, U 5 at 4
-    //   128 fp32 slots (16-byte lanes): V 10 at 2, U 8 at 3
-    //   otherwise SwPipe's defaults (U side at 4 blocks/SM when the default is 3)
+    // Dense pulls.  B < 32: k_pull_small.  B >= 32: the row-flag pull k_pull_rf on the
+    // store's flagged edge stream; k_pull_sw (row-pointer walk, SwPipe's default geometry)
+    // serves stores without that stream (a caller's graph with an empty row) and BH_PULL=sw.
     using PullFn = void (*)(PullArgs<T>);
     template <int SIDE>
     static PullFn sw_kernel() {
-        if constexpr (!WIDE) {
-            return k_pull_small<B, T, SIDE>;
-        } else {
-            // (rows in flight per warp, 256-thread blocks per SM) per side and lane width,
-            // swept on one box in round 2 (profiles/r02_pull_geometry.md)
-            constexpr int LB = SwPipe<B, T>::LANE_BYTES;
-            if constexpr (sizeof(T) == 8 && B == 64) {  // 16-byte fp64 lanes (c2 fp64)
-                if constexpr (SIDE == SIDE_V) return k_pull_sw<B, T, SIDE_V, 6, 3>;
-                else return k_pull_sw<B, T, SIDE_U, 5, 4>;
-            }
-            if constexpr (LB == 8) {  // 64 fp32 slots (c2)
-                if constexpr (SIDE == SIDE_V) return k_pull_sw<B, T, SIDE_V, 7, 4>;
-                else return k_pull_sw<B, T, SIDE_U, 7, 4>;
-            }
-            if constexpr (LB == 16 && sizeof(T) == 4) {  // 128 fp32 slots (c3, c4, c5)
-                if constexpr (SIDE == SIDE_V) return k_pull_sw<B, T, SIDE_V, 10, 2>;
-                else return k_pull_sw<B, T, SIDE_U, 8, 3>;
-            }
-            if constexpr (SIDE == SIDE_U && SwPipe<B, T>::MINB == 3) return k_pull_sw<B, T, SIDE_U, SwPipe<B, T>::S, 4>;
-            return k_pull_sw<B, T, SIDE>;
-        }
+        if constexpr (!WIDE) return k_pull_small<B, T, SIDE>;
+        else return k_pull_sw<B, T, SIDE>;
     }
-    // Row-flag pull geometries (rows in flight per warp, 256-thread blocks per SM);
-    // BH_RF_GEO="v,u" picks one per side for A/B runs.
-    static constexpr int RF_GEOS = 4;
+    // Row-flag pull geometries, measured on one B200 (profiles/r02_rf_pull.md): 8 rows in
+    // flight per warp; 8-byte lanes (64 fp32 slots) run four blocks of 7 warps per SM (72
+    // registers), 16-byte lanes three blocks of 8 (80), 32-byte lanes two blocks of 8.
+    // BH_RF_GEO="v,u" overrides per side for A/B runs.
+    static constexpr int RF_GEOS = 3;
     template <int SIDE>
     static PullFn rf_kernel(int geo) {
         if constexpr (!WIDE) {
@@ -345,8 +324,7 @@ struct Engine final : EngineBase {
             switch (geo) {
                 case 0: return k_pull_rf<B, T, SIDE, 8, 3>;
                 case 1: return k_pull_rf<B, T, SIDE, 8, 2>;
-                case 2: return k_pull_rf<B, T, SIDE, 8, 4, 7>;
-                default: return k_pull_rf<B, T, SIDE, 8, 4>;
+                default: return k_pull_rf<B, T, SIDE, 8, 4, 7>;
             }
         }
     }

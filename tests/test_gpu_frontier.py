@@ -137,3 +137,36 @@ def test_frontier_rounds_are_deterministic(monkeypatch):
     b = bh.bhpp_query_batch(g, meta, srcs, 1e-7, k=50, dtype="fp32", return_scores=True, slots=16)
     np.testing.assert_array_equal(a.scores, b.scores)
     assert a.traces.tobytes() == b.traces.tobytes()
+
+
+@pytest.mark.parametrize("name", ["c2s", "c4s"])
+def test_row_pointer_pull_fallback(name, monkeypatch):
+    """The dense pull that walks row pointers (k_pull_sw) serves device stores
+    without the flagged edge stream; BH_PULL=sw selects it when an engine is
+    built.  A fresh graph object (so a fresh store and engines) must meet the
+    same bar against the golden fixtures as the default row-flag pull, and the
+    two pulls must agree on the fp64 scores to summation-order noise."""
+    from golden_io import _CFG
+    from paper_2312_06724_b200.synth import make_graph
+
+    d = load(name)
+    g_rf = config_graph(name)
+    monkeypatch.setenv("BH_PULL", "sw")
+    g = graph_from(d) if "eu" in d else make_graph(_CFG[name])  # not the cached object: new store, new engines
+    assert g.fingerprint == str(d["fingerprint"])
+    alpha = _CFG[name].alpha
+    meta = bh.build_index_meta(g, alpha)
+    n = min(len(d["sources"]), 6)
+    srcs = d["sources"][:n]
+    ties = np.array([tie_skip_from(t) for t in d["ties"][:n]], dtype=np.int32)
+    k, eps = int(d["k"]), float(d["eps"])
+    r_sw = bh.bhpp_query_batch(g, meta, srcs, eps, k=k, dtype="fp64", return_scores=True, tie_skip=ties, slots=64)
+    monkeypatch.delenv("BH_PULL")
+    meta_rf = bh.build_index_meta(g_rf, alpha)
+    r_rf = bh.bhpp_query_batch(g_rf, meta_rf, srcs, eps, k=k, dtype="fp64", return_scores=True, tie_skip=ties,
+                               slots=64)
+    for i in range(n):
+        np.testing.assert_allclose(r_sw.scores[i], d["scores"][i], atol=ATOL64, rtol=0)
+        np.testing.assert_allclose(r_sw.scores[i], r_rf.scores[i], atol=1e-13, rtol=0)
+        back, fwd, gamma = split_traces(d["traces"][i])
+        assert_traces(r_sw.traces[i], back, fwd, gamma)

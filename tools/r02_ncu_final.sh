@@ -7,7 +7,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 BH_NO_GRAPH=1 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2_launches_bench.csv \
   python bench.py --steps 2 --warmup 1 --no-cpu --no-fp64 --no-c3 > gpurun_out/r2_ncu_bench.log 2>&1; tail -1 gpurun_out/r2_ncu_bench.log
 BH_NO_GRAPH=1 timeout 900 ncu --set full --import-source on --clock-control none --profile-from-start off \
-  -k regex:"k_push|k_pull_sw|k_combine|k_control" --launch-skip 240 --launch-count 5 -o gpurun_out/r2_ncu_c2_round -f \
+  -k regex:"k_push|k_pull_rf|k_combine|k_control" --launch-skip 240 --launch-count 5 -o gpurun_out/r2_ncu_c2_round -f \
   python tools/prof_step.py --config c2 > gpurun_out/r2_ncu_c2.log 2>&1; tail -1 gpurun_out/r2_ncu_c2.log
 timeout 600 ncu --set full --import-source on --clock-control none --profile-from-start off -k regex:"k_small_query" \
   --launch-count 1 -o gpurun_out/r2_ncu_small -f python tools/small_phases.py > gpurun_out/r2_ncu_small.log 2>&1; tail -1 gpurun_out/r2_ncu_small.log

@@ -1,0 +1,11 @@
+# 128-slot (16-byte lane) geometry A/B on a c5-like proxy: the c2 graph, 1024 sources through 128 slots
+one() {  # label, bench args, env...
+  label=$1; shift; args=$1; shift
+  env "$@" python bench.py --no-cpu --no-fp64 --no-c3 $args > gpurun_out/bench_l.json 2>gpurun_out/bench_l.err || { echo "$label FAILED"; tail -3 gpurun_out/bench_l.err; return; }
+  python -c "
+import json; d=json.load(open('gpurun_out/bench_l.json')); r=d['roofline']
+print('$label', round(d['value'],1), {k: round(v,3) for k,v in r['breakdown_ms_per_step'].items()}, r['timed_step_ms'][:3], 'slots', d['config'].get('slots'))"
+}
+for g in "$@"; do
+  one "c2x1024/128 geo $g" "--steps 3 --warmup 2 --scaling strong --batch 1024 --slots 128" BH_RF_GEO=$g
+done
