@@ -174,7 +174,8 @@ struct SidePlan {
 };
 
 static void build_plan(const Side &sd, int64_t n_e, int n_warps, SidePlan &pl) {
-    constexpr int64_t ROWCOST = 2;
+    int64_t ROWCOST = 2;
+    if (const char *m = getenv("BH_ROWCOST")) ROWCOST = std::max(0, atoi(m));  // A/B switch
     const std::vector<int64_t> &ip = sd.h_indptr;
     const int64_t n = sd.n_rows;
     const int64_t total = n_e + ROWCOST * n;

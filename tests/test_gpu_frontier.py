@@ -169,4 +169,4 @@ def test_row_pointer_pull_fallback(name, monkeypatch):
         np.testing.assert_allclose(r_sw.scores[i], d["scores"][i], atol=ATOL64, rtol=0)
         np.testing.assert_allclose(r_sw.scores[i], r_rf.scores[i], atol=1e-13, rtol=0)
         back, fwd, gamma = split_traces(d["traces"][i])
-        assert_traces(r_sw.traces[i], back, fwd, gamma)
+        assert_traces(r_sw.trace_dicts(i), back, fwd, gamma)
