@@ -173,9 +173,8 @@ struct SidePlan {
     }
 };
 
-static void build_plan(const Side &sd, int64_t n_e, int n_warps, SidePlan &pl) {
-    int64_t ROWCOST = 2;
-    if (const char *m = getenv("BH_ROWCOST")) ROWCOST = std::max(0, atoi(m));  // A/B switch
+static void build_plan(const Side &sd, int64_t n_e, int n_warps, SidePlan &pl, int64_t row_cost) {
+    const int64_t ROWCOST = row_cost;
     const std::vector<int64_t> &ip = sd.h_indptr;
     const int64_t n = sd.n_rows;
     const int64_t total = n_e + ROWCOST * n;
@@ -391,7 +390,10 @@ struct Engine final : EngineBase {
             grid = std::max<int64_t>(1, std::min(grid, want));
             pl.grid = (int)grid;
             pl.front_grid = (int)((grid * wpb + PULL_WARPS - 1) / PULL_WARPS);
-            build_plan(sd, g->n_e, (int)grid * wpb, pl);
+            // cost of a row in edges: a V-pull emit also counts n_p (measured at c2, rows of 10 / 20
+            // edges, profiles/r02_rf_pull.md: V 2 -> 3 gains 1.3 %, U 2 -> 1 gains 2 %; 0 and >= 4
+            // lose 4-30 %)
+            build_plan(sd, g->n_e, (int)grid * wpb, pl, use_rf ? (side == SIDE_V ? 3 : 1) : 2);
         }
         {  // one resident wave of the elementwise kernels
             int occ_p = 1, occ_c = 1;
