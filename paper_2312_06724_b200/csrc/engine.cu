@@ -287,7 +287,7 @@ struct Engine final : EngineBase {
     // per thread at 4 blocks/SM, K1a software-pipelined at 3 blocks/SM; fp64 two
     // nodes per thread at 2 blocks/SM.  The same geometry is at least as fast in
     // the HBM regime (c3: 4-8 nodes per thread measured equal or slower,
-    // profiles/r02_elem_geometry.md), so there is one geometry per dtype.
+    // profiles/r02_store_ab.md), so there is one geometry per dtype.
     using ElemFn = void (*)(ElemArgs<T>);
     ElemFn push_kernel() const {
         if (front_on) {
@@ -469,7 +469,7 @@ struct Engine final : EngineBase {
         const double row = (double)B * sizeof(T);
         const double operands = row * (double)(nu + nv);
         // Off by default: at c3 the carve-out slowed K1 / K1a by 35 % and gained
-        // the pulls 2-5 %, a net loss (profiles/r02_c3_store_ab.md); opt-in with
+        // the pulls 2-5 %, a net loss (profiles/r02_store_ab.md); opt-in with
         // BH_L2_PERSIST_MB (a carve-out of that size, shared by the two windows)
         double mb = 0.0;
         (void)operands;
