@@ -29,7 +29,7 @@ __global__ void k_build_rows(int64_t n_rows, const int64_t *__restrict__ old_ind
                              const double *__restrict__ w, const double *__restrict__ ws_old,
                              const int32_t *__restrict__ perm, const int32_t *__restrict__ inv_col,
                              const int64_t *__restrict__ new_indptr, int32_t *__restrict__ new_idx,
-                             T *__restrict__ vals, EdgeRF<T> *__restrict__ ecv) {
+                             T *__restrict__ vals, EdgeRF<T> *__restrict__ ecv, int32_t *__restrict__ bad) {
     const int lane = threadIdx.x & 31;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < n_rows; i += nw) {
@@ -43,6 +43,7 @@ __global__ void k_build_rows(int64_t n_rows, const int64_t *__restrict__ old_ind
             new_idx[n + k] = c;
             vals[n + k] = v;
             if (ecv) ecv[n + k] = EdgeRF<T>{c, k == deg - 1 ? -v : v};
+            if (!(v > (T)0)) atomicOr(bad, 1);  // the sign carries the row end: needs v > 0
         }
     }
 }
@@ -104,9 +105,14 @@ void upload_side(Side &s, int64_t n_rows, int64_t n_e, const int64_t *indptr, co
     s.indices = dmalloc<int32_t>(n_e, acc);
     s.vals = dmalloc<T>(n_e, acc);
     s.deg = dmalloc<int32_t>(n_rows, acc);
+    // the dense pulls' flagged edge stream needs every row non-empty (validated) and every
+    // prescaled value positive in T (checked on the device below); otherwise the row-pointer
+    // pull serves this store
     bool no_empty_row = true;
     for (int64_t i = 0; i < n_rows && no_empty_row; i++) no_empty_row = indptr[i + 1] > indptr[i];
-    s.ecv = no_empty_row ? (void *)dmalloc<EdgeRF<T>>(n_e, acc) : nullptr;
+    int64_t ecv_bytes = 0;
+    s.ecv = no_empty_row ? (void *)dmalloc<EdgeRF<T>>(n_e, ecv_bytes) : nullptr;
+    acc += ecv_bytes;
     std::vector<int64_t> nip;
     const int64_t *new_ip = indptr;
     if (!perm.empty()) {
@@ -127,19 +133,29 @@ void upload_side(Side &s, int64_t n_rows, int64_t n_e, const int64_t *indptr, co
     double *dw = dmalloc<double>(n_e, tmp);
     double *dws = dmalloc<double>(n_rows, tmp);
     int32_t *d_invc = inv_col.empty() ? nullptr : dmalloc<int32_t>(inv_col.size(), tmp);
+    int32_t *d_bad = dmalloc<int32_t>(1, tmp);
+    BH_CUDA(cudaMemset(d_bad, 0, sizeof(int32_t)));
     BH_CUDA(cudaMemcpy(d_oip, indptr, (n_rows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
     BH_CUDA(cudaMemcpy(d_oidx, indices, n_e * sizeof(int32_t), cudaMemcpyHostToDevice));
     BH_CUDA(cudaMemcpy(dw, w, n_e * sizeof(double), cudaMemcpyHostToDevice));
     BH_CUDA(cudaMemcpy(dws, ws_rows, n_rows * sizeof(double), cudaMemcpyHostToDevice));
     if (d_invc) BH_CUDA(cudaMemcpy(d_invc, inv_col.data(), inv_col.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     k_build_rows<T><<<grid_for(n_rows * 32), 256>>>(n_rows, d_oip, d_oidx, dw, dws, s.perm, d_invc, s.indptr,
-                                                     s.indices, (T *)s.vals, (EdgeRF<T> *)s.ecv);
+                                                     s.indices, (T *)s.vals, (EdgeRF<T> *)s.ecv, d_bad);
     count_launch();
     BH_CUDA(cudaGetLastError());
     k_deg<<<grid_for(n_rows), 256>>>(n_rows, s.indptr, s.deg);
     count_launch();
     BH_CUDA(cudaGetLastError());
     BH_CUDA(cudaDeviceSynchronize());
+    int32_t bad = 0;
+    BH_CUDA(cudaMemcpy(&bad, d_bad, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    if (bad && s.ecv) {  // a zero, negative or underflowed value: no flagged stream
+        cudaFree(s.ecv);
+        s.ecv = nullptr;
+        acc -= ecv_bytes;
+    }
+    cudaFree(d_bad);
     cudaFree(d_oip);
     cudaFree(d_oidx);
     cudaFree(dw);

@@ -170,3 +170,27 @@ def test_row_pointer_pull_fallback(name, monkeypatch):
         np.testing.assert_allclose(r_sw.scores[i], r_rf.scores[i], atol=1e-13, rtol=0)
         back, fwd, gamma = split_traces(d["traces"][i])
         assert_traces(r_sw.trace_dicts(i), back, fwd, gamma)
+
+
+def test_value_underflow_falls_back_to_row_pointer_pull():
+    """The row-flag pull reads a row's end from the sign of the edge value, so the store
+    builds its flagged edge stream only when every prescaled value is positive in the store's
+    type.  A weight that underflows to zero in fp32 (1e-60 against sums of order 10) must make
+    the fp32 store fall back to the row-pointer pull; fp64 keeps the flagged stream.  Both must
+    agree with each other like any fp32 / fp64 pair."""
+    d = load("c2s")
+    g0 = config_graph("c2s")
+    eu = np.repeat(np.arange(g0.u_count), np.diff(g0.u_indptr))
+    ew = np.array(g0.u_weights, dtype=np.float64)
+    ew[::97] = 1e-60  # many rows end in, start with or contain an underflowing value
+    g = bh.BipartiteGraph.from_arrays(g0.u_count, g0.v_count, eu, np.array(g0.u_indices), ew)
+    meta = bh.build_index_meta(g, 0.15)
+    srcs = d["sources"][:6]
+    k, eps = int(d["k"]), float(d["eps"])
+    r64 = bh.bhpp_query_batch(g, meta, srcs, eps, k=k, dtype="fp64", return_scores=True, slots=64)
+    r32 = bh.bhpp_query_batch(g, meta, srcs, eps, k=k, dtype="fp32", slots=64)
+    for i in range(len(srcs)):
+        assert np.isfinite(r64.scores[i]).all()
+        ref = r64.scores[i]
+        np.testing.assert_allclose(r32.topk_score[i], ref[r32.topk_index[i]], rtol=RTOL32, atol=eps)
+        topk_equal_up_to_ties(r32.topk_index[i], r32.topk_score[i], r64.topk_index[i], ref, RTOL32, eps)
