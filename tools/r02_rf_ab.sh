@@ -7,5 +7,4 @@ import json; d=json.load(open('gpurun_out/bench_l.json')); r=d['roofline']
 print('$label', round(d['value'],1), {k: round(v,3) for k,v in r['breakdown_ms_per_step'].items()}, r['timed_step_ms'][:3], 'frac', round(r['frac'],3))"
 }
 one sw BH_PULL=sw
-[ -f tools/_build/libbhpp_rf1.so ] && one rf1_84 BH_LIBBHPP=tools/_build/libbhpp_rf1.so BH_RF_GEO=0,0
-for g in 0 1 2 3; do one rf_g$g BH_RF_GEO=$g,$g; done
+for g in 0 1 2; do one rf_g$g BH_RF_GEO=$g,$g; done
