@@ -131,3 +131,32 @@ def test_degenerate_graphs_one_sided(name):
             one = bh.bhpp_query(g, meta, q, eps, tie_skip=O.tie_skip_for(ref_tr["forward"]))
             np.testing.assert_allclose(one.scores, ref_scores, atol=1e-12, rtol=0, err_msg=f"{name} {eps} {q}")
             assert one.phase_trace["backward"] == ref_tr["backward"], (name, eps, q)
+
+
+@pytest.mark.parametrize("slots", [32, 64, 128])
+def test_wide_engine_on_tiny_graphs(slots, monkeypatch):
+    """The wide slot engine (row-flag pulls, 32+ slots) on graphs smaller than one warp range
+    or one 32-edge tile: a single U node, stars, a path, and a handful of random graphs, with
+    the small-graph path switched off.  One-sided against the dense solve like criterion 1."""
+    monkeypatch.setenv("BH_NO_SMALL", "1")
+    graphs = [
+        _graph(1, 3, [(0, 0), (0, 1), (0, 2)], [1.0, 2.0, 3.0]),
+        _graph(9, 8, [(0, j) for j in range(8)] + [(1 + j, j) for j in range(8)]),
+        _graph(8, 9, [(i, 0) for i in range(8)] + [(i, 1 + i) for i in range(8)]),
+        _graph(8, 7, [(i, i) for i in range(7)] + [(i + 1, i) for i in range(7)]),
+    ]
+    rng = substream(2027, "wide-tiny")
+    for _ in range(6):
+        nu, nv = (int(x) for x in rng.integers(3, 80, size=2))
+        graphs.append(random_bigraph(rng, nu, nv, float(rng.uniform(0.5, 3.0)), 10.0))
+    for gi, g in enumerate(graphs):
+        Pi = dense_pi(g)
+        meta = bh.build_index_meta(g, ALPHA)
+        srcs = np.arange(g.u_count)
+        for eps in (1e-2, 1e-7):
+            for dtype, tol in (("fp64", 1e-10), ("fp32", 1e-5)):
+                res = bh.bhpp_query_batch(g, meta, srcs, eps, k=min(3, g.u_count), dtype=dtype, return_scores=True,
+                                          slots=slots)
+                for j, q in enumerate(srcs):
+                    diff = (Pi[q, :] + Pi[:, q]) - res.scores[j]
+                    assert diff.min() >= -tol and diff.max() <= eps + tol, (gi, slots, eps, dtype, int(q), diff)

@@ -194,3 +194,29 @@ def test_value_underflow_falls_back_to_row_pointer_pull():
         ref = r64.scores[i]
         np.testing.assert_allclose(r32.topk_score[i], ref[r32.topk_index[i]], rtol=RTOL32, atol=eps)
         topk_equal_up_to_ties(r32.topk_index[i], r32.topk_score[i], r64.topk_index[i], ref, RTOL32, eps)
+
+
+@pytest.mark.parametrize("geo", ["0", "1", "2"])
+def test_row_flag_pull_geometries(geo, monkeypatch):
+    """Every compiled geometry of the row-flag pull (BH_RF_GEO: 8 rows in flight at 3 or 2 blocks of
+    8 warps, or 4 blocks of 7 warps per SM; the defaults pick one per lane width) meets the golden
+    bar on c4 at 1/100 scale (hub rows cut across warps) in fp64 and fp32."""
+    from golden_io import _CFG
+    from paper_2312_06724_b200.synth import make_graph
+
+    monkeypatch.setenv("BH_RF_GEO", geo)
+    d = load("c4s")
+    g = graph_from(d) if "eu" in d else make_graph(_CFG["c4s"])  # fresh store and engines
+    meta = bh.build_index_meta(g, _CFG["c4s"].alpha)
+    srcs = d["sources"]
+    ties = np.array([tie_skip_from(t) for t in d["ties"]], dtype=np.int32)
+    k, eps = int(d["k"]), float(d["eps"])
+    r64 = bh.bhpp_query_batch(g, meta, srcs, eps, k=k, dtype="fp64", return_scores=True, tie_skip=ties, slots=64)
+    r32 = bh.bhpp_query_batch(g, meta, srcs, eps, k=k, dtype="fp32", tie_skip=ties, slots=64)
+    for i in range(len(srcs)):
+        np.testing.assert_allclose(r64.scores[i], d["scores"][i], atol=ATOL64, rtol=0)
+        back, fwd, gamma = split_traces(d["traces"][i])
+        assert_traces(r64.trace_dicts(i), back, fwd, gamma)
+        ref, exp = d["scores"][i], d["topk"][i]
+        np.testing.assert_allclose(r32.topk_score[i], ref[exp], rtol=RTOL32, atol=eps)
+        topk_equal_up_to_ties(r32.topk_index[i], r32.topk_score[i], exp, ref, RTOL32, eps)
