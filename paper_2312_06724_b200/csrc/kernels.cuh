@@ -907,6 +907,9 @@ __global__ void __launch_bounds__(PULL_THREADS, MINB) k_pull_sw(PullArgs<T> a) {
 //   - S (a divisor of 32) operand rows are in flight per warp in registers; the
 //     S-edge body is unrolled, the bodies of a tile are a loop; WARPS warps per
 //     block (7 lets four blocks of 72-register threads share an SM);
+//   - one ballot per tile turns the value signs into a bitmask: a body without a
+//     row end runs branch-free, a body with one tests the mask bit per edge and
+//     emits inline (fp64 fold, scale, store, n_p);
 //   - fp32: products accumulate in fp32 over one S-edge body at most and are
 //     folded into the row's fp64 accumulator after it (and at a row end).
 template <int B, typename T, int SIDE, int S, int MINB, int WARPS = PULL_WARPS>
